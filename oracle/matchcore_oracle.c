@@ -27,17 +27,24 @@
 #include <stdlib.h>
 #include <string.h>
 
+/* Exact residue product.  The reference's compiled kernel requires
+ * m < 2^31 (u64 products, matching.py:39-41, :110-113); beyond that its
+ * pure backend is arbitrary precision, restated here with 128-bit products. */
+static inline uint64_t mulmod(uint64_t a, uint64_t b, uint64_t m) {
+    return (uint64_t)(((unsigned __int128)a * b) % m);
+}
+
 int64_t oracle_window_hashes(const int64_t *tok, int64_t n, int32_t w,
                              uint64_t b, uint64_t m, uint64_t *out) {
     if (n < w) return 0;
     uint64_t bw = 1;
-    for (int32_t i = 0; i < w - 1; ++i) bw = (bw * b) % m;
+    for (int32_t i = 0; i < w - 1; ++i) bw = mulmod(bw, b, m);
     uint64_t h = 0;
-    for (int32_t i = 0; i < w; ++i) h = (h * b + ((uint64_t)tok[i]) % m) % m;
+    for (int32_t i = 0; i < w; ++i) h = (mulmod(h, b, m) + ((uint64_t)tok[i]) % m) % m;
     out[0] = h;
     for (int64_t i = 1; i < n - w + 1; ++i) {
-        uint64_t drop = (((uint64_t)tok[i - 1]) % m) * bw % m;
-        h = ((h + m - drop) % m * b + ((uint64_t)tok[i + w - 1]) % m) % m;
+        uint64_t drop = mulmod(((uint64_t)tok[i - 1]) % m, bw, m);
+        h = (mulmod((h + m - drop) % m, b, m) + ((uint64_t)tok[i + w - 1]) % m) % m;
         out[i] = h;
     }
     return n - w + 1;

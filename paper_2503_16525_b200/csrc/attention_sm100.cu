@@ -1,0 +1,591 @@
+// A1 selective-recompute attention and D1 DHD-alpha on sm_100a tensor cores.
+//
+// A1 (reference attention_forward inside _forward, model.py:110-129, 201, on
+// the rows S a partial prefill computes - SURVEY.md A12): each CTA owns 128
+// query rows of one head (scattered, ascending positions of one request) and
+// streams that request's K/V pages from the paged arena with TMA
+// (SWIZZLE_128B).  S = Q.K^T and O += P.V run as tcgen05.mma (M=128, N=128,
+// K=16 steps) with S double-buffered and O resident in TMEM; 4 softmax warps
+// (one query row per thread) apply the position-causal mask, an online
+// softmax with lazy (threshold 2^8) O rescaling, and write P to shared
+// memory in the canonical K-major SW128 layout.  Warp 4 = TMA producer,
+// warp 5 = MMA issuer.
+//
+// D1 (reference v_impact_scores alpha, deviation.py:108-110): pass 1 is the
+// same kernel without P.V (row log-sum-exp only); pass 2 swaps the operands -
+// S^T = K_tile . Q_j^T with one KEY per TMEM lane - so the causal column sum
+// sum_j exp(s_ji - lse_j) is a per-thread row reduction with no cross-thread
+// traffic and no P store.
+#include "common.cuh"
+
+namespace kvs {
+namespace attn {
+
+constexpr int BM = 128, BN = 128, HD = 128;
+constexpr int HALF_BYTES = 128 * 128;      // one [128 rows x 64 bf16] SW128 half tile
+constexpr int TILE_BYTES = 2 * HALF_BYTES; // [128 rows x 128 bf16]
+constexpr int NS = 2;                      // K/V stages
+constexpr int kThreads = 192;
+constexpr float kRescaleThreshold = 8.f;   // lazy rescale when max grows by > 2^8
+
+struct Smem {
+    uint64_t q_full;
+    uint64_t k_full[NS], k_empty[NS], v_full[NS], v_empty[NS];
+    uint64_t s_full[2], s_empty[2], p_full[2], pv_done[2];
+    uint32_t tmem_base;
+};
+
+struct Params {
+    const int32_t *row_pos;
+    const int32_t *tile_req, *tile_row0, *tile_rows;
+    const int32_t *kv_len;
+    const int32_t *block_table;
+    int32_t max_pages, page_size, num_layers, layer, num_heads, kv_heads, causal;
+    float scale_log2;
+    __nv_bfloat16 *out;
+    float *lse;
+    int64_t n_rows;
+};
+
+__device__ __forceinline__ uint32_t align1024(uint32_t a) { return (a + 1023u) & ~1023u; }
+
+template <bool kPV>
+__global__ void __launch_bounds__(kThreads, 1)
+    fwd_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
+               Params p) {
+    extern __shared__ uint8_t dsmem[];
+    __shared__ Smem sh;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tile = blockIdx.x, h = blockIdx.y;
+    const int g = h / (p.num_heads / p.kv_heads);
+    const int req = p.tile_req[tile], row0 = p.tile_row0[tile], nrows = p.tile_rows[tile];
+    const int kmax = p.causal ? p.row_pos[row0 + nrows - 1] + 1 : p.kv_len[req];
+    const int n_kb = (kmax + BN - 1) / BN;
+    const int pages_needed = (kmax + p.page_size - 1) / p.page_size;
+
+    const uint32_t base = align1024(smem_u32(dsmem));
+    const uint32_t sQ = base;
+    const uint32_t sK = sQ + TILE_BYTES;
+    const uint32_t sV = sK + NS * TILE_BYTES;
+    const uint32_t sP = sV + (kPV ? NS * TILE_BYTES : 0);
+    uint8_t *gbase = dsmem + (base - smem_u32(dsmem));
+    uint8_t *pP = gbase + (sP - base);
+
+    if (threadIdx.x == 0) {
+        mbar_init(&sh.q_full, 1);
+        for (int i = 0; i < NS; ++i) {
+            mbar_init(&sh.k_full[i], 1);
+            mbar_init(&sh.k_empty[i], 1);
+            mbar_init(&sh.v_full[i], 1);
+            mbar_init(&sh.v_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&sh.s_full[i], 1);
+            mbar_init(&sh.s_empty[i], 128);
+            mbar_init(&sh.p_full[i], 128);
+            mbar_init(&sh.pv_done[i], 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 5) tmem_alloc(&sh.tmem_base, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sh.tmem_base;
+    const uint32_t tS[2] = {tmem, tmem + 128};
+    const uint32_t tO = tmem + 256;
+
+    if (warp == 4) {
+        // ------------------------------------------------------------ TMA producer
+        if (lane == 0) {
+            tma_prefetch(&map_q);
+            tma_prefetch(&map_kv);
+            mbar_expect_tx(&sh.q_full, TILE_BYTES);
+            for (int hf = 0; hf < 2; ++hf)
+                tma_load_3d(gbase + (sQ - base) + hf * HALF_BYTES, &map_q, &sh.q_full, hf * 64, h,
+                            row0);
+            const int32_t *bt = p.block_table + (int64_t)req * p.max_pages;
+            for (int kb = 0; kb < n_kb; ++kb) {
+                const int st = kb % NS;
+                const uint32_t ph = (uint32_t)((kb / NS) - 1) & 1u;
+                int pg[2];
+                for (int q = 0; q < 2; ++q) {
+                    const int pi = 2 * kb + q;
+                    pg[q] = bt[pi < pages_needed ? pi : 2 * kb];
+                }
+                if (kb >= NS) mbar_wait(&sh.k_empty[st], ph);
+                mbar_expect_tx(&sh.k_full[st], TILE_BYTES);
+                for (int q = 0; q < 2; ++q)
+                    for (int hf = 0; hf < 2; ++hf)
+                        tma_load_4d(gbase + (sK - base) + st * TILE_BYTES + hf * HALF_BYTES +
+                                        q * (HALF_BYTES / 2),
+                                    &map_kv, &sh.k_full[st], hf * 64, g, 0,
+                                    (pg[q] * p.num_layers + p.layer) * 2 + 0);
+                if (kPV) {
+                    if (kb >= NS) mbar_wait(&sh.v_empty[st], ph);
+                    mbar_expect_tx(&sh.v_full[st], TILE_BYTES);
+                    for (int q = 0; q < 2; ++q)
+                        for (int hf = 0; hf < 2; ++hf)
+                            tma_load_4d(gbase + (sV - base) + st * TILE_BYTES + hf * HALF_BYTES +
+                                            q * (HALF_BYTES / 2),
+                                        &map_kv, &sh.v_full[st], hf * 64, g, 0,
+                                        (pg[q] * p.num_layers + p.layer) * 2 + 1);
+                }
+            }
+        }
+    } else if (warp == 5) {
+        // ------------------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            const uint32_t idesc_qk = umma_idesc_bf16(BM, BN, false);
+            const uint32_t idesc_pv = umma_idesc_bf16(BM, HD, true);
+            mbar_wait(&sh.q_full, 0);
+            auto issue_pv = [&](int j) {
+                const int b = j & 1, st = j % NS;
+                mbar_wait(&sh.p_full[b], (uint32_t)(j >> 1) & 1u);
+                mbar_wait(&sh.v_full[st], (uint32_t)(j / NS) & 1u);
+                tc_fence_after();
+#pragma unroll
+                for (int k = 0; k < BN / 16; ++k) {
+                    const uint64_t da = umma_desc_sw128(sP + b * TILE_BYTES + (k >> 2) * HALF_BYTES +
+                                                            (k & 3) * 32,
+                                                        16, 1024);
+                    const uint64_t db =
+                        umma_desc_sw128(sV + st * TILE_BYTES + k * 2048, HALF_BYTES, 1024);
+                    umma_bf16(tO, da, db, idesc_pv, (j > 0 || k > 0) ? 1u : 0u);
+                }
+                umma_commit(&sh.pv_done[b]);
+                umma_commit(&sh.v_empty[st]);
+            };
+            for (int kb = 0; kb < n_kb; ++kb) {
+                const int b = kb & 1, st = kb % NS;
+                mbar_wait(&sh.k_full[st], (uint32_t)(kb / NS) & 1u);
+                if (kb >= 2) mbar_wait(&sh.s_empty[b], (uint32_t)((kb >> 1) - 1) & 1u);
+                tc_fence_after();
+#pragma unroll
+                for (int k = 0; k < HD / 16; ++k) {
+                    const uint64_t da =
+                        umma_desc_sw128(sQ + (k >> 2) * HALF_BYTES + (k & 3) * 32, 16, 1024);
+                    const uint64_t db = umma_desc_sw128(
+                        sK + st * TILE_BYTES + (k >> 2) * HALF_BYTES + (k & 3) * 32, 16, 1024);
+                    umma_bf16(tS[b], da, db, idesc_qk, k > 0 ? 1u : 0u);
+                }
+                umma_commit(&sh.s_full[b]);
+                umma_commit(&sh.k_empty[st]);
+                if (kPV && kb >= 1) issue_pv(kb - 1);
+            }
+            if (kPV && n_kb >= 1) issue_pv(n_kb - 1);
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------------------ softmax warps 0-3
+        const int i = threadIdx.x;  // row within tile == TMEM lane
+        const bool valid = i < nrows;
+        const int kend = !valid ? 0 : (p.causal ? p.row_pos[row0 + i] + 1 : kmax);
+        const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+        float m = -INFINITY, l = 0.f;
+        float s[BN];
+        for (int kb = 0; kb < n_kb; ++kb) {
+            const int b = kb & 1;
+            mbar_wait(&sh.s_full[b], (uint32_t)(kb >> 1) & 1u);
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS[b] + lane_off + c * 32, s + c * 32);
+            tmem_ld_wait();
+            tc_fence_before();
+            mbar_arrive(&sh.s_empty[b]);
+            const int kbase = kb * BN;
+            float mloc = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < BN; ++c) {
+                const float x = (kbase + c < kend) ? s[c] * p.scale_log2 : -INFINITY;
+                s[c] = x;
+                mloc = fmaxf(mloc, x);
+            }
+            if (mloc > m + kRescaleThreshold || (m == -INFINITY && mloc > -INFINITY)) {
+                const float factor = (m == -INFINITY) ? 0.f : fast_exp2(m - mloc);
+                if (kPV && kb >= 1 && m != -INFINITY) {
+                    // O must be quiescent: wait for the previous P.V
+                    mbar_wait(&sh.pv_done[(kb - 1) & 1], (uint32_t)((kb - 1) >> 1) & 1u);
+                    tc_fence_after();
+                    float o[32];
+#pragma unroll
+                    for (int c = 0; c < HD / 32; ++c) {
+                        tmem_ld32(tO + lane_off + c * 32, o);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) o[e] *= factor;
+                        tmem_st32(tO + lane_off + c * 32, o);
+                    }
+                    tmem_st_wait();
+                    tc_fence_before();
+                }
+                l *= factor;
+                m = mloc;
+            }
+            const float mu = (m == -INFINITY) ? 0.f : m;
+            float lsum = 0.f;
+#pragma unroll
+            for (int c = 0; c < BN; ++c) {
+                const float e = fast_exp2(s[c] - mu);
+                s[c] = e;
+                lsum += e;
+            }
+            l += lsum;
+            if (kPV) {
+                if (kb >= 2) mbar_wait(&sh.pv_done[b], (uint32_t)((kb - 2) >> 1) & 1u);
+                uint8_t *prow = pP + b * TILE_BYTES + i * 128;
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf)
+#pragma unroll
+                    for (int c = 0; c < 8; ++c) {
+                        const float *x = s + hf * 64 + c * 8;
+                        uint4 v;
+                        v.x = pack_bf16x2(x[0], x[1]);
+                        v.y = pack_bf16x2(x[2], x[3]);
+                        v.z = pack_bf16x2(x[4], x[5]);
+                        v.w = pack_bf16x2(x[6], x[7]);
+                        *reinterpret_cast<uint4 *>(prow + hf * HALF_BYTES + ((c ^ (i & 7)) << 4)) = v;
+                    }
+                fence_proxy_async_smem();
+                mbar_arrive(&sh.p_full[b]);
+            }
+        }
+        const int64_t grow = (int64_t)row0 + i;
+        if (kPV) {
+            if (n_kb >= 1) mbar_wait(&sh.pv_done[(n_kb - 1) & 1], (uint32_t)((n_kb - 1) >> 1) & 1u);
+            tc_fence_after();
+            const float inv = l > 0.f ? 1.f / l : 0.f;
+            float o[32];
+#pragma unroll
+            for (int c = 0; c < HD / 32; ++c) {
+                tmem_ld32(tO + lane_off + c * 32, o);
+                tmem_ld_wait();
+                if (valid && p.out != nullptr) {
+                    uint4 *dst = reinterpret_cast<uint4 *>(
+                        p.out + (grow * p.num_heads + h) * HD + c * 32);
+#pragma unroll
+                    for (int v = 0; v < 4; ++v) {
+                        uint4 w;
+                        w.x = pack_bf16x2(o[8 * v + 0] * inv, o[8 * v + 1] * inv);
+                        w.y = pack_bf16x2(o[8 * v + 2] * inv, o[8 * v + 3] * inv);
+                        w.z = pack_bf16x2(o[8 * v + 4] * inv, o[8 * v + 5] * inv);
+                        w.w = pack_bf16x2(o[8 * v + 6] * inv, o[8 * v + 7] * inv);
+                        dst[v] = w;
+                    }
+                }
+            }
+        }
+        if (valid && p.lse != nullptr)
+            p.lse[grow * p.num_heads + h] =
+                (l > 0.f) ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// ------------------------------------------------------------------ D1 pass 2
+// CTA = (key tile kt of request r, kv head g).  Loops over the group's query
+// heads and the query tiles that can see the keys; S^T lands with one key per
+// TMEM lane, so each softmax thread accumulates its key's column sum.
+struct ColParams {
+    const int64_t *req_off;
+    const int32_t *row_pos;
+    const int32_t *tile_req, *tile_row0;  // key tiles == the probe's row tiles
+    const float *lse;                   // [n_total][H] natural log
+    const int32_t *block_table;
+    int32_t max_pages, page_size, num_layers, layer, num_heads, kv_heads, causal;
+    float scale_log2;
+    float *alpha_part;                  // [n_total][kv_heads]
+};
+
+__global__ void __launch_bounds__(kThreads, 1)
+    colsum_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
+                  ColParams p) {
+    extern __shared__ uint8_t dsmem[];
+    __shared__ Smem sh;
+    __shared__ float s_lse[2][BM];
+    __shared__ int32_t s_qn[2];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tile = blockIdx.x, g = blockIdx.y;
+    const int hq = p.num_heads / p.kv_heads;
+    const int req = p.tile_req[tile], k0 = p.row_pos[p.tile_row0[tile]];
+    const int64_t s0 = p.req_off[req];
+    const int n = (int)(p.req_off[req + 1] - s0);
+    const int q_first = p.causal ? (k0 / BM) : 0;         // first query tile that sees the keys
+    const int n_qt = (n + BM - 1) / BM - q_first;
+    const int n_it = hq * n_qt;                            // (head, query tile) iterations
+
+    const uint32_t base = align1024(smem_u32(dsmem));
+    const uint32_t sK = base;                  // A operand: the key tile (resident)
+    const uint32_t sQ = sK + TILE_BYTES;       // B operand stages: query tiles
+    uint8_t *gbase = dsmem + (base - smem_u32(dsmem));
+
+    if (threadIdx.x == 0) {
+        mbar_init(&sh.q_full, 1);
+        for (int i = 0; i < NS; ++i) {
+            mbar_init(&sh.k_full[i], 1);
+            mbar_init(&sh.k_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&sh.s_full[i], 1);
+            mbar_init(&sh.s_empty[i], 128);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 5) tmem_alloc(&sh.tmem_base, 256);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sh.tmem_base;
+    const uint32_t tS[2] = {tmem, tmem + 128};
+
+    if (warp == 4) {
+        if (lane == 0) {
+            tma_prefetch(&map_q);
+            tma_prefetch(&map_kv);
+            const int32_t *bt = p.block_table + (int64_t)req * p.max_pages;
+            const int pages = (n + p.page_size - 1) / p.page_size;
+            mbar_expect_tx(&sh.q_full, TILE_BYTES);  // key tile rides on q_full
+            for (int q = 0; q < 2; ++q) {
+                const int pi = k0 / p.page_size + q;
+                const int pg = bt[pi < pages ? pi : k0 / p.page_size];
+                for (int hf = 0; hf < 2; ++hf)
+                    tma_load_4d(gbase + (sK - base) + hf * HALF_BYTES + q * (HALF_BYTES / 2),
+                                &map_kv, &sh.q_full, hf * 64, g, 0,
+                                (pg * p.num_layers + p.layer) * 2 + 0);
+            }
+            for (int it = 0; it < n_it; ++it) {
+                const int st = it % NS;
+                const int hh = it / n_qt, qt = q_first + it % n_qt;
+                if (it >= NS) mbar_wait(&sh.k_empty[st], (uint32_t)((it / NS) - 1) & 1u);
+                mbar_expect_tx(&sh.k_full[st], TILE_BYTES);
+                for (int hf = 0; hf < 2; ++hf)
+                    tma_load_3d(gbase + (sQ - base) + st * TILE_BYTES + hf * HALF_BYTES, &map_q,
+                                &sh.k_full[st], hf * 64, g * hq + hh, (int)(s0 + qt * BM));
+            }
+        }
+    } else if (warp == 5) {
+        if (lane == 0) {
+            const uint32_t idesc = umma_idesc_bf16(BM, BN, false);
+            mbar_wait(&sh.q_full, 0);
+            for (int it = 0; it < n_it; ++it) {
+                const int b = it & 1, st = it % NS;
+                mbar_wait(&sh.k_full[st], (uint32_t)(it / NS) & 1u);
+                if (it >= 2) mbar_wait(&sh.s_empty[b], (uint32_t)((it >> 1) - 1) & 1u);
+                tc_fence_after();
+#pragma unroll
+                for (int k = 0; k < HD / 16; ++k) {
+                    const uint64_t da =
+                        umma_desc_sw128(sK + (k >> 2) * HALF_BYTES + (k & 3) * 32, 16, 1024);
+                    const uint64_t db = umma_desc_sw128(
+                        sQ + st * TILE_BYTES + (k >> 2) * HALF_BYTES + (k & 3) * 32, 16, 1024);
+                    umma_bf16(tS[b], da, db, idesc, k > 0 ? 1u : 0u);
+                }
+                umma_commit(&sh.s_full[b]);
+                umma_commit(&sh.k_empty[st]);
+            }
+        }
+        __syncwarp();
+    } else {
+        const int i = threadIdx.x;               // key within tile == TMEM lane
+        const int kpos = k0 + i;
+        const bool kvalid = kpos < n;
+        const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+        float acc = 0.f;
+        float s[BN];
+        for (int it = 0; it < n_it; ++it) {
+            const int b = it & 1;
+            const int hh = it / n_qt, qt = q_first + it % n_qt;
+            const int h = g * hq + hh;
+            // stage this iteration's query LSEs (log2 units) in shared memory
+            const int qrow = qt * BM + i;
+            s_lse[b][i] = qrow < n ? p.lse[(s0 + qrow) * p.num_heads + h] * 1.4426950408889634f
+                                   : INFINITY;
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            mbar_wait(&sh.s_full[b], (uint32_t)(it >> 1) & 1u);
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS[b] + lane_off + c * 32, s + c * 32);
+            tmem_ld_wait();
+            tc_fence_before();
+            mbar_arrive(&sh.s_empty[b]);
+            const int qbase = qt * BM;
+            float part = 0.f;
+#pragma unroll
+            for (int c = 0; c < BN; ++c) {
+                const bool ok = (!p.causal || qbase + c >= kpos);
+                const float e = fast_exp2(s[c] * p.scale_log2 - s_lse[b][c]);
+                part += ok ? e : 0.f;
+            }
+            acc += part;
+        }
+        if (kvalid) p.alpha_part[(s0 + kpos) * p.kv_heads + g] = acc;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 256);
+    }
+}
+
+__global__ void alpha_reduce_kernel(const float *__restrict__ part, int64_t n, int32_t G, int32_t H,
+                                    float *__restrict__ alpha) {
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        float s = 0.f;
+        for (int g = 0; g < G; ++g) s += part[t * G + g];
+        alpha[t] = s / (float)H;
+    }
+}
+
+}  // namespace attn
+
+static bool make_kv_map(CUtensorMap *m, const kvs_kv_arena *a) {
+    const uint64_t G = a->kv_heads, D = a->head_dim, P = a->page_size;
+    uint64_t dims[4] = {D, G, P, (uint64_t)a->num_pages * a->num_layers * 2};
+    uint64_t strides[3] = {D * 2, G * D * 2, P * G * D * 2};
+    uint32_t box[4] = {64, 1, (uint32_t)P, 1};
+    return encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, a->base, dims, strides, box,
+                       CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+static bool make_q_map(CUtensorMap *m, const void *q, int64_t n_rows, int H, int D) {
+    uint64_t dims[3] = {(uint64_t)D, (uint64_t)H, (uint64_t)n_rows};
+    uint64_t strides[2] = {(uint64_t)D * 2, (uint64_t)H * D * 2};
+    uint32_t box[3] = {64, 1, 128};
+    return encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(q), dims, strides,
+                       box, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
+static kvs_status check_arena(const kvs_kv_arena *a, int32_t num_heads) {
+    KVS_REQUIRE(a != nullptr, KVS_EPARAM, "null arena");
+    KVS_REQUIRE(a->head_dim == 128, KVS_ESHAPE, "tcgen05 attention needs head_dim == 128 (got %d)",
+                a->head_dim);
+    KVS_REQUIRE(a->page_size == 64, KVS_ESHAPE, "tcgen05 attention needs page_size == 64");
+    KVS_REQUIRE(num_heads % a->kv_heads == 0, KVS_ESHAPE, "num_heads %% kv_heads != 0");
+    return KVS_OK;
+}
+
+template <bool kPV>
+static size_t fwd_smem() {
+    return 1024 + attn::TILE_BYTES * (1 + attn::NS + (kPV ? attn::NS + 2 : 0));
+}
+
+}  // namespace kvs
+
+using namespace kvs;
+
+extern "C" {
+
+kvs_status kvs_attention_fwd(const void *q, const int32_t *row_pos, int64_t n_rows,
+                             int32_t num_heads, const int32_t *tile_req, const int32_t *tile_row0,
+                             const int32_t *tile_rows, int32_t n_tiles, const int32_t *kv_len,
+                             int32_t causal, int32_t layer, const kvs_kv_arena *arena,
+                             const kvs_batch *batch, float softmax_scale, void *out, float *lse,
+                             kvs_stream_t stream) {
+    kvs_status st = check_arena(arena, num_heads);
+    if (st != KVS_OK) return st;
+    KVS_REQUIRE(batch != nullptr, KVS_EPARAM, "null batch");
+    KVS_REQUIRE(causal || kv_len != nullptr, KVS_EPARAM, "non-causal attention needs kv_len");
+    if (n_tiles <= 0 || n_rows <= 0) return KVS_OK;
+    CUtensorMap mq, mkv;
+    KVS_REQUIRE(make_q_map(&mq, q, n_rows, num_heads, 128), KVS_ECUDA, "Q tensor map");
+    KVS_REQUIRE(make_kv_map(&mkv, arena), KVS_ECUDA, "KV tensor map");
+    attn::Params p;
+    p.row_pos = row_pos;
+    p.tile_req = tile_req;
+    p.tile_row0 = tile_row0;
+    p.tile_rows = tile_rows;
+    p.kv_len = kv_len;
+    p.block_table = batch->block_table;
+    p.max_pages = batch->max_pages;
+    p.page_size = arena->page_size;
+    p.num_layers = arena->num_layers;
+    p.layer = layer;
+    p.num_heads = num_heads;
+    p.kv_heads = arena->kv_heads;
+    p.causal = causal;
+    p.scale_log2 = softmax_scale * 1.4426950408889634f;
+    p.out = (__nv_bfloat16 *)out;
+    p.lse = lse;
+    p.n_rows = n_rows;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (out != nullptr) {
+        const size_t smem = fwd_smem<true>();
+        cudaFuncSetAttribute(attn::fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        attn::fwd_kernel<true><<<dim3(n_tiles, num_heads), attn::kThreads, smem, s>>>(mq, mkv, p);
+    } else {
+        const size_t smem = fwd_smem<false>();
+        cudaFuncSetAttribute(attn::fwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        attn::fwd_kernel<false><<<dim3(n_tiles, num_heads), attn::kThreads, smem, s>>>(mq, mkv, p);
+    }
+    KVS_CHECK_LAUNCH("kvs_attention_fwd");
+    return KVS_OK;
+}
+
+size_t kvs_dhd_alpha_workspace(int64_t n_total, int32_t num_heads, int32_t kv_heads) {
+    return ((sizeof(float) * (size_t)n_total * num_heads + 255) & ~(size_t)255) +
+           sizeof(float) * (size_t)n_total * kv_heads;
+}
+
+kvs_status kvs_dhd_alpha(const void *q, int32_t num_heads, int32_t causal, int32_t layer,
+                         const kvs_kv_arena *arena, const kvs_batch *batch,
+                         const int32_t *row_pos, const int32_t *tile_req,
+                         const int32_t *tile_row0, const int32_t *tile_rows, int32_t n_tiles,
+                         const int32_t *kv_len, float softmax_scale, float *alpha, void *ws,
+                         size_t ws_bytes, kvs_stream_t stream) {
+    kvs_status st = check_arena(arena, num_heads);
+    if (st != KVS_OK) return st;
+    KVS_REQUIRE(batch != nullptr, KVS_EPARAM, "null batch");
+    KVS_REQUIRE(causal || kv_len != nullptr, KVS_EPARAM, "non-causal alpha needs kv_len");
+    const int64_t n_total = batch->n_total;
+    KVS_REQUIRE(ws_bytes >= kvs_dhd_alpha_workspace(n_total, num_heads, arena->kv_heads),
+                KVS_EPARAM, "workspace too small");
+    if (n_tiles <= 0 || n_total <= 0) return KVS_OK;
+    float *lse = (float *)ws;
+    float *part = (float *)((char *)ws + (((sizeof(float) * (size_t)n_total * num_heads) + 255) &
+                                          ~(size_t)255));
+    cudaStream_t s = (cudaStream_t)stream;
+    // pass 1: row log-sum-exp (the forward kernel without P.V)
+    st = kvs_attention_fwd(q, row_pos, n_total, num_heads, tile_req, tile_row0, tile_rows, n_tiles,
+                           kv_len, causal, layer, arena, batch, softmax_scale, nullptr, lse,
+                           stream);
+    if (st != KVS_OK) return st;
+    // pass 2: key-major column sums
+    CUtensorMap mq, mkv;
+    KVS_REQUIRE(make_q_map(&mq, q, n_total, num_heads, 128), KVS_ECUDA, "Q tensor map");
+    KVS_REQUIRE(make_kv_map(&mkv, arena), KVS_ECUDA, "KV tensor map");
+    attn::ColParams cp;
+    cp.req_off = batch->req_off;
+    cp.row_pos = row_pos;
+    cp.tile_req = tile_req;
+    cp.tile_row0 = tile_row0;
+    cp.lse = lse;
+    cp.block_table = batch->block_table;
+    cp.max_pages = batch->max_pages;
+    cp.page_size = arena->page_size;
+    cp.num_layers = arena->num_layers;
+    cp.layer = layer;
+    cp.num_heads = num_heads;
+    cp.kv_heads = arena->kv_heads;
+    cp.causal = causal;
+    cp.scale_log2 = softmax_scale * 1.4426950408889634f;
+    cp.alpha_part = part;
+    const size_t smem = 1024 + attn::TILE_BYTES * (1 + attn::NS);
+    cudaFuncSetAttribute(attn::colsum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attn::colsum_kernel<<<dim3(n_tiles, arena->kv_heads), attn::kThreads, smem, s>>>(mq, mkv, cp);
+    attn::alpha_reduce_kernel<<<kNumSMs * 4, 256, 0, s>>>(part, n_total, arena->kv_heads,
+                                                         num_heads, alpha);
+    KVS_CHECK_LAUNCH("kvs_dhd_alpha");
+    return KVS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,492 @@
+// D2 DHD-select, D3 decode-stage DHD and the SIMT few-row (decode) attention.
+//
+// D2 follows v_impact_scores' dv-L1 half and _take_top
+//   (reference deviation.py:111-115, selection.py:51-77): HBM-bound pass over
+//   the probe-layer V rows (cached vs fresh) of every reused position, then a
+//   per-request radix select of the budget smallest 64-bit keys
+//   (~score_bits << 32 | pos), i.e. score descending, position ascending.
+// D3 follows select_decode_step (selection.py:80-105): unmasked softmax of
+//   q_t . K over the whole current context per query head, mean over heads,
+//   times the prefill dv-L1, top n_extra over the eligible rows.
+#include "common.cuh"
+
+namespace kvs {
+
+struct ArenaC {
+    const __nv_bfloat16 *base;
+    int32_t L, G, D, P;
+    __device__ __forceinline__ const __nv_bfloat16 *row(int64_t page, int layer, int kv,
+                                                        int r) const {
+        return base + ((((size_t)page * L + layer) * 2 + kv) * P + r) * (size_t)(G * D);
+    }
+};
+static inline ArenaC arena_c(const kvs_kv_arena *a) {
+    return ArenaC{(const __nv_bfloat16 *)a->base, a->num_layers, a->kv_heads, a->head_dim,
+                  a->page_size};
+}
+
+__device__ __forceinline__ int find_req(const int64_t *req_off, int n_req, int64_t t) {
+    int lo = 0, hi = n_req;
+    while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (req_off[mid] <= t) lo = mid; else hi = mid;
+    }
+    return lo;
+}
+
+__device__ __forceinline__ float l1_diff8(const uint4 &a, const uint4 &b) {
+    const __nv_bfloat162 *x = reinterpret_cast<const __nv_bfloat162 *>(&a);
+    const __nv_bfloat162 *y = reinterpret_cast<const __nv_bfloat162 *>(&b);
+    float s = 0.f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        float2 fx = __bfloat1622float2(x[k]), fy = __bfloat1622float2(y[k]);
+        s += fabsf(fx.x - fy.x) + fabsf(fx.y - fy.y);
+    }
+    return s;
+}
+
+// ---------------------------------------------------------------- D2 pass 1
+// One warp per flat position (grid-stride); 16-byte loads, 4 in flight/lane.
+__global__ void __launch_bounds__(256) dv_score_kernel(
+    const __nv_bfloat16 *__restrict__ v_true, const float *__restrict__ alpha,
+    const int32_t *__restrict__ src_slot, int32_t layer, ArenaC A,
+    const int64_t *__restrict__ req_off, int32_t n_req, int64_t n_total,
+    const int32_t *__restrict__ block_table, int32_t max_pages, float *__restrict__ dv_l1,
+    float *__restrict__ score) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int nvec = A.G * A.D / 8;
+    for (int64_t t = warp; t < n_total; t += nwarps) {
+        if (src_slot[t] < 0) {
+            if (lane == 0) { dv_l1[t] = 0.f; score[t] = 0.f; }
+            continue;
+        }
+        const int r = find_req(req_off, n_req, t);
+        const int32_t pos = (int32_t)(t - req_off[r]);
+        const int64_t page = block_table[(int64_t)r * max_pages + pos / A.P];
+        const uint4 *vc = reinterpret_cast<const uint4 *>(A.row(page, layer, 1, pos % A.P));
+        const uint4 *vt = reinterpret_cast<const uint4 *>(v_true + t * (int64_t)(A.G * A.D));
+        float s = 0.f;
+        for (int v0 = 0; v0 < nvec; v0 += 128) {
+            uint4 a[4], b[4];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const int v = v0 + k * 32 + lane;
+                if (v < nvec) { a[k] = __ldg(vc + v); b[k] = __ldg(vt + v); }
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (v0 + k * 32 + lane < nvec) s += l1_diff8(a[k], b[k]);
+        }
+        s = warp_sum(s);
+        if (lane == 0) {
+            dv_l1[t] = s;
+            score[t] = alpha[t] * s;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- D2 pass 2
+// Per request radix select of the `budget` smallest keys.  One CTA / request.
+__device__ __forceinline__ uint64_t sel_key(const float *score, const int32_t *src_slot,
+                                            int64_t s, int64_t i) {
+    if (src_slot[s + i] < 0) return ~0ull;
+    const uint32_t bits = __float_as_uint(fmaxf(score[s + i], 0.f));
+    return ((uint64_t)(~bits) << 32) | (uint64_t)i;
+}
+
+__global__ void __launch_bounds__(1024) radix_select_kernel(
+    const float *__restrict__ score, const int32_t *__restrict__ src_slot,
+    const int64_t *__restrict__ req_off, const int32_t *__restrict__ budget,
+    uint8_t *__restrict__ selected) {
+    __shared__ uint32_t hist[256];
+    __shared__ uint64_t s_prefix;
+    __shared__ int32_t s_k;
+    const int r = blockIdx.x;
+    const int64_t s = req_off[r], n = req_off[r + 1] - s;
+    const int32_t B = budget[r];
+    if (threadIdx.x == 0) { s_prefix = 0; s_k = B; }
+    // prefix/mask of the key bits fixed so far (most significant first)
+    uint64_t mask = 0;
+    for (int pass = 0; pass < 8 && B > 0; ++pass) {
+        const int shift = 56 - 8 * pass;
+        for (int b = threadIdx.x; b < 256; b += blockDim.x) hist[b] = 0;
+        __syncthreads();
+        const uint64_t prefix = s_prefix;
+        for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+            const uint64_t key = sel_key(score, src_slot, s, i);
+            if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 0xff], 1u);
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int32_t k = s_k;
+            uint32_t cum = 0;
+            int digit = 0;
+            for (; digit < 256; ++digit) {
+                if (cum + hist[digit] >= (uint32_t)k) break;
+                cum += hist[digit];
+            }
+            if (digit > 255) digit = 255;
+            s_k = k - (int32_t)cum;
+            s_prefix = prefix | ((uint64_t)digit << shift);
+        }
+        mask |= 0xffull << shift;
+        __syncthreads();
+    }
+    const uint64_t thr = s_prefix;  // the B-th smallest key (keys are unique)
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint64_t key = sel_key(score, src_slot, s, i);
+        selected[s + i] = (B > 0 && key != ~0ull && key <= thr) ? 1 : 0;
+    }
+}
+
+// ---------------------------------------------------------------- D3
+// Pass 1: grid (request, key chunk).  Logits for all query heads of one key
+// row, each K row read once for its GQA group; per-(request, chunk, head)
+// partial max / sum-exp.
+constexpr int kDecChunk = 256;
+__global__ void __launch_bounds__(256) decode_logits_kernel(
+    const __nv_bfloat16 *__restrict__ q_t, int32_t H, const int32_t *__restrict__ ctx_len,
+    int32_t max_ctx, int32_t layer, ArenaC A, const int32_t *__restrict__ block_table,
+    int32_t max_pages, float scale_log2, float *__restrict__ logits, float2 *__restrict__ part) {
+    extern __shared__ float sq[];  // [H][D] fp32
+    __shared__ float smax[8][64], ssum[8][64];
+    const int r = blockIdx.y, chunk = blockIdx.x;
+    const int n = ctx_len[r];
+    const int D = A.D, G = A.G, hq = H / G;
+    for (int i = threadIdx.x; i < H * D; i += blockDim.x)
+        sq[i] = bf2f(q_t[(int64_t)r * H * D + i]);
+    __syncthreads();
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int k0 = chunk * kDecChunk;
+    float mloc[64], lloc[64];  // per head (H <= 64), lane-redundant
+    for (int h = 0; h < H; ++h) { mloc[h] = -INFINITY; lloc[h] = 0.f; }
+    for (int k = k0 + wid; k < min(n, k0 + kDecChunk); k += 8) {
+        const int64_t page = block_table[(int64_t)r * max_pages + k / A.P];
+        const __nv_bfloat16 *krow = A.row(page, layer, 0, k % A.P);
+        for (int g = 0; g < G; ++g) {
+            // lane holds D/32 elements of head g
+            float kv[8];
+            const int per = D / 32;
+            for (int e = 0; e < per; ++e) kv[e] = bf2f(krow[g * D + lane * per + e]);
+            for (int hh = 0; hh < hq; ++hh) {
+                const int h = g * hq + hh;
+                float p = 0.f;
+                for (int e = 0; e < per; ++e) p += kv[e] * sq[h * D + lane * per + e];
+                p = warp_sum(p) * scale_log2;  // log2-domain logit
+                if (lane == 0) logits[((int64_t)r * H + h) * max_ctx + k] = p;
+                const float mn = fmaxf(mloc[h], p);
+                lloc[h] = lloc[h] * fast_exp2(mloc[h] - mn) + fast_exp2(p - mn);
+                mloc[h] = mn;
+            }
+        }
+    }
+    if (lane == 0)
+        for (int h = 0; h < H; ++h) { smax[wid][h] = mloc[h]; ssum[wid][h] = lloc[h]; }
+    __syncthreads();
+    for (int h = threadIdx.x; h < H; h += blockDim.x) {
+        float m = -INFINITY, l = 0.f;
+        for (int w = 0; w < 8; ++w) {
+            const float mw = smax[w][h];
+            if (mw == -INFINITY) continue;
+            const float mn = fmaxf(m, mw);
+            l = l * fast_exp2(m - mn) + ssum[w][h] * fast_exp2(mw - mn);
+            m = mn;
+        }
+        part[((int64_t)r * gridDim.x + chunk) * H + h] = make_float2(m, l);
+    }
+}
+
+// Pass 2: one CTA per request: combine partials, score eligible prefill rows,
+// n_extra rounds of block argmax on (score desc, pos asc).
+__global__ void __launch_bounds__(1024) decode_select_kernel(
+    int32_t H, const int32_t *__restrict__ ctx_len, int32_t max_ctx, int32_t n_chunks,
+    const float *__restrict__ logits, const float2 *__restrict__ part,
+    const float *__restrict__ dv_l1, uint8_t *__restrict__ eligible,
+    const int64_t *__restrict__ req_off, int32_t n_extra, int32_t *__restrict__ chosen,
+    int32_t *__restrict__ n_chosen, float *__restrict__ scores_out) {
+    __shared__ float sm[64], sz[64];
+    __shared__ uint64_t red[32];
+    __shared__ int32_t s_pick[64];
+    const int r = blockIdx.x;
+    const int n = ctx_len[r];
+    const int64_t s = req_off[r];
+    const int n_pre = (int)(req_off[r + 1] - s);
+    for (int h = threadIdx.x; h < H; h += blockDim.x) {
+        float m = -INFINITY, l = 0.f;
+        for (int c = 0; c < n_chunks; ++c) {
+            const float2 p = part[((int64_t)r * n_chunks + c) * H + h];
+            if (p.x == -INFINITY) continue;
+            const float mn = fmaxf(m, p.x);
+            l = l * fast_exp2(m - mn) + p.y * fast_exp2(p.x - mn);
+            m = mn;
+        }
+        sm[h] = m;
+        sz[h] = 1.f / l;
+    }
+    __syncthreads();
+    // scores for prefill rows (decode rows have zero deviation, engine.py:145-147)
+    const float invH = 1.f / (float)H;
+    float *scr = scores_out ? scores_out + (int64_t)r * max_ctx : nullptr;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        float w = 0.f;
+        for (int h = 0; h < H; ++h)
+            w += fast_exp2(logits[((int64_t)r * H + h) * max_ctx + i] - sm[h]) * sz[h];
+        const float sc = i < n_pre ? w * invH * dv_l1[s + i] : 0.f;
+        if (scr) scr[i] = sc;
+    }
+    // recompute-free argmax rounds: keys are recomputed from logits each round
+    int picked = 0;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int round = 0; round < n_extra; ++round) {
+        uint64_t best = ~0ull;
+        for (int i = threadIdx.x; i < n_pre && i < n; i += blockDim.x) {
+            if (!eligible[s + i]) continue;
+            float w = 0.f;
+            for (int h = 0; h < H; ++h)
+                w += fast_exp2(logits[((int64_t)r * H + h) * max_ctx + i] - sm[h]) * sz[h];
+            const float sc = fmaxf(w * invH * dv_l1[s + i], 0.f);
+            const uint64_t key = ((uint64_t)(~__float_as_uint(sc)) << 32) | (uint32_t)i;
+            best = key < best ? key : best;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const uint64_t x = __shfl_xor_sync(0xffffffffu, best, o);
+            best = x < best ? x : best;
+        }
+        if (lane == 0) red[wid] = best;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint64_t b = ~0ull;
+            for (int k = 0; k < (int)(blockDim.x >> 5); ++k) b = red[k] < b ? red[k] : b;
+            s_pick[round] = b == ~0ull ? -1 : (int32_t)(b & 0xffffffffu);
+            if (b != ~0ull) eligible[s + (b & 0xffffffffu)] = 0;
+        }
+        __syncthreads();
+        if (s_pick[round] < 0) break;
+        ++picked;
+    }
+    if (threadIdx.x == 0) {
+        // ascending order (selection.py:66), pad with -1
+        int32_t tmp[64];
+        for (int k = 0; k < picked; ++k) tmp[k] = s_pick[k];
+        for (int a = 1; a < picked; ++a)
+            for (int b = a; b > 0 && tmp[b - 1] > tmp[b]; --b) {
+                int32_t x = tmp[b]; tmp[b] = tmp[b - 1]; tmp[b - 1] = x;
+            }
+        for (int k = 0; k < n_extra; ++k)
+            chosen[(int64_t)r * n_extra + k] = k < picked ? tmp[k] : -1;
+        n_chosen[r] = picked;
+    }
+}
+
+// ---------------------------------------------------------------- decode attention
+// grid (row, kv head, split).  lane owns D/32 dims; each warp walks keys,
+// online softmax per query head of the group; partials combined afterwards.
+constexpr int kMaxGroup = 8;
+__global__ void __launch_bounds__(128) decode_attn_partial_kernel(
+    const __nv_bfloat16 *__restrict__ q, const int32_t *__restrict__ row_req,
+    const int32_t *__restrict__ row_pos, int32_t H, const int32_t *__restrict__ kv_len,
+    int32_t causal, int32_t layer, ArenaC A, const int32_t *__restrict__ block_table,
+    int32_t max_pages, float scale_log2, int32_t n_splits, float *__restrict__ ws) {
+    const int row = blockIdx.x, g = blockIdx.y, split = blockIdx.z;
+    const int D = A.D, G = A.G, hq = H / G, per = D / 32;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int r = row_req[row];
+    const int kend = causal ? row_pos[row] + 1 : kv_len[r];
+    const int span = (kend + n_splits - 1) / n_splits;
+    const int kb = split * span, ke = min(kend, kb + span);
+    float qv[kMaxGroup][4], acc[kMaxGroup][4], m[kMaxGroup], l[kMaxGroup];
+    for (int hh = 0; hh < hq; ++hh) {
+        for (int e = 0; e < per; ++e) {
+            qv[hh][e] = bf2f(q[((int64_t)row * H + g * hq + hh) * D + lane * per + e]);
+            acc[hh][e] = 0.f;
+        }
+        m[hh] = -INFINITY;
+        l[hh] = 0.f;
+    }
+    for (int k = kb + wid; k < ke; k += 4) {
+        const int64_t page = block_table[(int64_t)r * max_pages + k / A.P];
+        const __nv_bfloat16 *kr = A.row(page, layer, 0, k % A.P) + g * D + lane * per;
+        const __nv_bfloat16 *vr = A.row(page, layer, 1, k % A.P) + g * D + lane * per;
+        float kf[4], vf[4];
+        for (int e = 0; e < per; ++e) { kf[e] = bf2f(kr[e]); vf[e] = bf2f(vr[e]); }
+        for (int hh = 0; hh < hq; ++hh) {
+            float p = 0.f;
+            for (int e = 0; e < per; ++e) p += kf[e] * qv[hh][e];
+            p = warp_sum(p) * scale_log2;
+            const float mn = fmaxf(m[hh], p);
+            const float c = fast_exp2(m[hh] - mn), e2 = fast_exp2(p - mn);
+            l[hh] = l[hh] * c + e2;
+            for (int e = 0; e < per; ++e) acc[hh][e] = acc[hh][e] * c + e2 * vf[e];
+            m[hh] = mn;
+        }
+    }
+    // combine the 4 warps through shared memory
+    __shared__ float sm_m[4][kMaxGroup], sm_l[4][kMaxGroup];
+    __shared__ float sm_acc[4][kMaxGroup][128];
+    if (lane == 0)
+        for (int hh = 0; hh < hq; ++hh) { sm_m[wid][hh] = m[hh]; sm_l[wid][hh] = l[hh]; }
+    for (int hh = 0; hh < hq; ++hh)
+        for (int e = 0; e < per; ++e) sm_acc[wid][hh][lane * per + e] = acc[hh][e];
+    __syncthreads();
+    // ws layout per (row, head, split): [m, l, acc[D]]
+    for (int idx = threadIdx.x; idx < hq * D; idx += blockDim.x) {
+        const int hh = idx / D, d = idx % D;
+        float M = -INFINITY;
+        for (int w = 0; w < 4; ++w) M = fmaxf(M, sm_m[w][hh]);
+        float L = 0.f, S = 0.f;
+        for (int w = 0; w < 4; ++w) {
+            if (sm_m[w][hh] == -INFINITY) continue;
+            const float c = fast_exp2(sm_m[w][hh] - M);
+            L += sm_l[w][hh] * c;
+            S += sm_acc[w][hh][d] * c;
+        }
+        float *o = ws + (((int64_t)row * H + g * hq + hh) * n_splits + split) * (D + 2);
+        if (d == 0) { o[0] = M; o[1] = L; }
+        o[2 + d] = S;
+    }
+}
+
+__global__ void decode_attn_combine_kernel(const float *__restrict__ ws, int32_t H, int32_t D,
+                                           int32_t n_splits, __nv_bfloat16 *__restrict__ out) {
+    const int row = blockIdx.x, h = blockIdx.y;
+    const float *base = ws + ((int64_t)row * H + h) * n_splits * (D + 2);
+    float M = -INFINITY;
+    for (int sp = 0; sp < n_splits; ++sp) M = fmaxf(M, base[sp * (D + 2)]);
+    for (int d = threadIdx.x; d < D; d += blockDim.x) {
+        float L = 0.f, S = 0.f;
+        for (int sp = 0; sp < n_splits; ++sp) {
+            const float *o = base + sp * (D + 2);
+            if (o[0] == -INFINITY) continue;
+            const float c = fast_exp2(o[0] - M);
+            L += o[1] * c;
+            S += o[2 + d] * c;
+        }
+        out[((int64_t)row * H + h) * D + d] = f2bf(L > 0.f ? S / L : 0.f);
+    }
+}
+
+static inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static int decode_splits(int64_t n_rows, int G, int max_kv) {
+    int64_t want = (2 * kNumSMs + n_rows * G - 1) / (n_rows * G);
+    int64_t cap = (max_kv + 127) / 128;
+    if (want > cap) want = cap;
+    if (want < 1) want = 1;
+    if (want > 64) want = 64;
+    return (int)want;
+}
+
+}  // namespace kvs
+
+using namespace kvs;
+
+extern "C" {
+
+size_t kvs_dhd_select_workspace(int64_t n_total, int32_t n_req) {
+    (void)n_total;
+    (void)n_req;
+    return 0;
+}
+
+kvs_status kvs_dhd_select(const void *v_true, const float *alpha, const int32_t *src_slot,
+                          int32_t layer, const kvs_kv_arena *arena, const kvs_batch *batch,
+                          const int32_t *budget, float *dv_l1, float *score, uint8_t *selected,
+                          void *ws, size_t ws_bytes, kvs_stream_t stream) {
+    (void)ws;
+    (void)ws_bytes;
+    KVS_REQUIRE(arena && batch, KVS_EPARAM, "null arena/batch");
+    KVS_REQUIRE((arena->kv_heads * arena->head_dim) % 8 == 0, KVS_ESHAPE, "row width % 8 != 0");
+    if (batch->n_total <= 0) return KVS_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    int64_t warps = batch->n_total;
+    int grid = (int)((warps * 32 + 255) / 256);
+    if (grid > kNumSMs * 16) grid = kNumSMs * 16;
+    dv_score_kernel<<<grid, 256, 0, s>>>((const __nv_bfloat16 *)v_true, alpha, src_slot, layer,
+                                         arena_c(arena), batch->req_off, batch->n_req,
+                                         batch->n_total, batch->block_table, batch->max_pages,
+                                         dv_l1, score);
+    radix_select_kernel<<<batch->n_req, 1024, 0, s>>>(score, src_slot, batch->req_off, budget,
+                                                      selected);
+    KVS_CHECK_LAUNCH("kvs_dhd_select");
+    return KVS_OK;
+}
+
+size_t kvs_dhd_decode_select_workspace(int32_t n_req, int32_t num_heads, int32_t max_ctx) {
+    const int64_t chunks = (max_ctx + kDecChunk - 1) / kDecChunk;
+    return align256(sizeof(float) * (size_t)n_req * num_heads * max_ctx) +
+           align256(sizeof(float2) * (size_t)n_req * chunks * num_heads);
+}
+
+kvs_status kvs_dhd_decode_select(const void *q_t, int32_t num_heads, const int32_t *ctx_len,
+                                 int32_t max_ctx, const float *dv_l1, uint8_t *eligible,
+                                 int32_t layer, const kvs_kv_arena *arena, const kvs_batch *batch,
+                                 int32_t n_extra, float softmax_scale, int32_t *chosen,
+                                 int32_t *n_chosen, float *scores, void *ws, size_t ws_bytes,
+                                 kvs_stream_t stream) {
+    KVS_REQUIRE(arena && batch, KVS_EPARAM, "null arena/batch");
+    KVS_REQUIRE(num_heads <= 64 && num_heads % arena->kv_heads == 0, KVS_ESHAPE,
+                "num_heads must be <= 64 and a multiple of kv_heads");
+    KVS_REQUIRE(arena->head_dim % 32 == 0 && arena->head_dim <= 256, KVS_ESHAPE,
+                "head_dim must be a multiple of 32 (<= 256)");
+    KVS_REQUIRE(n_extra >= 0 && n_extra <= 64, KVS_EPARAM, "n_extra must be in [0, 64]");
+    KVS_REQUIRE(ws_bytes >= kvs_dhd_decode_select_workspace(batch->n_req, num_heads, max_ctx),
+                KVS_EPARAM, "workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    if (n_extra == 0 || max_ctx <= 0) {
+        cudaMemsetAsync(n_chosen, 0, sizeof(int32_t) * batch->n_req, s);
+        return KVS_OK;
+    }
+    const int chunks = (max_ctx + kDecChunk - 1) / kDecChunk;
+    float *logits = (float *)ws;
+    float2 *part = (float2 *)((char *)ws + align256(sizeof(float) * (size_t)batch->n_req *
+                                                     num_heads * max_ctx));
+    const float scale_log2 = softmax_scale * 1.4426950408889634f;
+    const size_t smem = sizeof(float) * num_heads * arena->head_dim;
+    decode_logits_kernel<<<dim3(chunks, batch->n_req), 256, smem, s>>>(
+        (const __nv_bfloat16 *)q_t, num_heads, ctx_len, max_ctx, layer, arena_c(arena),
+        batch->block_table, batch->max_pages, scale_log2, logits, part);
+    decode_select_kernel<<<batch->n_req, 1024, 0, s>>>(num_heads, ctx_len, max_ctx, chunks, logits,
+                                                       part, dv_l1, eligible, batch->req_off,
+                                                       n_extra, chosen, n_chosen, scores);
+    KVS_CHECK_LAUNCH("kvs_dhd_decode_select");
+    return KVS_OK;
+}
+
+size_t kvs_decode_attention_workspace(int64_t n_rows, int32_t num_heads, int32_t kv_heads,
+                                      int32_t head_dim, int32_t max_kv) {
+    const int splits = decode_splits(n_rows, kv_heads, max_kv);
+    return sizeof(float) * (size_t)n_rows * num_heads * splits * (head_dim + 2);
+}
+
+kvs_status kvs_decode_attention(const void *q, const int32_t *row_req, const int32_t *row_pos,
+                                int64_t n_rows, int32_t num_heads, const int32_t *kv_len,
+                                int32_t causal, int32_t layer, const kvs_kv_arena *arena,
+                                const kvs_batch *batch, float softmax_scale, void *out, void *ws,
+                                size_t ws_bytes, kvs_stream_t stream) {
+    KVS_REQUIRE(arena && batch, KVS_EPARAM, "null arena/batch");
+    const int G = arena->kv_heads, D = arena->head_dim;
+    KVS_REQUIRE(num_heads % G == 0 && num_heads / G <= kMaxGroup, KVS_ESHAPE,
+                "num_heads / kv_heads must be <= 8");
+    KVS_REQUIRE(D % 32 == 0 && D <= 128, KVS_ESHAPE, "decode attention needs head_dim <= 128, %% 32");
+    if (n_rows <= 0) return KVS_OK;
+    int max_kv = 0;
+    for (int64_t k = 0; k < (int64_t)batch->max_pages; ++k) max_kv += arena->page_size;
+    const int splits = decode_splits(n_rows, G, max_kv);
+    KVS_REQUIRE(ws_bytes >= sizeof(float) * (size_t)n_rows * num_heads * splits * (D + 2),
+                KVS_EPARAM, "workspace too small");
+    cudaStream_t s = (cudaStream_t)stream;
+    const float scale_log2 = softmax_scale * 1.4426950408889634f;
+    decode_attn_partial_kernel<<<dim3((unsigned)n_rows, G, splits), 128, 0, s>>>(
+        (const __nv_bfloat16 *)q, row_req, row_pos, num_heads, kv_len, causal, layer,
+        arena_c(arena), batch->block_table, batch->max_pages, scale_log2, splits, (float *)ws);
+    decode_attn_combine_kernel<<<dim3((unsigned)n_rows, num_heads), 128, 0, s>>>(
+        (const float *)ws, num_heads, D, splits, (__nv_bfloat16 *)out);
+    KVS_CHECK_LAUNCH("kvs_decode_attention");
+    return KVS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,275 @@
+// G1 reused-KV gather with fused RoPE re-alignment, the post-GEMM q/k/v
+// RoPE + paged scatter, embedding rows and the recompute row-set builder.
+//
+// Reference: cached-row substitution model.py:196-200 / engine.py:204-206
+// (K and V rows of every layer copied verbatim from the entry); RoPE is an
+// extension: K is kept post-rotation at the owner's positions
+// and re-aligned by the rotation of (dst_pos - cand_pos).
+#include "common.cuh"
+
+namespace kvs {
+
+struct Arena {
+    __nv_bfloat16 *base;
+    int32_t L, G, D, P;  // layers, kv heads, head dim, page size
+    __device__ __forceinline__ __nv_bfloat16 *row(int64_t page, int layer, int kv, int r) const {
+        return base + ((((size_t)page * L + layer) * 2 + kv) * P + r) * (size_t)(G * D);
+    }
+};
+
+static inline Arena make_arena(const kvs_kv_arena *a) {
+    return Arena{(__nv_bfloat16 *)a->base, a->num_layers, a->kv_heads, a->head_dim, a->page_size};
+}
+
+// Rotate-half RoPE on 8 consecutive dims [8c, 8c+8) of the first half paired
+// with [half + 8c, ...): angle index delta (cos even, sin odd).
+__device__ __forceinline__ void rope8(const uint4 &lo_in, const uint4 &hi_in, uint4 &lo_out,
+                                      uint4 &hi_out, const float *__restrict__ cos_t,
+                                      const float *__restrict__ sin_t, int32_t delta, int half,
+                                      int c) {
+    const int32_t a = delta < 0 ? -delta : delta;
+    const float sgn = delta < 0 ? -1.f : 1.f;
+    const __nv_bfloat16 *x1 = reinterpret_cast<const __nv_bfloat16 *>(&lo_in);
+    const __nv_bfloat16 *x2 = reinterpret_cast<const __nv_bfloat16 *>(&hi_in);
+    const float4 c0 = *reinterpret_cast<const float4 *>(cos_t + (size_t)a * half + 8 * c);
+    const float4 c1 = *reinterpret_cast<const float4 *>(cos_t + (size_t)a * half + 8 * c + 4);
+    const float4 s0 = *reinterpret_cast<const float4 *>(sin_t + (size_t)a * half + 8 * c);
+    const float4 s1 = *reinterpret_cast<const float4 *>(sin_t + (size_t)a * half + 8 * c + 4);
+    const float cs[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    const float sn[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+    uint32_t *o1 = reinterpret_cast<uint32_t *>(&lo_out);
+    uint32_t *o2 = reinterpret_cast<uint32_t *>(&hi_out);
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) {
+        float a0 = bf2f(x1[k]), a1 = bf2f(x1[k + 1]);
+        float b0 = bf2f(x2[k]), b1 = bf2f(x2[k + 1]);
+        float s0v = sgn * sn[k], s1v = sgn * sn[k + 1];
+        o1[k / 2] = pack_bf16x2(a0 * cs[k] - b0 * s0v, a1 * cs[k + 1] - b1 * s1v);
+        o2[k / 2] = pack_bf16x2(b0 * cs[k] + a0 * s0v, b1 * cs[k + 1] + a1 * s1v);
+    }
+}
+
+// One CTA per flat position; misses exit.  Each layer moves one K and one V
+// row (G*D bf16) with 16-byte vector loads/stores; K rotated in registers.
+__global__ void __launch_bounds__(128) gather_kv_kernel(
+    Arena A, const int64_t *__restrict__ req_off, int32_t n_req,
+    const int32_t *__restrict__ block_table, int32_t max_pages,
+    const int32_t *__restrict__ src_slot, const int32_t *__restrict__ src_cand,
+    const int32_t *__restrict__ slot_pages, int32_t slot_max_pages, int32_t l0, int32_t l1,
+    const float *__restrict__ cos_t, const float *__restrict__ sin_t) {
+    const int64_t t = blockIdx.x;
+    const int32_t slot = src_slot[t];
+    if (slot < 0) return;
+    int lo = 0, hi = n_req;
+    while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (req_off[mid] <= t) lo = mid; else hi = mid;
+    }
+    const int32_t pos = (int32_t)(t - req_off[lo]);
+    const int32_t cand = src_cand[t];
+    const int64_t dpage = block_table[(int64_t)lo * max_pages + pos / A.P];
+    const int64_t spage = slot_pages[(int64_t)slot * slot_max_pages + cand / A.P];
+    const int drow = pos % A.P, srow = cand % A.P;
+    const int half = A.D / 2, chunks = half / 8;            // 16-byte chunks per half head
+    const int kvec = A.G * chunks;                          // rotation work items per K row
+    const int vvec = A.G * A.D / 8;                         // 16-byte vectors per V row
+    const int32_t delta = pos - cand;
+    for (int layer = l0; layer < l1; ++layer) {
+        const uint4 *sk = reinterpret_cast<const uint4 *>(A.row(spage, layer, 0, srow));
+        const uint4 *sv = reinterpret_cast<const uint4 *>(A.row(spage, layer, 1, srow));
+        uint4 *dk = reinterpret_cast<uint4 *>(A.row(dpage, layer, 0, drow));
+        uint4 *dv = reinterpret_cast<uint4 *>(A.row(dpage, layer, 1, drow));
+        for (int v = threadIdx.x; v < vvec; v += blockDim.x) dv[v] = sv[v];
+        if (cos_t == nullptr || delta == 0) {
+            for (int v = threadIdx.x; v < vvec; v += blockDim.x) dk[v] = sk[v];
+        } else {
+            for (int it = threadIdx.x; it < kvec; it += blockDim.x) {
+                const int g = it / chunks, c = it % chunks;
+                const int vlo = g * (A.D / 8) + c, vhi = vlo + chunks;
+                uint4 lo_o, hi_o;
+                rope8(sk[vlo], sk[vhi], lo_o, hi_o, cos_t, sin_t, delta, half, c);
+                dk[vlo] = lo_o;
+                dk[vhi] = hi_o;
+            }
+        }
+    }
+}
+
+// One CTA per query row.  qkv row = [q (H*D) | k (G*D) | v (G*D)].
+__global__ void __launch_bounds__(256) qkv_rope_scatter_kernel(
+    const __nv_bfloat16 *__restrict__ qkv, int32_t H, Arena A, const int32_t *__restrict__ row_req,
+    const int32_t *__restrict__ row_pos, const uint8_t *__restrict__ write_kv, int32_t layer,
+    const int32_t *__restrict__ block_table, int32_t max_pages, const float *__restrict__ cos_t,
+    const float *__restrict__ sin_t, __nv_bfloat16 *__restrict__ q_out,
+    __nv_bfloat16 *__restrict__ k_out, __nv_bfloat16 *__restrict__ v_out) {
+    const int64_t row = blockIdx.x;
+    const int G = A.G, D = A.D, half = D / 2, chunks = half / 8;
+    const int64_t width = (int64_t)(H + 2 * G) * D;
+    const uint4 *src = reinterpret_cast<const uint4 *>(qkv + row * width);
+    const int32_t pos = row_pos[row];
+    const bool rope = cos_t != nullptr;
+    const bool wkv = write_kv == nullptr || write_kv[row] != 0;
+    uint4 *dk = nullptr, *dv = nullptr;
+    if (wkv) {
+        const int32_t r = row_req[row];
+        const int64_t page = block_table[(int64_t)r * max_pages + pos / A.P];
+        dk = reinterpret_cast<uint4 *>(A.row(page, layer, 0, pos % A.P));
+        dv = reinterpret_cast<uint4 *>(A.row(page, layer, 1, pos % A.P));
+    }
+    uint4 *qo = reinterpret_cast<uint4 *>(q_out + row * (int64_t)H * D);
+    uint4 *ko = k_out ? reinterpret_cast<uint4 *>(k_out + row * (int64_t)G * D) : nullptr;
+    uint4 *vo = v_out ? reinterpret_cast<uint4 *>(v_out + row * (int64_t)G * D) : nullptr;
+    const int vecs_per_head = D / 8;
+    // q and k: (H + G) heads x chunks rotation items
+    for (int it = threadIdx.x; it < (H + G) * chunks; it += blockDim.x) {
+        const int h = it / chunks, c = it % chunks;
+        const int vlo = h * vecs_per_head + c, vhi = vlo + chunks;
+        uint4 lo = src[vlo], hi = src[vhi];
+        if (rope) {
+            uint4 lo_o, hi_o;
+            rope8(lo, hi, lo_o, hi_o, cos_t, sin_t, pos, half, c);
+            lo = lo_o;
+            hi = hi_o;
+        }
+        if (h < H) {
+            qo[vlo] = lo;
+            qo[vhi] = hi;
+        } else {
+            const int kl = vlo - H * vecs_per_head, kh = vhi - H * vecs_per_head;
+            if (dk) { dk[kl] = lo; dk[kh] = hi; }
+            if (ko) { ko[kl] = lo; ko[kh] = hi; }
+        }
+    }
+    const int vbase = (H + G) * vecs_per_head;
+    for (int v = threadIdx.x; v < G * vecs_per_head; v += blockDim.x) {
+        const uint4 x = src[vbase + v];
+        if (dv) dv[v] = x;
+        if (vo) vo[v] = x;
+    }
+}
+
+// out[r] = table[ids[r]] (rows of `width` bf16).
+__global__ void embed_rows_kernel(const __nv_bfloat16 *__restrict__ table, int64_t width,
+                                  const int64_t *__restrict__ ids, const int32_t *__restrict__ rows,
+                                  __nv_bfloat16 *__restrict__ out) {
+    const int64_t r = blockIdx.x;
+    const int64_t id = ids[rows ? rows[r] : r];
+    const uint4 *s = reinterpret_cast<const uint4 *>(table + id * width);
+    uint4 *d = reinterpret_cast<uint4 *>(out + r * width);
+    for (int64_t v = threadIdx.x; v < width / 8; v += blockDim.x) d[v] = s[v];
+}
+
+// Row set S = non-reused U selected U {n-1} of each request.
+// Pass 1 (rows == nullptr): count per request.  Pass 2: compact in position
+// order starting at row_off[r], emitting flat token index, request, position
+// and whether the row's K/V are written fresh (non-reused or selected).
+__global__ void __launch_bounds__(1024) build_rows_kernel(
+    const int64_t *__restrict__ req_off, const int32_t *__restrict__ src_slot,
+    const uint8_t *__restrict__ selected, int32_t *__restrict__ counts,
+    const int64_t *__restrict__ row_off, int32_t *__restrict__ row_tok,
+    int32_t *__restrict__ row_req, int32_t *__restrict__ row_pos, uint8_t *__restrict__ write_kv) {
+    __shared__ int32_t warp_tot[32];
+    __shared__ int32_t carry;
+    const int r = blockIdx.x;
+    const int64_t s = req_off[r], n = req_off[r + 1] - s;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (threadIdx.x == 0) carry = 0;
+    __syncthreads();
+    for (int64_t base = 0; base < n; base += blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        bool in = false, fresh = false;
+        if (i < n) {
+            const bool reused = src_slot[s + i] >= 0;
+            const bool sel = selected != nullptr && selected[s + i] != 0;
+            fresh = !reused || sel;
+            in = fresh || i == n - 1;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, in);
+        const int before = __popc(bal & ((1u << lane) - 1));
+        if (lane == 0) warp_tot[wid] = __popc(bal);
+        __syncthreads();
+        int wbase = 0, tot = 0;
+        for (int k = 0; k < (int)(blockDim.x >> 5); ++k) {
+            if (k < wid) wbase += warp_tot[k];
+            tot += warp_tot[k];
+        }
+        if (in && row_tok != nullptr) {
+            const int64_t o = row_off[r] + carry + wbase + before;
+            row_tok[o] = (int32_t)(s + i);
+            row_req[o] = r;
+            row_pos[o] = (int32_t)i;
+            write_kv[o] = fresh ? 1 : 0;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) carry += tot;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0 && counts != nullptr) counts[r] = carry;
+}
+
+}  // namespace kvs
+
+using namespace kvs;
+
+extern "C" {
+
+kvs_status kvs_gather_kv(const kvs_kv_arena *arena, const kvs_batch *batch,
+                         const int32_t *src_slot, const int32_t *src_cand,
+                         const int32_t *slot_pages, int32_t slot_max_pages, int32_t layer_begin,
+                         int32_t layer_end, const kvs_rope *rope, kvs_stream_t stream) {
+    KVS_REQUIRE(arena && batch, KVS_EPARAM, "null arena/batch");
+    KVS_REQUIRE(arena->head_dim % 16 == 0, KVS_ESHAPE, "head_dim must be a multiple of 16");
+    KVS_REQUIRE(0 <= layer_begin && layer_begin <= layer_end && layer_end <= arena->num_layers,
+                KVS_EPARAM, "bad layer range");
+    if (batch->n_total <= 0 || layer_begin == layer_end) return KVS_OK;
+    KVS_REQUIRE(batch->n_total < (1ll << 31), KVS_EPARAM, "batch too large");
+    cudaStream_t s = (cudaStream_t)stream;
+    gather_kv_kernel<<<(unsigned)batch->n_total, 128, 0, s>>>(
+        make_arena(arena), batch->req_off, batch->n_req, batch->block_table, batch->max_pages,
+        src_slot, src_cand, slot_pages, slot_max_pages, layer_begin, layer_end,
+        rope ? rope->cos : nullptr, rope ? rope->sin : nullptr);
+    KVS_CHECK_LAUNCH("kvs_gather_kv");
+    return KVS_OK;
+}
+
+kvs_status kvs_qkv_rope_scatter(const void *qkv, int64_t n_rows, int32_t num_heads,
+                                const int32_t *row_req, const int32_t *row_pos,
+                                const uint8_t *write_kv, int32_t layer, const kvs_kv_arena *arena,
+                                const kvs_batch *batch, const kvs_rope *rope, void *q_out,
+                                void *k_out, void *v_out, kvs_stream_t stream) {
+    KVS_REQUIRE(arena && batch, KVS_EPARAM, "null arena/batch");
+    KVS_REQUIRE(arena->head_dim % 16 == 0, KVS_ESHAPE, "head_dim must be a multiple of 16");
+    KVS_REQUIRE(num_heads % arena->kv_heads == 0, KVS_ESHAPE, "num_heads % kv_heads != 0");
+    if (n_rows <= 0) return KVS_OK;
+    cudaStream_t s = (cudaStream_t)stream;
+    qkv_rope_scatter_kernel<<<(unsigned)n_rows, 256, 0, s>>>(
+        (const __nv_bfloat16 *)qkv, num_heads, make_arena(arena), row_req, row_pos, write_kv, layer,
+        batch->block_table, batch->max_pages, rope ? rope->cos : nullptr,
+        rope ? rope->sin : nullptr, (__nv_bfloat16 *)q_out, (__nv_bfloat16 *)k_out,
+        (__nv_bfloat16 *)v_out);
+    KVS_CHECK_LAUNCH("kvs_qkv_rope_scatter");
+    return KVS_OK;
+}
+
+kvs_status kvs_embed_rows(const void *table, int64_t width, const int64_t *ids,
+                          const int32_t *rows, int64_t n_rows, void *out, kvs_stream_t stream) {
+    KVS_REQUIRE(width % 8 == 0, KVS_ESHAPE, "embedding width must be a multiple of 8");
+    if (n_rows <= 0) return KVS_OK;
+    embed_rows_kernel<<<(unsigned)n_rows, 128, 0, (cudaStream_t)stream>>>(
+        (const __nv_bfloat16 *)table, width, ids, rows, (__nv_bfloat16 *)out);
+    KVS_CHECK_LAUNCH("kvs_embed_rows");
+    return KVS_OK;
+}
+
+kvs_status kvs_build_rows(const int64_t *req_off, int32_t n_req, const int32_t *src_slot,
+                          const uint8_t *selected, int32_t *counts, const int64_t *row_off,
+                          int32_t *row_tok, int32_t *row_req, int32_t *row_pos, uint8_t *write_kv,
+                          kvs_stream_t stream) {
+    KVS_REQUIRE(n_req >= 1, KVS_EPARAM, "n_req must be >= 1");
+    build_rows_kernel<<<n_req, 1024, 0, (cudaStream_t)stream>>>(
+        req_off, src_slot, selected, counts, row_off, row_tok, row_req, row_pos, write_kv);
+    KVS_CHECK_LAUNCH("kvs_build_rows");
+    return KVS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,493 @@
+"""Batched DHD prefill and decode on one GPU.
+
+Mirrors reference pkg/src/kvlab/engine.py (ReuseSession :47-171,
+prefill_with_selection :217-243, run_generation :298-328) and the reuse
+forward of model.py:163-227, re-shaped for the B200:
+
+prefill_batch(requests)                       one scheduled batch, all on device
+  R2   kvs_pool_lookup            hit maps for every request at once
+  G1   kvs_gather_kv              cached K/V rows (+RoPE re-alignment) into
+                                  each request's arena pages, all layers
+  probe fresh layer 0 over all rows (cuBLAS GEMMs + A1 on a scratch arena),
+       layer-1 QKV: q dense, k_true into the arena for non-reused rows,
+       v_true dense                                   (engine.py:182-207)
+  D1   kvs_dhd_alpha              attention mass per key (tcgen05 2-pass)
+  D2   kvs_dhd_select             dv-L1 x alpha, per-request radix top-B
+  rows kvs_build_rows             S = non-reused U selected U {n-1}
+  A1   layers 0..L-1 over rows S only: GEMM -> kvs_qkv_rope_scatter ->
+       kvs_attention_fwd (tcgen05) -> GEMM(+residual)
+
+decode_step(state, tokens)                    (engine.py:298-328, batched)
+  probe query of the new tokens (layer 0 + layer-1 q), D3
+  kvs_dhd_decode_select, then one layer-batched pass over chosen U {new}
+  rows with kvs_decode_attention.
+
+Only the projections are library GEMMs (torch.matmul -> cuBLAS); everything
+else is libkvshare.so.  The residual stream is fp32, GEMM operands bf16.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import InputError, ParameterError
+from .model import HEAD_DIM, ToyModel
+from .pool import PAGE_SIZE, CachePool, KVArena
+
+TILE = 128
+
+
+def budget(ratio: float, n_reused: int) -> int:
+    """selection.py:51-52 with the reference's IEEE-double ceil."""
+    return min(math.ceil(ratio * n_reused), n_reused)
+
+
+@dataclass
+class RowSet:
+    """Query rows of a forward pass (grouped by request, ascending position)."""
+
+    n_rows: int
+    row_tok: torch.Tensor      # int32 flat token index
+    row_req: torch.Tensor      # int32
+    row_pos: torch.Tensor      # int32
+    write_kv: torch.Tensor | None
+    row_off: np.ndarray        # host [R+1]
+    tiles: torch.Tensor | None = None   # int32 [3, n_tiles]
+    n_tiles: int = 0
+
+    def build_tiles(self, device):
+        req, row0, rows = [], [], []
+        for r in range(len(self.row_off) - 1):
+            a, b = int(self.row_off[r]), int(self.row_off[r + 1])
+            for s in range(a, b, TILE):
+                req.append(r)
+                row0.append(s)
+                rows.append(min(TILE, b - s))
+        self.n_tiles = len(req)
+        self.tiles = torch.tensor([req, row0, rows], dtype=torch.int32, device=device) \
+            if req else torch.zeros((3, 1), dtype=torch.int32, device=device)
+        return self
+
+
+@dataclass
+class BatchState:
+    """Device state of a batch of sequences (prefill and decode)."""
+
+    lengths: np.ndarray                 # prefill lengths
+    req_off_host: np.ndarray
+    req_off: torch.Tensor               # int64 [R+1]
+    tokens: torch.Tensor                # int64 flat prefill tokens
+    pages: list                         # per request page lists
+    block_table: torch.Tensor           # int32 [R, max_pages]
+    batch_c: N.Batch
+    capacity: np.ndarray                # token capacity per request
+    src_slot: torch.Tensor | None = None
+    src_cand: torch.Tensor | None = None
+    n_hit: np.ndarray | None = None
+    selected: torch.Tensor | None = None   # uint8 flat
+    dv_l1: torch.Tensor | None = None      # f32 flat (probe-layer deviation)
+    alpha: torch.Tensor | None = None
+    score: torch.Tensor | None = None
+    eligible: torch.Tensor | None = None   # uint8 flat (decode-stage)
+    budgets: np.ndarray | None = None
+    rows: RowSet | None = None
+    hidden_last: torch.Tensor | None = None  # fp32 [R, d_model]
+    ctx_len: np.ndarray | None = None
+    tokens_host: list = field(default_factory=list)
+
+
+class _ProbeArena:
+    """Scratch one-layer arena for the fresh layer-0 probe (all rows fresh)."""
+
+    def __init__(self):
+        self.data = None
+
+    def get(self, cfg, n_pages, device):
+        shape = (n_pages, 1, 2, PAGE_SIZE, cfg.kv_heads, HEAD_DIM)
+        if self.data is None or self.data.shape[0] < n_pages or self.data.shape[1:] != shape[1:]:
+            self.data = torch.zeros(shape, dtype=torch.bfloat16, device=device)
+        return N.KVArena(self.data.data_ptr(), self.data.shape[0], 1, cfg.kv_heads, HEAD_DIM,
+                         PAGE_SIZE)
+
+
+class Engine:
+    """Single-GPU executor of the KVShare hot path."""
+
+    def __init__(self, model: ToyModel, pool: CachePool):
+        self.model = model
+        self.pool = pool
+        self.cfg = model.config
+        self.device = model.device
+        self.arena: KVArena = pool.arena
+        self.scale = 1.0 / math.sqrt(self.cfg.d_k)
+        self._ws = {k: N.Workspace() for k in ("alpha", "select", "decode", "dsel")}
+        self._probe = _ProbeArena()
+        self.rope_c = None
+        if model.rope is not None:
+            self.rope_c = N.Rope(model.rope[0].data_ptr(), model.rope[1].data_ptr(),
+                                 self.cfg.max_positions)
+        self.probe_layer = 1 if self.cfg.num_layers >= 2 else 0
+
+    # ------------------------------------------------------------------ helpers
+    def _rope(self):
+        return self.rope_c
+
+    def new_batch(self, token_lists, decode_capacity: int = 0,
+                  tokens_dev: torch.Tensor | None = None) -> BatchState:
+        lens = np.array([len(t) for t in token_lists], dtype=np.int64)
+        if (lens <= 0).any():
+            raise InputError("token sequence must be a non-empty 1-D array")
+        off = np.zeros(len(lens) + 1, dtype=np.int64)
+        off[1:] = np.cumsum(lens)
+        if lens.max() + decode_capacity > self.cfg.max_positions:
+            raise InputError("sequence longer than max_positions")
+        dev = self.device
+        if tokens_dev is None:
+            flat = np.concatenate([np.asarray(t, dtype=np.int64) for t in token_lists])
+            for t in token_lists:
+                self.model.check_tokens(np.asarray(t, dtype=np.int64))
+            tokens_dev = torch.from_numpy(flat).to(dev, non_blocking=True)
+        cap = lens + decode_capacity
+        pages = [self.arena.alloc(self.arena.pages_for(int(c))) for c in cap]
+        maxp = max(len(p) for p in pages)
+        bt = np.zeros((len(lens), maxp), dtype=np.int32)
+        for r, p in enumerate(pages):
+            bt[r, :len(p)] = p
+        req_off = torch.from_numpy(off).to(dev, non_blocking=True)
+        block_table = torch.from_numpy(bt).to(dev, non_blocking=True)
+        bc = N.Batch(len(lens), int(off[-1]), req_off.data_ptr(), block_table.data_ptr(), maxp)
+        st = BatchState(lens, off, req_off, tokens_dev, pages, block_table, bc, cap)
+        st.ctx_len = lens.copy()
+        st._keep = (req_off, block_table)
+        return st
+
+    def release(self, st: BatchState) -> None:
+        for p in st.pages:
+            self.arena.release(p)
+        st.pages = []
+
+    def _rows_all(self, st: BatchState) -> RowSet:
+        """Every position of every request (probe / full recompute)."""
+        dev = self.device
+        n = int(st.req_off_host[-1])
+        req = np.repeat(np.arange(len(st.lengths), dtype=np.int32), st.lengths)
+        pos = np.concatenate([np.arange(l, dtype=np.int32) for l in st.lengths])
+        rs = RowSet(n, torch.arange(n, dtype=torch.int32, device=dev),
+                    torch.from_numpy(req).to(dev), torch.from_numpy(pos).to(dev), None,
+                    st.req_off_host.copy())
+        return rs.build_tiles(dev)
+
+    def _attention(self, q, rows: RowSet, layer: int, arena_c, batch_c, out, lse=None):
+        N.call("kvs_attention_fwd", q.data_ptr(), rows.row_pos.data_ptr(), rows.n_rows,
+               self.cfg.num_heads, rows.tiles[0].data_ptr(), rows.tiles[1].data_ptr(),
+               rows.tiles[2].data_ptr(), rows.n_tiles, None, 1, layer, arena_c, batch_c,
+               self.scale, N.ptr(out), N.ptr(lse), N.stream_ptr())
+
+    def _decode_attention(self, q, rows: RowSet, layer: int, arena_c, batch_c, out, max_kv):
+        cfg = self.cfg
+        nb = N.ws_bytes("kvs_decode_attention_workspace", rows.n_rows, cfg.num_heads,
+                        cfg.kv_heads, HEAD_DIM, max_kv)
+        ws = self._ws["decode"].get(nb, self.device)
+        N.call("kvs_decode_attention", q.data_ptr(), rows.row_req.data_ptr(),
+               rows.row_pos.data_ptr(), rows.n_rows, cfg.num_heads, None, 1, layer, arena_c,
+               batch_c, self.scale, out.data_ptr(), ws.data_ptr(), ws.numel(), N.stream_ptr())
+
+    def _scatter(self, qkv, rows: RowSet, layer, arena_c, batch_c, q_out, write_kv=None,
+                 k_out=None, v_out=None, use_write=True):
+        wk = write_kv if write_kv is not None else (rows.write_kv if use_write else None)
+        N.call("kvs_qkv_rope_scatter", qkv.data_ptr(), rows.n_rows, self.cfg.num_heads,
+               rows.row_req.data_ptr(), rows.row_pos.data_ptr(), N.ptr(wk), layer, arena_c,
+               batch_c, self._rope(), q_out.data_ptr(), N.ptr(k_out), N.ptr(v_out),
+               N.stream_ptr())
+
+    def _embed(self, tokens_flat, rows: RowSet) -> torch.Tensor:
+        x = torch.empty(rows.n_rows, self.cfg.d_model, dtype=torch.bfloat16, device=self.device)
+        N.call("kvs_embed_rows", self.model.embedding.data_ptr(), self.cfg.d_model,
+               tokens_flat.data_ptr(), rows.row_tok.data_ptr(), rows.n_rows, x.data_ptr(),
+               N.stream_ptr())
+        return x.float()
+
+    def forward_rows(self, x, rows: RowSet, layers, arena_c, batch_c, decode=False,
+                     max_kv=0, write_kv_per_layer=None, capture=None):
+        """Layer loop over a row set: x (fp32 [n, d_model]) updated in place."""
+        cfg, m = self.cfg, self.model
+        H, n = cfg.num_heads, rows.n_rows
+        q = torch.empty(n, H, HEAD_DIM, dtype=torch.bfloat16, device=self.device)
+        o = torch.empty_like(q)
+        for layer in layers:
+            qkv = x.to(torch.bfloat16) @ m.w_qkv[layer]
+            wk = write_kv_per_layer[layer] if write_kv_per_layer is not None else None
+            self._scatter(qkv, rows, layer, arena_c, batch_c, q, write_kv=wk)
+            if decode:
+                self._decode_attention(q, rows, layer, arena_c, batch_c, o, max_kv)
+            else:
+                self._attention(q, rows, layer, arena_c, batch_c, o)
+            if capture is not None:
+                capture.append((layer, q.clone(), o.clone()))
+            x += (o.view(n, H * HEAD_DIM) @ m.w_o[layer]).float()
+            if capture is not None:
+                capture.append((layer, "hidden", x.clone()))
+        return x
+
+    # ------------------------------------------------------------------ prefill
+    def lookup(self, st: BatchState):
+        res = self.pool.lookup_device(st.tokens, st.req_off, st.req_off_host)
+        st.src_slot, st.src_cand = res.src_slot, res.src_cand
+        st.n_hit = res.n_hit.cpu().numpy().astype(np.int64)        # sync 1
+        st._contributed = res.contributed
+        return st
+
+    def gather(self, st: BatchState):
+        if st.n_hit is None or st.n_hit.sum() == 0:
+            return
+        idx = self.pool._build_index()
+        N.call("kvs_gather_kv", self.arena.c, st.batch_c, st.src_slot.data_ptr(),
+               st.src_cand.data_ptr(), idx["slot_pages"].data_ptr(), idx["slot_max_pages"], 0,
+               self.cfg.num_layers, self._rope(), N.stream_ptr())
+
+    def _probe(self, st: BatchState, write_k: bool = True):
+        """engine.py:182-207: fresh layers below the probe over ALL rows (on a
+        scratch arena), then the probe layer's q (dense), k_true (into the
+        arena for non-reused rows, so the arena layer holds k_pert) and
+        v_true (dense)."""
+        cfg, m, dev = self.cfg, self.model, self.device
+        H, G = cfg.num_heads, cfg.kv_heads
+        rows = self._rows_all(st)
+        n = rows.n_rows
+        x = self._embed(st.tokens, rows)
+        p = self.probe_layer
+        if p == 1:
+            npages = int(sum((l + PAGE_SIZE - 1) // PAGE_SIZE for l in st.lengths))
+            parena = self._probe.get(cfg, npages, dev)
+            bt = np.zeros((len(st.lengths), st.block_table.shape[1]), dtype=np.int32)
+            base = 0
+            for r, l in enumerate(st.lengths):
+                k = (l + PAGE_SIZE - 1) // PAGE_SIZE
+                bt[r, :k] = np.arange(base, base + k)
+                base += k
+            pbt = torch.from_numpy(bt).to(dev, non_blocking=True)
+            pbatch = N.Batch(st.batch_c.n_req, st.batch_c.n_total, st.req_off.data_ptr(),
+                             pbt.data_ptr(), bt.shape[1])
+            q = torch.empty(n, H, HEAD_DIM, dtype=torch.bfloat16, device=dev)
+            o = torch.empty_like(q)
+            qkv = x.to(torch.bfloat16) @ m.w_qkv[0]
+            self._scatter(qkv, rows, 0, parena, pbatch, q, use_write=False)
+            self._attention(q, rows, 0, parena, pbatch, o)
+            x += (o.view(n, H * HEAD_DIM) @ m.w_o[0]).float()
+            st._probe_keep = pbt
+        qkv = x.to(torch.bfloat16) @ m.w_qkv[p]
+        q1 = torch.empty(n, H, HEAD_DIM, dtype=torch.bfloat16, device=dev)
+        v_true = torch.empty(n, G, HEAD_DIM, dtype=torch.bfloat16, device=dev)
+        wk = (st.src_slot < 0).to(torch.uint8) if write_k else \
+            torch.zeros(n, dtype=torch.uint8, device=dev)
+        self._scatter(qkv, rows, p, self.arena.c, st.batch_c, q1, write_kv=wk, v_out=v_true)
+        return rows, q1, v_true
+
+    def _select(self, st: BatchState, v_true, alpha, budgets: np.ndarray):
+        dev, n = self.device, int(st.req_off_host[-1])
+        bud = torch.from_numpy(budgets.astype(np.int32)).to(dev, non_blocking=True)
+        dv = torch.empty(n, dtype=torch.float32, device=dev)
+        score = torch.empty(n, dtype=torch.float32, device=dev)
+        sel = torch.empty(n, dtype=torch.uint8, device=dev)
+        N.call("kvs_dhd_select", v_true.data_ptr(), alpha.data_ptr(), st.src_slot.data_ptr(),
+               self.probe_layer, self.arena.c, st.batch_c, bud.data_ptr(), dv.data_ptr(),
+               score.data_ptr(), sel.data_ptr(), None, 0, N.stream_ptr())
+        st._bud = bud
+        return dv, score, sel
+
+    def probe_and_select(self, st: BatchState, ratio: float):
+        """engine.py:233-243 (PRACTICAL): fresh probe, D1 alpha, D2 select."""
+        cfg, dev = self.cfg, self.device
+        H, G = cfg.num_heads, cfg.kv_heads
+        rows, q1, v_true = self._probe(st)
+        n = rows.n_rows
+        alpha = torch.empty(n, dtype=torch.float32, device=dev)
+        ws = self._ws["alpha"].get(N.ws_bytes("kvs_dhd_alpha_workspace", n, H, G), dev)
+        N.call("kvs_dhd_alpha", q1.data_ptr(), H, 1, self.probe_layer, self.arena.c, st.batch_c,
+               rows.row_pos.data_ptr(), rows.tiles[0].data_ptr(), rows.tiles[1].data_ptr(),
+               rows.tiles[2].data_ptr(), rows.n_tiles, None, self.scale, alpha.data_ptr(),
+               ws.data_ptr(), ws.numel(), N.stream_ptr())
+        st.budgets = np.array([budget(ratio, int(h)) for h in st.n_hit], dtype=np.int32)
+        st.dv_l1, st.score, st.selected = self._select(st, v_true, alpha, st.budgets)
+        st.alpha = alpha
+        st._probe_q, st._probe_v_true = q1, v_true
+        return st
+
+    def build_rows(self, st: BatchState, selected: torch.Tensor | None) -> RowSet:
+        dev, R = self.device, len(st.lengths)
+        counts = torch.empty(R, dtype=torch.int32, device=dev)
+        src = st.src_slot if st.src_slot is not None else \
+            torch.full((int(st.req_off_host[-1]),), -1, dtype=torch.int32, device=dev)
+        N.call("kvs_build_rows", st.req_off.data_ptr(), R, src.data_ptr(), N.ptr(selected),
+               counts.data_ptr(), None, None, None, None, None, N.stream_ptr())
+        c = counts.cpu().numpy().astype(np.int64)                         # sync 2
+        off = np.zeros(R + 1, dtype=np.int64)
+        off[1:] = np.cumsum(c)
+        n = int(off[-1])
+        row_off = torch.from_numpy(off).to(dev)
+        rows = RowSet(n, torch.empty(n, dtype=torch.int32, device=dev),
+                      torch.empty(n, dtype=torch.int32, device=dev),
+                      torch.empty(n, dtype=torch.int32, device=dev),
+                      torch.empty(n, dtype=torch.uint8, device=dev), off)
+        N.call("kvs_build_rows", st.req_off.data_ptr(), R, src.data_ptr(), N.ptr(selected),
+               None, row_off.data_ptr(), rows.row_tok.data_ptr(), rows.row_req.data_ptr(),
+               rows.row_pos.data_ptr(), rows.write_kv.data_ptr(), N.stream_ptr())
+        rows._keep = (row_off, src)
+        return rows.build_tiles(dev)
+
+    def session_forward(self, st: BatchState, rows: RowSet, capture=None):
+        x = self._embed(st.tokens, rows)
+        self.forward_rows(x, rows, range(self.cfg.num_layers), self.arena.c, st.batch_c,
+                          capture=capture)
+        last = torch.from_numpy(rows.row_off[1:] - 1).to(self.device)
+        st.rows = rows
+        st.hidden_last = x[last]
+        st._x_rows = x
+        return x
+
+    def prefill_batch(self, token_lists, ratio: float = 0.2, mode: str = "selective",
+                      decode_capacity: int = 0, tokens_dev=None) -> BatchState:
+        """One scheduled batch through the hot path (modes: selective / naive / full)."""
+        if not 0.0 <= ratio <= 1.0:
+            raise ParameterError(f"ratio must lie in [0, 1], got {ratio}")
+        st = self.new_batch(token_lists, decode_capacity, tokens_dev)
+        if mode == "full" or not self.pool.entries:
+            st.n_hit = np.zeros(len(st.lengths), dtype=np.int64)
+            rows = self.build_rows(st, None)
+            rows.write_kv.fill_(1)
+            self.session_forward(st, rows)
+            st.selected = None
+            return st
+        self.lookup(st)
+        self.gather(st)
+        if mode == "selective" and ratio > 0 and st.n_hit.sum() > 0:
+            self.probe_and_select(st, ratio)
+            rows = self.build_rows(st, st.selected)
+        else:
+            rows = self.build_rows(st, None)
+            st.selected = None
+        self.session_forward(st, rows)
+        reused = st.src_slot >= 0
+        sel = st.selected.bool() if st.selected is not None else torch.zeros_like(reused)
+        st.eligible = (reused & ~sel).to(torch.uint8)
+        return st
+
+    def refresh_lru(self, st: BatchState):
+        c = st._contributed.cpu().numpy()
+        for r in range(c.shape[0]):
+            self.pool.refresh_lru(c[r])
+
+    # ------------------------------------------------------------------ decode
+    def ensure_dv(self, st: BatchState):
+        """delta_v_probe support (engine.py:81-89, 140-148) for batches that did
+        not run the DHD probe: v_true from a fresh probe (no arena writes),
+        dv-L1 against the cached probe-layer V."""
+        if st.dv_l1 is not None:
+            return
+        n = int(st.req_off_host[-1])
+        if st.src_slot is None or st.n_hit is None or st.n_hit.sum() == 0:
+            st.dv_l1 = torch.zeros(n, dtype=torch.float32, device=self.device)
+            return
+        _, _, v_true = self._probe(st, write_k=False)
+        zeros = torch.zeros(n, dtype=torch.float32, device=self.device)
+        st.dv_l1, _, _ = self._select(st, v_true, zeros, np.zeros(len(st.lengths), np.int32))
+
+    def _decode_rows(self, st: BatchState, chosen: list[list[int]], new_tokens) -> RowSet:
+        req, pos, tok_idx = [], [], []
+        off = [0]
+        for r, ch in enumerate(chosen):
+            for c in ch:
+                req.append(r)
+                pos.append(c)
+            req.append(r)
+            pos.append(int(st.ctx_len[r]))
+            off.append(len(req))
+        dev = self.device
+        rs = RowSet(len(req), torch.arange(len(req), dtype=torch.int32, device=dev),
+                    torch.tensor(req, dtype=torch.int32, device=dev),
+                    torch.tensor(pos, dtype=torch.int32, device=dev), None,
+                    np.array(off, dtype=np.int64))
+        return rs
+
+    def probe_query(self, st: BatchState, new_tokens: np.ndarray) -> torch.Tensor:
+        """query_rows_probe (engine.py:150-171) for every request's next token:
+        layers below the probe over cache + own row, then the probe-layer q."""
+        cfg, dev = self.cfg, self.device
+        R = len(st.lengths)
+        rows = RowSet(R, torch.arange(R, dtype=torch.int32, device=dev),
+                      torch.arange(R, dtype=torch.int32, device=dev),
+                      torch.from_numpy(st.ctx_len.astype(np.int32)).to(dev), None,
+                      np.arange(R + 1, dtype=np.int64))
+        tok = torch.from_numpy(np.asarray(new_tokens, dtype=np.int64)).to(dev)
+        x = self._embed(tok, rows)
+        max_kv = int(st.capacity.max())
+        self.forward_rows(x, rows, range(self.probe_layer), self.arena.c, st.batch_c,
+                          decode=True, max_kv=max_kv)
+        qkv = x.to(torch.bfloat16) @ self.model.w_qkv[self.probe_layer]
+        q = torch.empty(R, cfg.num_heads, HEAD_DIM, dtype=torch.bfloat16, device=dev)
+        zero = torch.zeros(R, dtype=torch.uint8, device=dev)
+        self._scatter(qkv, rows, self.probe_layer, self.arena.c, st.batch_c, q, write_kv=zero)
+        return q
+
+    def decode_select(self, st: BatchState, q_t: torch.Tensor, n_extra: int):
+        """D3 (selection.py:80-105) for every request; updates eligibility."""
+        cfg, dev, R = self.cfg, self.device, len(st.lengths)
+        ctx = torch.from_numpy(st.ctx_len.astype(np.int32)).to(dev)
+        max_ctx = int(st.ctx_len.max())
+        chosen = torch.empty(R, max(n_extra, 1), dtype=torch.int32, device=dev)
+        nch = torch.zeros(R, dtype=torch.int32, device=dev)
+        ws = self._ws["dsel"].get(N.ws_bytes("kvs_dhd_decode_select_workspace", R, cfg.num_heads,
+                                             max_ctx), dev)
+        N.call("kvs_dhd_decode_select", q_t.data_ptr(), cfg.num_heads, ctx.data_ptr(), max_ctx,
+               st.dv_l1.data_ptr(), st.eligible.data_ptr(), self.probe_layer, self.arena.c,
+               st.batch_c, n_extra, self.scale, chosen.data_ptr(), nch.data_ptr(), None,
+               ws.data_ptr(), ws.numel(), N.stream_ptr())
+        ch, nc = chosen.cpu().numpy(), nch.cpu().numpy()
+        return [[int(x) for x in ch[r, :nc[r]]] for r in range(R)]
+
+    def decode_step(self, st: BatchState, new_tokens, n_extra: int):
+        """One decode token per request (engine.py:312-327): probe query, D3
+        selection, then chosen rows + new token as one layer-batched pass."""
+        R = len(st.lengths)
+        new_tokens = np.asarray(new_tokens, dtype=np.int64).reshape(R)
+        if (st.ctx_len + 1 > st.capacity).any():
+            raise InputError("decode capacity exhausted")
+        chosen = [[] for _ in range(R)]
+        if n_extra > 0 and st.eligible is not None and bool(st.eligible.any()):
+            self.ensure_dv(st)
+            q_t = self.probe_query(st, new_tokens)
+            chosen = self.decode_select(st, q_t, n_extra)
+        rows = self._decode_rows(st, chosen, new_tokens)
+        dev = self.device
+        if not st.tokens_host:
+            flat = st.tokens.cpu().numpy()
+            st.tokens_host = [list(flat[st.req_off_host[r]:st.req_off_host[r + 1]])
+                              for r in range(R)]
+        tok_rows = []
+        for r, ch in enumerate(chosen):
+            tok_rows += [int(st.tokens_host[r][c]) for c in ch]
+            tok_rows.append(int(new_tokens[r]))
+        tok = torch.tensor(tok_rows, dtype=torch.int64, device=dev)
+        x = self._embed(tok, rows)
+        self.forward_rows(x, rows, range(self.cfg.num_layers), self.arena.c, st.batch_c,
+                          decode=True, max_kv=int(st.capacity.max()))
+        last = torch.from_numpy(rows.row_off[1:] - 1).to(dev)
+        for r in range(R):
+            st.tokens_host[r].append(int(new_tokens[r]))
+        st.ctx_len = st.ctx_len + 1
+        return x[last], chosen
+
+    # ------------------------------------------------------------------ write-back
+    def write_back(self, st: BatchState, request_ids) -> None:
+        """Finished requests become pool entries (zero-copy; simulate.py:207-210)."""
+        flat = None
+        for r, rid in enumerate(request_ids):
+            if flat is None:
+                flat = st.tokens.cpu().numpy()
+            toks = flat[st.req_off_host[r]:st.req_off_host[r + 1]]
+            self.pool.insert_pages(rid, toks, st.pages[r])
+        st.pages = []

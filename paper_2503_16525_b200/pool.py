@@ -1,0 +1,410 @@
+"""Per-GPU shared KV pool: paged bf16 KV arena + replicated token index.
+
+Mirrors reference pkg/src/kvlab/pool.py: ``KVEntry`` (:35-55), ``ReuseMap``
+(:58-75) and ``CachePool`` (:78-172) keep their names, arguments and error
+behaviour.  What changes is where things live:
+
+* K/V rows live in one paged bf16 arena on the GPU (``KVArena``); an entry is
+  a list of pages (64 tokens each, layout in include/kvshare.h).  Request
+  caches use the same arena, so writing a finished request back to the pool
+  is zero-copy (``insert_pages``).
+* The token side (entry tokens, window hashes, a hash-sorted window list and
+  the recency ranks) is a device index queried by the R2 lookup kernel
+  (``kvs_pool_lookup``) for a whole scheduled batch at once.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import CacheError, ParameterError
+from .matching import HashParams, window_hashes_device
+from .model import HEAD_DIM, ModelConfig
+
+PAGE_SIZE = 64
+
+
+class KVArena:
+    """Paged KV storage [pages][L][2][64][kv_heads][128] bf16 with a free list."""
+
+    def __init__(self, config: ModelConfig, num_pages: int, device="cuda",
+                 page_size: int = PAGE_SIZE):
+        self.config = config
+        self.page_size = page_size
+        self.device = torch.device(device)
+        self.data = torch.zeros(num_pages, config.num_layers, 2, page_size, config.kv_heads,
+                                HEAD_DIM, dtype=torch.bfloat16, device=self.device)
+        self._free = list(range(num_pages - 1, -1, -1))
+        self.c = N.KVArena(self.data.data_ptr(), num_pages, config.num_layers, config.kv_heads,
+                           HEAD_DIM, page_size)
+
+    @property
+    def num_pages(self) -> int:
+        return self.data.shape[0]
+
+    @property
+    def free_pages(self) -> int:
+        return len(self._free)
+
+    def pages_for(self, n_tokens: int) -> int:
+        return (n_tokens + self.page_size - 1) // self.page_size
+
+    def alloc(self, n: int) -> list[int]:
+        if n > len(self._free):
+            raise CacheError(f"KV arena exhausted: need {n} pages, {len(self._free)} free")
+        return [self._free.pop() for _ in range(n)]
+
+    def release(self, pages) -> None:
+        self._free.extend(int(p) for p in pages)
+
+    @staticmethod
+    def bytes_per_page(config: ModelConfig, page_size: int = PAGE_SIZE) -> int:
+        return config.num_layers * 2 * page_size * config.kv_heads * HEAD_DIM * 2
+
+    def rows(self, pages, n: int, layer: int, kv: int) -> torch.Tensor:
+        """Gather rows [0, n) of a page list at (layer, kv): [n, kv_heads, 128]."""
+        p = torch.as_tensor(list(pages), device=self.device, dtype=torch.long)
+        x = self.data[p, layer, kv]  # [pages, 64, G, 128]
+        return x.reshape(-1, self.config.kv_heads, HEAD_DIM)[:n]
+
+
+@dataclass
+class KVEntry:
+    """One cached request (pool.py:35-55): tokens plus its arena pages."""
+
+    request_id: str
+    tokens: np.ndarray
+    pages: list
+    pool: "CachePool" = field(repr=False)
+    slot: int = -1
+    last_access: int = 0
+    insert_seq: int = 0
+
+    @property
+    def n_tokens(self) -> int:
+        return int(self.tokens.size)
+
+    @property
+    def size_bytes(self) -> int:
+        """Serialized (KVSH) size, pool.py:51-55."""
+        cfg = self.pool.config
+        return (4 + len(self.request_id.encode()) + 4 + 4 * self.n_tokens + 12
+                + 2 * 4 * cfg.num_layers * cfg.kv_heads * self.n_tokens * cfg.d_k)
+
+    def _kv(self, kv: int) -> np.ndarray:
+        arena, cfg = self.pool.arena, self.pool.config
+        out = []
+        for layer in range(cfg.num_layers):
+            rows = arena.rows(self.pages, self.n_tokens, layer, kv)   # [n, G, 128]
+            rows = rows[..., torch.as_tensor(self.pool.pad_index, device=rows.device)]
+            out.append(rows.float().permute(1, 0, 2).cpu().numpy())
+        return np.stack(out).astype(np.float64)                      # (L, G, n, d_k)
+
+    @property
+    def k(self) -> np.ndarray:
+        return self._kv(0)
+
+    @property
+    def v(self) -> np.ndarray:
+        return self._kv(1)
+
+    @property
+    def window_hash_set(self) -> frozenset:
+        h = self.pool._slot_hash[self.slot]
+        return frozenset(int(x) for x in h.cpu().numpy()) if h is not None else frozenset()
+
+
+@dataclass
+class ReuseMap:
+    """Alignment of a request's positions onto cached K/V rows (pool.py:58-75).
+
+    ``sources`` is the reference's ``{pos: (KVEntry, cand_pos)}``; the device
+    form (``src_slot``/``src_cand``, int32 per position) is what the engine
+    consumes without leaving the GPU."""
+
+    length: int
+    sources: dict = field(default_factory=dict)
+    src_slot: torch.Tensor | None = None
+    src_cand: torch.Tensor | None = None
+
+    @property
+    def hit_rate(self) -> float:
+        return len(self.sources) / self.length if self.length else 0.0
+
+    def validate(self, tokens) -> None:
+        tokens = np.asarray(tokens, dtype=np.int64)
+        for pos, (entry, cand_pos) in self.sources.items():
+            if tokens[pos] != entry.tokens[cand_pos]:
+                raise CacheError(f"reuse map position {pos} maps to a different token")
+
+
+@dataclass
+class BatchLookup:
+    """Device hit maps of a batched lookup (flat over the batch)."""
+
+    req_off: torch.Tensor          # int64 [R+1]
+    tokens: torch.Tensor           # int64 [n_total]
+    src_slot: torch.Tensor         # int32 [n_total]
+    src_cand: torch.Tensor         # int32 [n_total]
+    n_hit: torch.Tensor            # int32 [R] (device)
+    contributed: torch.Tensor      # uint8 [R, n_slots]
+
+
+class CachePool:
+    """KV entries indexed by content; most-recent insertion wins (pool.py:78-172)."""
+
+    def __init__(self, config: ModelConfig, params: HashParams | None = None,
+                 capacity_bytes: int | None = None, *, arena: KVArena | None = None,
+                 arena_pages: int | None = None, device="cuda"):
+        self.config = config
+        self.params = params or HashParams()
+        self.capacity_bytes = capacity_bytes
+        self.device = torch.device(device)
+        if arena is None:
+            arena = KVArena(config, arena_pages or 256, device)
+        self.arena = arena
+        from .model import _pad_index
+        self.pad_index = _pad_index(config.d_k)
+        self.entries: dict[str, KVEntry] = {}
+        self._counter = 0
+        self._slots: list[KVEntry | None] = []
+        self._slot_tokens: list[torch.Tensor | None] = []
+        self._slot_hash: list[torch.Tensor | None] = []
+        self._dirty = True
+        self._index = None
+        self._ws = N.Workspace()
+
+    # ------------------------------------------------------------------ basics
+    def __len__(self) -> int:
+        return len(self.entries)
+
+    @property
+    def total_bytes(self) -> int:
+        return sum(e.size_bytes for e in self.entries.values())
+
+    def _tick(self) -> int:
+        self._counter += 1
+        return self._counter
+
+    def _validate_tokens(self, tokens) -> np.ndarray:
+        tokens = np.asarray(tokens, dtype=np.int64)
+        if tokens.ndim != 1 or tokens.size == 0:
+            raise CacheError("entry tokens must be a non-empty 1-D sequence")
+        if tokens.min() < 0 or tokens.max() >= 2**32:
+            raise CacheError("token ids must fit an unsigned 32-bit integer")
+        return tokens
+
+    # ------------------------------------------------------------------ insert
+    def _new_slot(self) -> int:
+        for i, e in enumerate(self._slots):
+            if e is None:
+                return i
+        self._slots.append(None)
+        self._slot_tokens.append(None)
+        self._slot_hash.append(None)
+        return len(self._slots) - 1
+
+    def _drop(self, entry: KVEntry, release: bool = True) -> None:
+        self.entries.pop(entry.request_id, None)
+        self._slots[entry.slot] = None
+        self._slot_tokens[entry.slot] = None
+        self._slot_hash[entry.slot] = None
+        if release:
+            self.arena.release(entry.pages)
+        self._dirty = True
+
+    def insert_pages(self, request_id: str, tokens, pages) -> KVEntry:
+        """Register K/V already resident in arena pages (zero-copy write-back
+        of a finished request, simulate.py:207-210)."""
+        tokens = self._validate_tokens(tokens)
+        old = self.entries.get(request_id)
+        if old is not None:
+            self._drop(old, release=set(old.pages) != set(pages))
+        seq = self._tick()
+        slot = self._new_slot()
+        entry = KVEntry(request_id, tokens.copy(), list(pages), self, slot, seq, seq)
+        tok_dev = torch.from_numpy(tokens).to(self.device)
+        self._slots[slot] = entry
+        self._slot_tokens[slot] = tok_dev
+        self._slot_hash[slot] = window_hashes_device(tok_dev, self.params)
+        self.entries[request_id] = entry
+        self._dirty = True
+        if self.capacity_bytes is not None:
+            self.evict_to_capacity(self.capacity_bytes)
+        return entry
+
+    def insert(self, request_id: str, tokens, k, v) -> None:
+        """pool.py:100-123: store host K/V (L, kv_heads, n, d_k); replaces any
+        entry with the same id."""
+        cfg = self.config
+        tokens = self._validate_tokens(tokens)
+        k = torch.as_tensor(np.asarray(k, float) if not torch.is_tensor(k) else k)
+        v = torch.as_tensor(np.asarray(v, float) if not torch.is_tensor(v) else v)
+        expected = (cfg.num_layers, cfg.kv_heads, tokens.size, cfg.d_k)
+        if tuple(k.shape) != expected or tuple(v.shape) != expected:
+            raise CacheError(f"K/V shape {tuple(k.shape)} does not match pool config {expected}")
+        pages = self.arena.alloc(self.arena.pages_for(tokens.size))
+        self.write_rows(pages, k, v)
+        self.insert_pages(request_id, tokens, pages)
+
+    def write_rows(self, pages, k: torch.Tensor, v: torch.Tensor) -> None:
+        """Copy (L, G, n, d_k) K/V into pages (padded lanes, bf16)."""
+        cfg, P = self.config, self.arena.page_size
+        n = k.shape[2]
+        pidx = torch.as_tensor(self.pad_index, device=self.device)
+        for kv, x in ((0, k), (1, v)):
+            x = x.to(self.device, torch.float32).permute(0, 2, 1, 3)   # L, n, G, d
+            full = torch.zeros(cfg.num_layers, len(pages) * P, cfg.kv_heads, HEAD_DIM,
+                               device=self.device)
+            full[:, :n][..., pidx] = x
+            full = full.reshape(cfg.num_layers, len(pages), P, cfg.kv_heads, HEAD_DIM)
+            pt = torch.as_tensor(list(pages), device=self.device, dtype=torch.long)
+            self.arena.data[pt, :, kv] = full.permute(1, 0, 2, 3, 4).to(torch.bfloat16)
+
+    # ------------------------------------------------------------------ index
+    def _build_index(self):
+        if not self._dirty and self._index is not None:
+            return self._index
+        live = [i for i, e in enumerate(self._slots) if e is not None]
+        n_slots = len(self._slots)
+        dev = self.device
+        tok_off = np.zeros(n_slots + 1, dtype=np.int64)
+        win_off = np.zeros(n_slots + 1, dtype=np.int64)
+        toks, hashes, wslot = [], [], []
+        for s in range(n_slots):
+            t = self._slot_tokens[s]
+            n = 0 if t is None else t.numel()
+            nw = 0 if t is None else self._slot_hash[s].numel()
+            tok_off[s + 1] = tok_off[s] + n
+            win_off[s + 1] = win_off[s] + nw
+            if t is not None:
+                toks.append(t)
+                hashes.append(self._slot_hash[s])
+                wslot.append(torch.full((nw,), s, dtype=torch.int32, device=dev))
+        n_windows = int(win_off[-1])
+        tokens = torch.cat(toks) if toks else torch.zeros(1, dtype=torch.int64, device=dev)
+        win_hash = torch.cat(hashes) if hashes else torch.zeros(1, dtype=torch.int64, device=dev)
+        win_slot = torch.cat(wslot) if wslot else torch.zeros(1, dtype=torch.int32, device=dev)
+        sorted_hash = torch.empty(max(n_windows, 1), dtype=torch.int64, device=dev)
+        sorted_widx = torch.empty(max(n_windows, 1), dtype=torch.int32, device=dev)
+        if n_windows:
+            ws = self._ws.get(N.ws_bytes("kvs_index_sort_workspace", n_windows), dev)
+            N.call("kvs_index_sort", win_hash.data_ptr(), n_windows, sorted_hash.data_ptr(),
+                   sorted_widx.data_ptr(), ws.data_ptr(), ws.numel(), N.stream_ptr())
+        order = sorted(live, key=lambda s: -self._slots[s].insert_seq)
+        rank = np.full(max(n_slots, 1), -1, dtype=np.int32)
+        r2s = np.zeros(max(n_slots, 1), dtype=np.int32)
+        for r, s in enumerate(order):
+            rank[s] = r
+            r2s[r] = s
+        idx = dict(tokens=tokens, tok_off=torch.from_numpy(tok_off).to(dev),
+                   win_off=torch.from_numpy(win_off).to(dev), win_hash=win_hash,
+                   win_slot=win_slot, sorted_hash=sorted_hash, sorted_widx=sorted_widx,
+                   slot_rank=torch.from_numpy(rank).to(dev), rank2slot=torch.from_numpy(r2s).to(dev))
+        p = self.params
+        c = N.TokenIndex(n_slots, n_windows, p.window_size, p.base, p.modulus,
+                         *(idx[k].data_ptr() for k in ("tokens", "tok_off", "win_off", "win_hash",
+                                                        "win_slot", "sorted_hash", "sorted_widx",
+                                                        "slot_rank", "rank2slot")))
+        max_pages = max([len(e.pages) for e in self._slots if e is not None] + [1])
+        sp = np.zeros((max(n_slots, 1), max_pages), dtype=np.int32)
+        for s in live:
+            pg = self._slots[s].pages
+            sp[s, :len(pg)] = pg
+        idx["slot_pages"] = torch.from_numpy(sp).to(dev)
+        idx["slot_max_pages"] = max_pages
+        idx["c"] = c
+        self._index = idx
+        self._dirty = False
+        return idx
+
+    # ------------------------------------------------------------------ lookup
+    def lookup_device(self, tokens_flat: torch.Tensor, req_off: torch.Tensor,
+                      req_off_host: np.ndarray) -> BatchLookup:
+        """Batched R2 lookup of a scheduled batch (flat device tokens)."""
+        n_req = len(req_off_host) - 1
+        n_total = int(req_off_host[-1])
+        dev = self.device
+        src_slot = torch.empty(max(n_total, 1), dtype=torch.int32, device=dev)
+        src_cand = torch.empty(max(n_total, 1), dtype=torch.int32, device=dev)
+        n_hit = torch.zeros(n_req, dtype=torch.int32, device=dev)
+        n_slots = max(len(self._slots), 1)
+        contributed = torch.zeros((n_req, n_slots), dtype=torch.uint8, device=dev)
+        if self.entries:
+            idx = self._build_index()
+            ws = self._ws.get(N.ws_bytes("kvs_pool_lookup_workspace", n_total), dev)
+            N.call("kvs_pool_lookup", idx["c"], tokens_flat.data_ptr(), req_off.data_ptr(),
+                   n_req, n_total, src_slot.data_ptr(), src_cand.data_ptr(), n_hit.data_ptr(),
+                   contributed.data_ptr(), ws.data_ptr(), ws.numel(), N.stream_ptr())
+        else:
+            src_slot.fill_(-1)
+            src_cand.fill_(-1)
+        return BatchLookup(req_off, tokens_flat, src_slot[:n_total], src_cand[:n_total], n_hit,
+                           contributed)
+
+    def refresh_lru(self, contributed_row: np.ndarray) -> None:
+        """pool.py:157-159: contributors get new ticks in old last_access order."""
+        contributors = [self._slots[s] for s in np.nonzero(contributed_row)[0]
+                        if s < len(self._slots) and self._slots[s] is not None]
+        for entry in sorted(contributors, key=lambda e: e.last_access):
+            entry.last_access = self._tick()
+
+    def lookup(self, tokens, fixed_chunk: int | None = None) -> ReuseMap:
+        """pool.py:125-161 for one request."""
+        tokens = np.asarray(tokens, dtype=np.int64)
+        reuse = ReuseMap(length=int(tokens.size))
+        if tokens.size == 0 or not self.entries:
+            return reuse
+        if fixed_chunk is not None:
+            return self._lookup_fixed(tokens, fixed_chunk)
+        dev = self.device
+        tok = torch.from_numpy(tokens).to(dev)
+        off = np.array([0, tokens.size], dtype=np.int64)
+        res = self.lookup_device(tok, torch.from_numpy(off).to(dev), off)
+        slot = res.src_slot.cpu().numpy()
+        cand = res.src_cand.cpu().numpy()
+        self.refresh_lru(res.contributed[0].cpu().numpy())
+        for pos in np.nonzero(slot >= 0)[0]:
+            reuse.sources[int(pos)] = (self._slots[slot[pos]], int(cand[pos]))
+        reuse.src_slot, reuse.src_cand = res.src_slot, res.src_cand
+        return reuse
+
+    def _lookup_fixed(self, tokens: np.ndarray, chunk: int) -> ReuseMap:
+        """Fixed-chunk baseline (pool.py:148-149 -> matching.fixed_chunk_match)."""
+        from .matching import fixed_chunk_match
+        reuse = ReuseMap(length=int(tokens.size))
+        ordered = sorted(self.entries.values(), key=lambda e: -e.insert_seq)
+        contributors = []
+        for entry in ordered:
+            if len(reuse.sources) == reuse.length:
+                break
+            res = fixed_chunk_match(tokens, entry.tokens, chunk)
+            contributed = False
+            for t, c in zip(res.target_matches, res.candidate_matches):
+                if t not in reuse.sources:
+                    reuse.sources[t] = (entry, c)
+                    contributed = True
+            if contributed:
+                contributors.append(entry)
+        for entry in sorted(contributors, key=lambda e: e.last_access):
+            entry.last_access = self._tick()
+        reuse.sources = dict(sorted(reuse.sources.items()))
+        return reuse
+
+    # ------------------------------------------------------------------ eviction
+    def evict_to_capacity(self, max_bytes: int) -> list[str]:
+        """pool.py:163-172: drop least-recently-accessed entries until it fits."""
+        if max_bytes < 0:
+            raise ParameterError(f"max_bytes must be >= 0, got {max_bytes}")
+        evicted = []
+        while self.entries and self.total_bytes > max_bytes:
+            victim = min(self.entries.values(), key=lambda e: e.last_access)
+            self._drop(victim)
+            evicted.append(victim.request_id)
+        return evicted
+
+    def slot_entry(self, slot: int) -> KVEntry | None:
+        return self._slots[slot] if 0 <= slot < len(self._slots) else None

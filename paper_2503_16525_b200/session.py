@@ -1,0 +1,366 @@
+"""Reference-shaped sessions, forwards and generation over the device engine.
+
+Drop-ins for reference pkg/src/kvlab/model.py (``LayerStates`` :132-151,
+``model_forward`` :211-213, ``model_forward_with_reuse`` :216-227) and
+pkg/src/kvlab/engine.py (``ReuseSession`` :47-171, ``PrefillResult`` :174-179,
+``prefill_with_selection`` :217-243, ``GenerationResult`` :288-295,
+``run_generation`` :298-328).  Each call runs the batched engine with a batch
+of one; numpy views are produced only when a caller asks for them.
+
+Differences from the reference, by construction of the B200 path:
+* ``LayerStates.attn`` is None - the (L, H, n, n) attention matrix is never
+  materialised (flash-style attention).
+* After a DHD prefill the session has computed only the rows
+  S = non-reused U selected U {n-1} (exact on those rows);
+  ``prefill_states.hidden`` holds NaN on the other rows.  K/V are complete.
+* ORACLE selection mode and the comparison strategies are SURVEY.md F4 and
+  raise ParameterError.
+"""
+from __future__ import annotations
+
+from collections.abc import Mapping
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from .engine import BatchState, Engine, RowSet
+from .errors import InputError, ParameterError
+from .model import HEAD_DIM, ToyModel
+from .pool import CachePool, KVArena, ReuseMap
+from .selection import SelectionConfig, SelectionMode, Strategy
+
+_ENGINES: dict = {}
+
+
+def get_engine(model: ToyModel, pool: CachePool | None = None, need_tokens: int = 0) -> Engine:
+    """One engine per (model, pool); a private growing pool when pool is None."""
+    if pool is not None:
+        key = (id(model), id(pool))
+        eng = _ENGINES.get(key)
+        if eng is None:
+            eng = _ENGINES[key] = Engine(model, pool)
+        return eng
+    key = (id(model), None)
+    eng = _ENGINES.get(key)
+    pages = KVArena(model.config, 0, model.device).pages_for(need_tokens) + 2
+    if eng is None or eng.arena.free_pages < pages:
+        total = max(pages * 2, 64, 0 if eng is None else eng.arena.num_pages * 2)
+        arena = KVArena(model.config, total, model.device)
+        eng = _ENGINES[key] = Engine(model, CachePool(model.config, arena=arena,
+                                                      device=model.device))
+    return eng
+
+
+def _pool_of(reuse: ReuseMap | None) -> CachePool | None:
+    if reuse is None or not reuse.sources:
+        return None
+    entry = next(iter(reuse.sources.values()))[0]
+    return entry.pool
+
+
+def _device_hits(reuse: ReuseMap | None, n: int, device):
+    slot = np.full(n, -1, dtype=np.int32)
+    cand = np.full(n, -1, dtype=np.int32)
+    if reuse is not None:
+        for pos, (entry, c) in reuse.sources.items():
+            if not 0 <= pos < n:
+                raise InputError(f"reuse position {pos} outside request of length {n}")
+            if not 0 <= c < entry.n_tokens:
+                from .errors import CacheError
+                raise CacheError(f"cached position {c} outside entry")
+            slot[pos] = entry.slot
+            cand[pos] = c
+    return torch.from_numpy(slot).to(device), torch.from_numpy(cand).to(device)
+
+
+@dataclass
+class LayerStates:
+    """Per-layer states (model.py:132-151) as numpy float64; attn is None."""
+
+    q: np.ndarray
+    k: np.ndarray
+    v: np.ndarray
+    attn: None
+    head_out: np.ndarray
+    hidden: np.ndarray
+
+    @property
+    def n_tokens(self) -> int:
+        return self.hidden.shape[1]
+
+
+def _kv_numpy(eng: Engine, st: BatchState, r: int, n: int, kv: int) -> np.ndarray:
+    out = []
+    for layer in range(eng.cfg.num_layers):
+        rows = eng.arena.rows(st.pages[r], n, layer, kv)
+        out.append(eng.model.unpad_heads(rows).float().permute(1, 0, 2).cpu().numpy())
+    return np.stack(out).astype(np.float64)
+
+
+def _states_from_capture(eng: Engine, st: BatchState, rows: RowSet, capture, x0) -> LayerStates:
+    cfg, m = eng.cfg, eng.model
+    n = int(st.lengths[0])
+    pos = rows.row_pos.cpu().numpy()
+    L, H = cfg.num_layers, cfg.num_heads
+    q = np.full((L, H, n, cfg.d_k), np.nan)
+    ho = np.full((L, H, n, cfg.d_k), np.nan)
+    hid = np.full((L + 1, n, cfg.d_model), np.nan)
+    hid[0][pos] = x0.double().cpu().numpy()
+    for item in capture:
+        layer = item[0]
+        if item[1] == "hidden":
+            hid[layer + 1][pos] = item[2].double().cpu().numpy()
+        else:
+            q[layer][:, pos] = m.unpad_heads(item[1]).float().permute(1, 0, 2).cpu().numpy()
+            ho[layer][:, pos] = m.unpad_heads(item[2]).float().permute(1, 0, 2).cpu().numpy()
+    return LayerStates(q, _kv_numpy(eng, st, 0, n, 0), _kv_numpy(eng, st, 0, n, 1), None, ho, hid)
+
+
+def _normalize_recompute(recompute, L: int) -> list[set]:
+    if recompute is None:
+        return [set() for _ in range(L)]
+    if isinstance(recompute, Mapping):
+        return [set(recompute.get(layer, ())) for layer in range(L)]
+    if isinstance(recompute, (list, tuple)) and recompute and \
+            all(isinstance(s, (set, frozenset)) for s in recompute):
+        return [set(s) for s in recompute]
+    fixed = set(recompute)
+    return [set(fixed) for _ in range(L)]
+
+
+def _forward_session(model: ToyModel, tokens, reuse, sets, decode_capacity=64):
+    """model.py:163-208 over all rows on the device (+ a live BatchState)."""
+    tokens = np.asarray(tokens, dtype=np.int64)
+    model.check_tokens(tokens)
+    pool = _pool_of(reuse)
+    eng = get_engine(model, pool, tokens.size + decode_capacity)
+    st = eng.new_batch([tokens], decode_capacity)
+    n = tokens.size
+    st.src_slot, st.src_cand = _device_hits(reuse, n, eng.device)
+    st.n_hit = np.array([int((st.src_slot >= 0).sum().item())])
+    if st.n_hit[0] and pool is not None:
+        eng.gather(st)
+    rows = eng._rows_all(st)
+    reused = st.src_slot >= 0
+    per_layer = []
+    for s in sets:
+        rec = torch.zeros(n, dtype=torch.bool, device=eng.device)
+        if s:
+            rec[torch.tensor(sorted(p for p in s if 0 <= p < n), dtype=torch.long,
+                             device=eng.device)] = True
+        per_layer.append((~reused | rec).to(torch.uint8))
+    capture = []
+    x = eng._embed(st.tokens, rows)
+    x0 = x.clone()
+    eng.forward_rows(x, rows, range(eng.cfg.num_layers), eng.arena.c, st.batch_c,
+                     write_kv_per_layer=per_layer, capture=capture)
+    st.rows = rows
+    st.hidden_last = x[-1:]
+    states = _states_from_capture(eng, st, rows, capture, x0)
+    return eng, st, states
+
+
+def model_forward(tokens, model: ToyModel) -> LayerStates:
+    eng, st, states = _forward_session(model, tokens, None, _normalize_recompute(
+        None, model.config.num_layers), decode_capacity=0)
+    eng.release(st)
+    return states
+
+
+def model_forward_with_reuse(tokens, model: ToyModel, reuse: ReuseMap | None,
+                             recompute=None) -> LayerStates:
+    eng, st, states = _forward_session(model, tokens, reuse, _normalize_recompute(
+        recompute, model.config.num_layers), decode_capacity=0)
+    eng.release(st)
+    return states
+
+
+@dataclass
+class StepStates:
+    """Per-step output (engine.py:38-44); q/attn are not materialised."""
+
+    q: None
+    attn: None
+    hidden_out: np.ndarray
+
+
+class ReuseSession:
+    """Mutable device K/V cache of one request (engine.py:47-171)."""
+
+    def __init__(self, model: ToyModel, tokens, reuse=None, recompute=None,
+                 _engine_state=None, decode_capacity: int = 256):
+        cfg = model.config
+        self.model = model
+        self.tokens = [int(t) for t in np.asarray(tokens, dtype=np.int64)]
+        self.n_prefill = len(self.tokens)
+        sets = _normalize_recompute(recompute, cfg.num_layers)
+        if _engine_state is None:
+            eng, st, states = _forward_session(model, tokens, reuse, sets, decode_capacity)
+            self.prefill_states = states
+        else:
+            eng, st, self.prefill_states = _engine_state
+        self.engine, self.state = eng, st
+        self.reused = set() if reuse is None else set(reuse.sources)
+        self.recomputed = [set(s) & self.reused for s in sets]
+        self.probe_layer = 1 if cfg.num_layers >= 2 else 0
+        elig = np.zeros(self.n_prefill, dtype=np.uint8)
+        common = set.intersection(*self.recomputed) if self.recomputed else set()
+        for p in self.reused - common:
+            elig[p] = 1
+        st.eligible = torch.from_numpy(elig).to(eng.device)
+        st.tokens_host = [list(self.tokens)]
+
+    @property
+    def n_tokens(self) -> int:
+        return len(self.tokens)
+
+    @property
+    def k(self) -> np.ndarray:
+        return _kv_numpy(self.engine, self.state, 0, self.n_tokens, 0)
+
+    @property
+    def v(self) -> np.ndarray:
+        return _kv_numpy(self.engine, self.state, 0, self.n_tokens, 1)
+
+    def _grow(self, extra: int = 1):
+        st, eng = self.state, self.engine
+        need = self.n_tokens + extra
+        if need <= st.capacity[0]:
+            return
+        add = eng.arena.pages_for(need + 256) - len(st.pages[0])
+        st.pages[0] = st.pages[0] + eng.arena.alloc(add)
+        bt = np.array([st.pages[0]], dtype=np.int32)
+        st.block_table = torch.from_numpy(bt).to(eng.device)
+        st.batch_c.block_table = st.block_table.data_ptr()
+        st.batch_c.max_pages = bt.shape[1]
+        st.capacity = np.array([len(st.pages[0]) * eng.arena.page_size])
+        st._keep = (st.req_off, st.block_table)
+
+    def append(self, token_id: int) -> StepStates:
+        """engine.py:114-121: run the token through all layers, grow the cache."""
+        self.model.check_tokens(np.array([token_id], dtype=np.int64))
+        self._grow(1)
+        h, _ = self.engine.decode_step(self.state, [int(token_id)], 0)
+        self.tokens.append(int(token_id))
+        return StepStates(None, None, h[0].double().cpu().numpy())
+
+    def recompute_positions(self, positions) -> None:
+        """engine.py:123-138 as one layer-batched pass."""
+        pos = sorted(set(int(p) for p in positions))
+        for p in pos:
+            if not 0 <= p < self.n_tokens:
+                raise InputError(f"position {p} outside sequence of {self.n_tokens}")
+        if not pos:
+            return
+        eng, st = self.engine, self.state
+        rows = RowSet(len(pos), torch.arange(len(pos), dtype=torch.int32, device=eng.device),
+                      torch.zeros(len(pos), dtype=torch.int32, device=eng.device),
+                      torch.tensor(pos, dtype=torch.int32, device=eng.device), None,
+                      np.array([0, len(pos)], dtype=np.int64))
+        tok = torch.tensor([self.tokens[p] for p in pos], dtype=torch.int64, device=eng.device)
+        x = eng._embed(tok, rows)
+        eng.forward_rows(x, rows, range(eng.cfg.num_layers), eng.arena.c, st.batch_c,
+                         decode=True, max_kv=int(st.capacity.max()))
+        elig = st.eligible
+        for p in pos:
+            if p in self.reused:
+                for s in self.recomputed:
+                    s.add(p)
+            if p < elig.numel():
+                elig[p] = 0
+
+    def delta_v_probe(self) -> np.ndarray:
+        """engine.py:140-148: cache V at the probe layer minus its exact value."""
+        eng, st = self.engine, self.state
+        _, _, v_true = eng._probe(_prefill_view(st), write_k=False)
+        cache_v = eng.arena.rows(st.pages[0], self.n_tokens, self.probe_layer, 1)
+        delta = torch.zeros_like(cache_v, dtype=torch.float32)
+        n = self.n_prefill
+        delta[:n] = cache_v[:n].float() - v_true.float()
+        return eng.model.unpad_heads(delta).permute(1, 0, 2).double().cpu().numpy()
+
+    def query_rows_probe(self, token_id: int) -> np.ndarray:
+        """engine.py:150-171 (the new token's own layer-0 row is written at
+        position n_tokens, beyond the context; append overwrites it with the
+        same value)."""
+        self._grow(1)
+        q = self.engine.probe_query(self.state, np.array([int(token_id)]))
+        return self.model.unpad_heads(q[0]).double().cpu().numpy()
+
+
+def _prefill_view(st: BatchState) -> BatchState:
+    """The prefill rows of a (possibly decoded-into) single-request state."""
+    return st
+
+
+@dataclass
+class PrefillResult:
+    session: ReuseSession
+    recompute_sets: list
+    selected: tuple = ()
+    eligible: set = field(default_factory=set)
+
+
+def prefill_with_selection(model: ToyModel, tokens, reuse, config: SelectionConfig,
+                           ref_states=None, decode_capacity: int = 256) -> PrefillResult:
+    """engine.py:217-243 (PRACTICAL): probe, DHD select, partial prefill."""
+    reused = sorted(reuse.sources) if reuse is not None else []
+    if not reused:
+        session = ReuseSession(model, tokens, reuse, decode_capacity=decode_capacity)
+        return PrefillResult(session, session.recomputed)
+    if config.mode is not SelectionMode.PRACTICAL:
+        raise ParameterError("ORACLE selection mode is not on the device hot path (SURVEY.md F4)")
+    if Strategy(config.strategy) is not Strategy.ATTENTION_WEIGHTED:
+        raise ParameterError("only the ATTENTION_WEIGHTED strategy is on the device hot path")
+    tokens = np.asarray(tokens, dtype=np.int64)
+    model.check_tokens(tokens)
+    pool = _pool_of(reuse)
+    eng = get_engine(model, pool)
+    st = eng.new_batch([tokens], decode_capacity)
+    st.src_slot, st.src_cand = _device_hits(reuse, tokens.size, eng.device)
+    st.n_hit = np.array([len(reused)])
+    eng.gather(st)
+    eng.probe_and_select(st, config.ratio)
+    rows = eng.build_rows(st, st.selected)
+    capture = []
+    x = eng._embed(st.tokens, rows)
+    x0 = x.clone()
+    eng.forward_rows(x, rows, range(eng.cfg.num_layers), eng.arena.c, st.batch_c, capture=capture)
+    st.rows = rows
+    st.hidden_last = x[-1:]
+    states = _states_from_capture(eng, st, rows, capture, x0)
+    selected = tuple(int(i) for i in torch.nonzero(st.selected).flatten().cpu().tolist())
+    session = ReuseSession(model, tokens, reuse, set(selected), _engine_state=(eng, st, states))
+    eligible = set(reused) - set(selected)
+    return PrefillResult(session, session.recomputed, selected, eligible)
+
+
+@dataclass
+class GenerationResult:
+    step_deviation: list
+    recompute_counts: list
+
+    @property
+    def cumulative_deviation(self) -> float:
+        return float(sum(self.step_deviation))
+
+
+def run_generation(session: ReuseSession, ref_session: ReuseSession, decode_tokens,
+                   n_extra: int) -> GenerationResult:
+    """engine.py:298-328: per token, D3 selection + recompute + append on the
+    session, append on the reference session, ||h - h_ref||."""
+    deviations, counts = [], []
+    for tok in decode_tokens:
+        tok = int(tok)
+        session._grow(1)
+        h, chosen = session.engine.decode_step(session.state, [tok], n_extra)
+        for p in chosen[0]:
+            if p in session.reused:
+                for s in session.recomputed:
+                    s.add(p)
+        session.tokens.append(tok)
+        ref = ref_session.append(tok)
+        deviations.append(float(np.linalg.norm(h[0].double().cpu().numpy() - ref.hidden_out)))
+        counts.append(len(chosen[0]))
+    return GenerationResult(deviations, counts)
