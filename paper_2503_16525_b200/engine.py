@@ -125,7 +125,7 @@ class Engine:
         self.arena: KVArena = pool.arena
         self.scale = 1.0 / math.sqrt(self.cfg.d_k)
         self._ws = {k: N.Workspace() for k in ("alpha", "select", "decode", "dsel")}
-        self._probe = _ProbeArena()
+        self._probe_arena = _ProbeArena()
         self.rope_c = None
         if model.rope is not None:
             self.rope_c = N.Rope(model.rope[0].data_ptr(), model.rope[1].data_ptr(),
@@ -262,7 +262,7 @@ class Engine:
         p = self.probe_layer
         if p == 1:
             npages = int(sum((l + PAGE_SIZE - 1) // PAGE_SIZE for l in st.lengths))
-            parena = self._probe.get(cfg, npages, dev)
+            parena = self._probe_arena.get(cfg, npages, dev)
             bt = np.zeros((len(st.lengths), st.block_table.shape[1]), dtype=np.int32)
             base = 0
             for r, l in enumerate(st.lengths):
