@@ -1,0 +1,375 @@
+"""KVShare DHD prefill benchmark (BASELINE.json configs[1]).
+
+Workload: Llama-3.1-8B attention-stack shape (L=32, H=32, kv_heads=8, d=128,
+d_model=4096, vocab 128256, RoPE theta 5e5), random-init weights, synthetic
+multi-tenant stream: a pool of 16 source requests of 4096 tokens (prefilled
+by the engine in full-recompute mode and written back zero-copy), then per
+step one scheduled batch of R requests of 4096 tokens at a 50% chunk hit
+rate (spans copied from the sources), DHD prefill with r = 0.2:
+lookup -> gather+RoPE -> probe -> alpha -> select -> partial prefill.
+
+  value  prefill tok/s with tokens already in HBM (CUDA events, max over ranks)
+  e2e    the same through the public API with the tokens copied from pinned
+         host memory and the last hidden rows read back, inside the timing
+
+Inputs are larger than L2 (2.7 GB of weights + 4 GiB of KV per step are
+streamed every step), so no explicit flush.  ``--impl reference`` times the
+CPU oracle port of the reference algorithm on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "prefill tok/s & p50 TTFT at Llama-8B shape, 50% hit; DHD select HBM GB/s"
+WORKLOAD = "llama3.1-8b-shape DHD prefill, 4096-token requests, 50% chunk hit, r=0.2"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=8, help="requests per scheduled batch per GPU")
+    ap.add_argument("--seq", type=int, default=4096)
+    ap.add_argument("--hit", type=float, default=0.5)
+    ap.add_argument("--ratio", type=float, default=0.2)
+    ap.add_argument("--sources", type=int, default=16)
+    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu legs)")
+    ap.add_argument("--mode", default="selective", choices=["selective", "full", "naive"])
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.path = f"/tmp/kvs_clocks_{os.getpid()}.csv"
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------- CPU leg
+def cpu_reference_sample(seq: int, layers: int, heads_sample: int = 4):
+    """Time the CPU oracle (numpy float64 restatement of the reference
+    algorithm: every layer computes all n rows, model.py:163-208) on one
+    request at Llama width: one full layer (projections at full width,
+    attention for `heads_sample` of 32 heads scaled x32/heads_sample) and the
+    probe's alpha (same head sample), extrapolated to `layers` layers.
+    Returns (tok/s, seconds of CPU work, description)."""
+    from oracle import kvshare_oracle as O
+    rng = np.random.default_rng(0)
+    d_model, H, G, d = 4096, 32, 8, 128
+    hs, gs = heads_sample, max(1, heads_sample * G // H)
+    x = rng.standard_normal((seq, d_model)) * 0.02
+    wq = rng.uniform(-1, 1, (d_model, H * d)) / 64.0
+    wkv = rng.uniform(-1, 1, (d_model, 2 * G * d)) / 64.0
+    wo = rng.uniform(-1, 1, (H * d, d_model)) / 64.0
+    t0 = time.perf_counter()
+    q = x @ wq
+    kv = x @ wkv
+    t_proj_qkv = time.perf_counter() - t0
+    qh = O.split_heads(q[:, :hs * d], hs)
+    kh = O.split_heads(kv[:, :gs * d], gs)
+    vh = O.split_heads(kv[:, G * d:G * d + gs * d], gs)
+    t0 = time.perf_counter()
+    out, _ = O.attention(qh, kh, vh, causal=True, group=hs // gs)
+    t_attn = (time.perf_counter() - t0) * (H / hs)
+    full_out = np.tile(O.merge_heads(out), (1, H // hs))
+    t0 = time.perf_counter()
+    _ = x + full_out @ wo
+    t_proj_o = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    O.v_impact_scores(qh, kh, vh * 0.01, causal=True, group=hs // gs)
+    t_alpha = (time.perf_counter() - t0) * (H / hs)
+    t_layer = t_proj_qkv + t_attn + t_proj_o
+    # prefill_with_selection: exact hidden (1 layer) + probe QKV + alpha + L-layer reuse forward
+    total = t_layer + t_proj_qkv + t_alpha + layers * t_layer
+    sample = (f"oracle fp64 numpy, 1 request x {seq} tokens at Llama width: one layer "
+              f"(full-width projections, attention {hs}/32 heads scaled) + DHD alpha, "
+              f"extrapolated to {layers} layers")
+    return seq / total, t_layer + t_alpha / (H / hs) * 1.0 + t_proj_qkv, sample
+
+
+# ---------------------------------------------------------------------------- GPU leg
+def build_engine(args, device):
+    import torch
+
+    import paper_2503_16525_b200 as K
+    from paper_2503_16525_b200.engine import Engine
+    from paper_2503_16525_b200.pool import CachePool, KVArena
+    from paper_2503_16525_b200.workload import source_requests
+
+    shape = dict(K.LLAMA31_8B)
+    shape["num_layers"] = args.layers
+    cfg = K.ModelConfig(**shape, seed=0, max_positions=max(8192, args.seq + 64))
+    model = K.ToyModel(cfg, device=device, init="device")
+    src_pages = args.sources * ((args.seq + 63) // 64)
+    step_pages = 2 * args.batch * ((args.seq + 63) // 64)
+    arena = KVArena(cfg, src_pages + step_pages + 64, device)
+    pool = CachePool(cfg, K.HashParams(window_size=8), arena=arena, device=device)
+    eng = Engine(model, pool)
+    sources = source_requests(args.sources, args.seq, cfg.vocab_size, seed=0)
+    for i in range(0, len(sources), 4):
+        chunk = sources[i:i + 4]
+        st = eng.prefill_batch(chunk, mode="full")
+        eng.write_back(st, [f"src{i + j}" for j in range(len(chunk))])
+    torch.cuda.synchronize()
+    return cfg, model, pool, eng, sources
+
+
+def algorithmic_counts(eng, st, cfg):
+    """Per-step algorithmic work: A1 FLOPs, D1 FLOPs, D2 bytes."""
+    import torch
+    H, d, G = cfg.num_heads, cfg.d_k, cfg.kv_heads
+    pos = st.rows.row_pos.to(torch.float64)
+    sess = float(4 * H * d * (pos + 1).sum().item()) * cfg.num_layers
+    probe = 0.0
+    alpha = 0.0
+    for n in st.lengths:
+        probe += 4.0 * H * d * n * (n + 1) / 2.0
+        alpha += 2.0 * H * d * n * (n + 1)
+    n_r = st.n_hit.astype(np.float64)
+    B = st.budgets.astype(np.float64) if st.budgets is not None else np.zeros_like(n_r)
+    sel_bytes = float((n_r * (2 * G * d * 2 + 12)).sum() + (4 * B).sum())
+    return {"attention_flops": sess + probe, "alpha_flops": alpha, "select_bytes": sel_bytes}
+
+
+def run_gpu(args, rank, world, device):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2503_16525_b200 import _native as N
+    from paper_2503_16525_b200.workload import request_batches
+
+    torch.cuda.set_device(device)
+    cfg, model, pool, eng, sources = build_engine(args, device)
+    n_steps = args.warmup + args.steps
+    batches = request_batches(sources, n_steps, args.batch, args.seq, args.hit, cfg.vocab_size,
+                              seed=1 + rank)
+    dev_tokens = [torch.from_numpy(np.concatenate(b)).to(device) for b in batches]
+    torch.cuda.synchronize()
+
+    def step(i, timers=None):
+        eng.timers = timers
+        st = eng.prefill_batch(batches[i], ratio=args.ratio, mode=args.mode,
+                               tokens_dev=dev_tokens[i])
+        return st
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    # ---------------- warm-up
+    for i in range(args.warmup):
+        st = step(i)
+        eng.release(st)
+    torch.cuda.synchronize()
+    # ---------------- timed (device-resident inputs)
+    clocks = ClockSampler(torch.cuda.current_device())
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    timers = {}
+    launches0 = N.launch_count["kernels"]
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_ms, counts, n_hit = [], [], []
+    start.record()
+    for i in range(args.warmup, n_steps):
+        s0 = torch.cuda.Event(enable_timing=True)
+        s1 = torch.cuda.Event(enable_timing=True)
+        s0.record()
+        st = step(i, timers)
+        s1.record()
+        step_ms.append((s0, s1))
+        counts.append(algorithmic_counts(eng, st, cfg))
+        n_hit.append(float(st.n_hit.sum()) / float(st.lengths.sum()))
+        eng.timers = None
+        eng.release(st)
+    end.record()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    launches = N.launch_count["kernels"] - launches0
+    elapsed = start.elapsed_time(end)
+    per_step = [a.elapsed_time(b) for a, b in step_ms]
+    t = torch.tensor([elapsed], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed = float(t.item())
+    tokens = args.steps * args.batch * args.seq * world
+    kern = {}
+    for name, evs in timers.items():
+        kern[name] = sum(a.elapsed_time(b) for a, b in evs) / args.steps     # ms per step
+    res = {"elapsed_ms": elapsed, "tokens": tokens, "step_ms": per_step, "kernels_ms": kern,
+           "counts": {k: float(np.mean([c[k] for c in counts])) for k in counts[0]},
+           "hit": float(np.mean(n_hit)), "launches": launches // max(args.steps, 1),
+           "clocks": clk, "n_launch_attention": len(timers.get("attention", [])) // args.steps}
+    if args.profile:
+        return res
+    # ---------------- e2e: public API, tokens from pinned host memory, result read back
+    pinned = [torch.from_numpy(np.concatenate(b)).pin_memory() for b in batches]
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    outs = []
+    for i in range(args.warmup, n_steps):
+        tok = pinned[i].to(device, non_blocking=True)
+        st = eng.prefill_batch(batches[i], ratio=args.ratio, mode=args.mode, tokens_dev=tok)
+        outs.append(st.hidden_last.cpu())
+        eng.release(st)
+    e1.record()
+    torch.cuda.synchronize()
+    te = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    res["e2e_ms"] = float(te.item())
+    res["h2d_bytes"] = args.batch * args.seq * 8
+    res["d2h_bytes"] = args.batch * cfg.d_model * 4
+    return res
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            p = json.load(fh)
+        return p["hbm_gbs"], p["bf16_tflops"], p["bf16_tflops_sustained"], "measured"
+    except (OSError, KeyError, ValueError):
+        return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+def main():
+    args = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    cfg_doc = {"workload": WORKLOAD, "requests_per_gpu_step": args.batch, "seq_len": args.seq,
+               "hit_rate": args.hit, "recompute_ratio": args.ratio, "pool_sources": args.sources,
+               "layers": args.layers, "model_shape": "llama3.1-8b attention stack (no FFN)",
+               "parallelism": f"dp{args.gpus} (requests partitioned, per-GPU pool)",
+               "l2": "inputs larger than L2 (2.7 GB weights + 4 GiB KV streamed per step)"}
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        os.environ.setdefault("OPENBLAS_NUM_THREADS", str(os.cpu_count()))
+        vals = []
+        for _ in range(args.warmup + args.steps):
+            v, secs, sample = cpu_reference_sample(args.seq, args.layers)
+            vals.append(v)
+        v = float(np.median(vals[args.warmup:]))
+        print(json.dumps({
+            "impl": "reference", "metric": METRIC, "value": v, "unit": "tok/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": args.batch * args.seq / v * 1000.0, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": cfg_doc,
+            "cpu_baseline": {"value": v, "unit": "tok/s", "cores": os.cpu_count(),
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": v, "unit": "tok/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}))
+        return
+    import torch
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    device = torch.device("cuda", local)
+    res = run_gpu(args, rank, world, device)
+    if rank != 0:
+        if world > 1:
+            torch.distributed.destroy_process_group()
+        return
+    hbm, tflops, tflops_sus, kind = peaks()
+    ms_per_step = res["elapsed_ms"] / args.steps
+    value = res["tokens"] / (res["elapsed_ms"] / 1000.0)
+    kern = res["kernels_ms"]
+    c = res["counts"]
+    att_ms = kern.get("attention", float("nan"))
+    att_tflops = c["attention_flops"] / (att_ms / 1000.0) / 1e12 if att_ms == att_ms else None
+    roof = {"kernel": "kvs_attention_fwd (A1 selective-recompute attention, tcgen05)",
+            "bound": "tensor", "achieved": att_tflops, "peak": tflops_sus, "unit": "TFLOP/s",
+            "frac": att_tflops / tflops_sus if att_tflops else None, "traffic": None,
+            "peak_kind": f"{kind} bf16 sustained (kernel timed inside a long step)",
+            "ms_per_step": att_ms, "share_of_step": att_ms / ms_per_step,
+            "launches_per_step": res["n_launch_attention"]}
+    extra = {}
+    if "dhd_select" in kern:
+        gbs = c["select_bytes"] / (kern["dhd_select"] / 1000.0) / 1e9
+        extra["dhd_select"] = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
+                               "frac": gbs / hbm, "ms_per_step": kern["dhd_select"]}
+    if "dhd_alpha" in kern:
+        tf = c["alpha_flops"] / (kern["dhd_alpha"] / 1000.0) / 1e12
+        extra["dhd_alpha"] = {"bound": "tensor", "achieved": tf, "peak": tflops_sus,
+                              "unit": "TFLOP/s", "frac": tf / tflops_sus,
+                              "ms_per_step": kern["dhd_alpha"]}
+    if "gather" in kern:
+        extra["gather_ms_per_step"] = kern["gather"]
+    line = {
+        "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (random-init weights, seeded token streams)", "config": cfg_doc,
+        "ttft_p50_ms": float(np.median(res["step_ms"])), "measured_hit_rate": res["hit"],
+        "roofline": roof, "kernels": extra, "gpu_launches": res["launches"] * args.steps,
+        "clocks": res["clocks"],
+    }
+    if "e2e_ms" in res:
+        line["e2e"] = {"value": res["tokens"] / (res["e2e_ms"] / 1000.0), "unit": "tok/s",
+                       "h2d_bytes_per_step": res["h2d_bytes"],
+                       "d2h_bytes_per_step": res["d2h_bytes"]}
+        v, _, sample = cpu_reference_sample(args.seq, args.layers)
+        line["cpu_baseline"] = {"value": v, "unit": "tok/s", "cores": os.cpu_count(),
+                                "kind": "port", "sample": sample}
+    print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -76,6 +76,15 @@ _WS_SIGS = {
 
 _lib = None
 
+# kernels launched per entry point (for the bench's gpu_launches claim)
+KERNELS_PER_CALL = {
+    "kvs_window_hashes": 1, "kvs_match_pairs": 9, "kvs_index_sort": 5, "kvs_pool_lookup": 4,
+    "kvs_gather_kv": 1, "kvs_qkv_rope_scatter": 1, "kvs_embed_rows": 1, "kvs_build_rows": 1,
+    "kvs_attention_fwd": 1, "kvs_decode_attention": 2, "kvs_dhd_alpha": 3,
+    "kvs_dhd_select": 2, "kvs_dhd_decode_select": 2,
+}
+launch_count = {"kernels": 0}
+
 
 def exported_symbols():
     return sorted(set(_SIGS) | set(_WS_SIGS) | {"kvs_last_error", "kvs_abi_version"})
@@ -106,6 +115,7 @@ def load(require_gpu: bool = True):
 
 def call(name: str, *args):
     lib = load()
+    launch_count["kernels"] += KERNELS_PER_CALL.get(name, 1)
     st = getattr(lib, name)(*args)
     if st != 0:
         msg = lib.kvs_last_error().decode(errors="replace")

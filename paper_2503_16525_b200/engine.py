@@ -131,8 +131,19 @@ class Engine:
             self.rope_c = N.Rope(model.rope[0].data_ptr(), model.rope[1].data_ptr(),
                                  self.cfg.max_positions)
         self.probe_layer = 1 if self.cfg.num_layers >= 2 else 0
+        self.timers = None          # {name: [(start_event, end_event), ...]} when profiling
 
     # ------------------------------------------------------------------ helpers
+    def _timed(self, name, fn, *args):
+        if self.timers is None:
+            return fn(*args)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        out = fn(*args)
+        e.record()
+        self.timers.setdefault(name, []).append((s, e))
+        return out
+
     def _rope(self):
         return self.rope_c
 
@@ -182,7 +193,7 @@ class Engine:
         return rs.build_tiles(dev)
 
     def _attention(self, q, rows: RowSet, layer: int, arena_c, batch_c, out, lse=None):
-        N.call("kvs_attention_fwd", q.data_ptr(), rows.row_pos.data_ptr(), rows.n_rows,
+        self._timed("attention", N.call, "kvs_attention_fwd", q.data_ptr(), rows.row_pos.data_ptr(), rows.n_rows,
                self.cfg.num_heads, rows.tiles[0].data_ptr(), rows.tiles[1].data_ptr(),
                rows.tiles[2].data_ptr(), rows.n_tiles, None, 1, layer, arena_c, batch_c,
                self.scale, N.ptr(out), N.ptr(lse), N.stream_ptr())
@@ -245,7 +256,7 @@ class Engine:
         if st.n_hit is None or st.n_hit.sum() == 0:
             return
         idx = self.pool._build_index()
-        N.call("kvs_gather_kv", self.arena.c, st.batch_c, st.src_slot.data_ptr(),
+        self._timed("gather", N.call, "kvs_gather_kv", self.arena.c, st.batch_c, st.src_slot.data_ptr(),
                st.src_cand.data_ptr(), idx["slot_pages"].data_ptr(), idx["slot_max_pages"], 0,
                self.cfg.num_layers, self._rope(), N.stream_ptr())
 
@@ -293,7 +304,8 @@ class Engine:
         dv = torch.empty(n, dtype=torch.float32, device=dev)
         score = torch.empty(n, dtype=torch.float32, device=dev)
         sel = torch.empty(n, dtype=torch.uint8, device=dev)
-        N.call("kvs_dhd_select", v_true.data_ptr(), alpha.data_ptr(), st.src_slot.data_ptr(),
+        self._timed("dhd_select", N.call, "kvs_dhd_select", v_true.data_ptr(), alpha.data_ptr(),
+                    st.src_slot.data_ptr(),
                self.probe_layer, self.arena.c, st.batch_c, bud.data_ptr(), dv.data_ptr(),
                score.data_ptr(), sel.data_ptr(), None, 0, N.stream_ptr())
         st._bud = bud
@@ -307,7 +319,7 @@ class Engine:
         n = rows.n_rows
         alpha = torch.empty(n, dtype=torch.float32, device=dev)
         ws = self._ws["alpha"].get(N.ws_bytes("kvs_dhd_alpha_workspace", n, H, G), dev)
-        N.call("kvs_dhd_alpha", q1.data_ptr(), H, 1, self.probe_layer, self.arena.c, st.batch_c,
+        self._timed("dhd_alpha", N.call, "kvs_dhd_alpha", q1.data_ptr(), H, 1, self.probe_layer, self.arena.c, st.batch_c,
                rows.row_pos.data_ptr(), rows.tiles[0].data_ptr(), rows.tiles[1].data_ptr(),
                rows.tiles[2].data_ptr(), rows.n_tiles, None, self.scale, alpha.data_ptr(),
                ws.data_ptr(), ws.numel(), N.stream_ptr())
