@@ -151,7 +151,7 @@ def build_engine(args, device):
     cfg = K.ModelConfig(**shape, seed=0, max_positions=max(8192, args.seq + 64))
     model = K.ToyModel(cfg, device=device, init="device")
     src_pages = args.sources * ((args.seq + 63) // 64)
-    step_pages = 2 * args.batch * ((args.seq + 63) // 64)
+    step_pages = (args.steps + 1) * args.batch * ((args.seq + 63) // 64)
     arena = KVArena(cfg, src_pages + step_pages + 64, device)
     pool = CachePool(cfg, K.HashParams(window_size=8), arena=arena, device=device)
     eng = Engine(model, pool)
@@ -219,7 +219,9 @@ def run_gpu(args, rank, world, device):
     timers = {}
     launches0 = N.launch_count["kernels"]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    step_ms, counts, n_hit = [], [], []
+    step_ms, states = [], []
+    if args.profile:
+        torch.cuda.cudart().cudaProfilerStart()
     start.record()
     for i in range(args.warmup, n_steps):
         s0 = torch.cuda.Event(enable_timing=True)
@@ -228,12 +230,16 @@ def run_gpu(args, rank, world, device):
         st = step(i, timers)
         s1.record()
         step_ms.append((s0, s1))
-        counts.append(algorithmic_counts(eng, st, cfg))
-        n_hit.append(float(st.n_hit.sum()) / float(st.lengths.sum()))
+        states.append(st)
         eng.timers = None
-        eng.release(st)
     end.record()
     torch.cuda.synchronize()
+    if args.profile:
+        torch.cuda.cudart().cudaProfilerStop()
+    counts = [algorithmic_counts(eng, st, cfg) for st in states]
+    n_hit = [float(st.n_hit.sum()) / float(st.lengths.sum()) for st in states]
+    for st in states:
+        eng.release(st)
     barrier()
     clk = clocks.stop()
     launches = N.launch_count["kernels"] - launches0
