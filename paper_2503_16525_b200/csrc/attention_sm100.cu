@@ -194,13 +194,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_before();
             mbar_arrive(&sh.s_empty[b]);
             const int kbase = kb * BN;
-            float mloc = -INFINITY;
+            // row max of the raw scores (scale > 0 commutes with max); the
+            // position mask is only evaluated on blocks that cross this row's end
+            float mx[8];
 #pragma unroll
-            for (int c = 0; c < BN; ++c) {
-                const float x = (kbase + c < kend) ? s[c] * p.scale_log2 : -INFINITY;
-                s[c] = x;
-                mloc = fmaxf(mloc, x);
+            for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
+            if (kbase + BN <= kend) {
+#pragma unroll
+                for (int c = 0; c < BN; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < BN; ++c) {
+                    s[c] = (kbase + c < kend) ? s[c] : -INFINITY;
+                    mx[c & 7] = fmaxf(mx[c & 7], s[c]);
+                }
             }
+            const float mloc = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                     fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) *
+                               p.scale_log2;
             if (mloc > m + kRescaleThreshold || (m == -INFINITY && mloc > -INFINITY)) {
                 const float factor = (m == -INFINITY) ? 0.f : fast_exp2(m - mloc);
                 if (kPV && kb >= 1 && m != -INFINITY) {
@@ -223,14 +234,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 m = mloc;
             }
             const float mu = (m == -INFINITY) ? 0.f : m;
-            float lsum = 0.f;
+            float ls[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) ls[j] = 0.f;
 #pragma unroll
             for (int c = 0; c < BN; ++c) {
-                const float e = fast_exp2(s[c] - mu);
+                const float e = fast_exp2(fmaf(s[c], p.scale_log2, -mu));
                 s[c] = e;
-                lsum += e;
+                ls[c & 7] += e;
             }
-            l += lsum;
+            l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
             if (kPV) {
                 if (kb >= 2) mbar_wait(&sh.pv_done[b], (uint32_t)((kb - 2) >> 1) & 1u);
                 uint8_t *prow = pP + b * TILE_BYTES + i * 128;
@@ -414,13 +427,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             tc_fence_before();
             mbar_arrive(&sh.s_empty[b]);
             const int qbase = qt * BM;
-            float part = 0.f;
+            float ps[8];
 #pragma unroll
-            for (int c = 0; c < BN; ++c) {
-                const bool ok = (!p.causal || qbase + c >= kpos);
-                const float e = fast_exp2(s[c] * p.scale_log2 - s_lse[b][c]);
-                part += ok ? e : 0.f;
+            for (int j = 0; j < 8; ++j) ps[j] = 0.f;
+            if (!p.causal || qbase >= k0 + BM - 1) {
+                // every query of this tile sees every key of the key tile
+#pragma unroll
+                for (int c = 0; c < BN; ++c)
+                    ps[c & 7] += fast_exp2(fmaf(s[c], p.scale_log2, -s_lse[b][c]));
+            } else {
+#pragma unroll
+                for (int c = 0; c < BN; ++c) {
+                    const float e = fast_exp2(fmaf(s[c], p.scale_log2, -s_lse[b][c]));
+                    ps[c & 7] += (qbase + c >= kpos) ? e : 0.f;
+                }
             }
+            const float part = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
             acc += part;
         }
         if (kvalid) p.alpha_part[(s0 + kpos) * p.kv_heads + g] = acc;

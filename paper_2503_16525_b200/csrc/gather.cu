@@ -95,6 +95,25 @@ __global__ void __launch_bounds__(128) gather_kv_kernel(
     }
 }
 
+// Rotate-half with the row's coefficients already in shared memory.
+__device__ __forceinline__ void rope8_smem(const uint4 &lo_in, const uint4 &hi_in, uint4 &lo_out,
+                                           uint4 &hi_out, const float *cs, const float *sn,
+                                           int c) {
+    const __nv_bfloat16 *x1 = reinterpret_cast<const __nv_bfloat16 *>(&lo_in);
+    const __nv_bfloat16 *x2 = reinterpret_cast<const __nv_bfloat16 *>(&hi_in);
+    uint32_t *o1 = reinterpret_cast<uint32_t *>(&lo_out);
+    uint32_t *o2 = reinterpret_cast<uint32_t *>(&hi_out);
+#pragma unroll
+    for (int k = 0; k < 8; k += 2) {
+        const float c0 = cs[8 * c + k], c1 = cs[8 * c + k + 1];
+        const float s0 = sn[8 * c + k], s1 = sn[8 * c + k + 1];
+        const float a0 = bf2f(x1[k]), a1 = bf2f(x1[k + 1]);
+        const float b0 = bf2f(x2[k]), b1 = bf2f(x2[k + 1]);
+        o1[k / 2] = pack_bf16x2(a0 * c0 - b0 * s0, a1 * c1 - b1 * s1);
+        o2[k / 2] = pack_bf16x2(b0 * c0 + a0 * s0, b1 * c1 + a1 * s1);
+    }
+}
+
 // One CTA per query row.  qkv row = [q (H*D) | k (G*D) | v (G*D)].
 __global__ void __launch_bounds__(256) qkv_rope_scatter_kernel(
     const __nv_bfloat16 *__restrict__ qkv, int32_t H, Arena A, const int32_t *__restrict__ row_req,
@@ -116,6 +135,13 @@ __global__ void __launch_bounds__(256) qkv_rope_scatter_kernel(
         dk = reinterpret_cast<uint4 *>(A.row(page, layer, 0, pos % A.P));
         dv = reinterpret_cast<uint4 *>(A.row(page, layer, 1, pos % A.P));
     }
+    __shared__ float s_cos[128], s_sin[128];
+    if (rope)
+        for (int i = threadIdx.x; i < half; i += blockDim.x) {
+            s_cos[i] = cos_t[(size_t)pos * half + i];
+            s_sin[i] = sin_t[(size_t)pos * half + i];
+        }
+    __syncthreads();
     uint4 *qo = reinterpret_cast<uint4 *>(q_out + row * (int64_t)H * D);
     uint4 *ko = k_out ? reinterpret_cast<uint4 *>(k_out + row * (int64_t)G * D) : nullptr;
     uint4 *vo = v_out ? reinterpret_cast<uint4 *>(v_out + row * (int64_t)G * D) : nullptr;
@@ -127,7 +153,7 @@ __global__ void __launch_bounds__(256) qkv_rope_scatter_kernel(
         uint4 lo = src[vlo], hi = src[vhi];
         if (rope) {
             uint4 lo_o, hi_o;
-            rope8(lo, hi, lo_o, hi_o, cos_t, sin_t, pos, half, c);
+            rope8_smem(lo, hi, lo_o, hi_o, s_cos, s_sin, c);
             lo = lo_o;
             hi = hi_o;
         }

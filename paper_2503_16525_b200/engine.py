@@ -239,7 +239,8 @@ class Engine:
                 self._attention(q, rows, layer, arena_c, batch_c, o)
             if capture is not None:
                 capture.append((layer, q.clone(), o.clone()))
-            x += (o.view(n, H * HEAD_DIM) @ m.w_o[layer]).float()
+            # residual add fused into the cuBLAS epilogue (fp32 C/D, bf16 A/B)
+            x = torch.addmm(x, o.view(n, H * HEAD_DIM), m.w_o[layer], out_dtype=torch.float32)
             if capture is not None:
                 capture.append((layer, "hidden", x.clone()))
         return x
@@ -288,7 +289,7 @@ class Engine:
             qkv = x.to(torch.bfloat16) @ m.w_qkv[0]
             self._scatter(qkv, rows, 0, parena, pbatch, q, use_write=False)
             self._attention(q, rows, 0, parena, pbatch, o)
-            x += (o.view(n, H * HEAD_DIM) @ m.w_o[0]).float()
+            x = torch.addmm(x, o.view(n, H * HEAD_DIM), m.w_o[0], out_dtype=torch.float32)
             st._probe_keep = pbt
         qkv = x.to(torch.bfloat16) @ m.w_qkv[p]
         q1 = torch.empty(n, H, HEAD_DIM, dtype=torch.bfloat16, device=dev)
@@ -353,8 +354,8 @@ class Engine:
 
     def session_forward(self, st: BatchState, rows: RowSet, capture=None):
         x = self._embed(st.tokens, rows)
-        self.forward_rows(x, rows, range(self.cfg.num_layers), self.arena.c, st.batch_c,
-                          capture=capture)
+        x = self.forward_rows(x, rows, range(self.cfg.num_layers), self.arena.c, st.batch_c,
+                              capture=capture)
         last = torch.from_numpy(rows.row_off[1:] - 1).to(self.device)
         st.rows = rows
         st.hidden_last = x[last]
@@ -437,8 +438,8 @@ class Engine:
         tok = torch.from_numpy(np.asarray(new_tokens, dtype=np.int64)).to(dev)
         x = self._embed(tok, rows)
         max_kv = int(st.capacity.max())
-        self.forward_rows(x, rows, range(self.probe_layer), self.arena.c, st.batch_c,
-                          decode=True, max_kv=max_kv)
+        x = self.forward_rows(x, rows, range(self.probe_layer), self.arena.c, st.batch_c,
+                              decode=True, max_kv=max_kv)
         qkv = x.to(torch.bfloat16) @ self.model.w_qkv[self.probe_layer]
         q = torch.empty(R, cfg.num_heads, HEAD_DIM, dtype=torch.bfloat16, device=dev)
         zero = torch.zeros(R, dtype=torch.uint8, device=dev)
@@ -485,8 +486,8 @@ class Engine:
             tok_rows.append(int(new_tokens[r]))
         tok = torch.tensor(tok_rows, dtype=torch.int64, device=dev)
         x = self._embed(tok, rows)
-        self.forward_rows(x, rows, range(self.cfg.num_layers), self.arena.c, st.batch_c,
-                          decode=True, max_kv=int(st.capacity.max()))
+        x = self.forward_rows(x, rows, range(self.cfg.num_layers), self.arena.c, st.batch_c,
+                              decode=True, max_kv=int(st.capacity.max()))
         last = torch.from_numpy(rows.row_off[1:] - 1).to(dev)
         for r in range(R):
             st.tokens_host[r].append(int(new_tokens[r]))

@@ -153,8 +153,8 @@ def _forward_session(model: ToyModel, tokens, reuse, sets, decode_capacity=64):
     capture = []
     x = eng._embed(st.tokens, rows)
     x0 = x.clone()
-    eng.forward_rows(x, rows, range(eng.cfg.num_layers), eng.arena.c, st.batch_c,
-                     write_kv_per_layer=per_layer, capture=capture)
+    x = eng.forward_rows(x, rows, range(eng.cfg.num_layers), eng.arena.c, st.batch_c,
+                         write_kv_per_layer=per_layer, capture=capture)
     st.rows = rows
     st.hidden_last = x[-1:]
     states = _states_from_capture(eng, st, rows, capture, x0)
@@ -260,8 +260,8 @@ class ReuseSession:
                       np.array([0, len(pos)], dtype=np.int64))
         tok = torch.tensor([self.tokens[p] for p in pos], dtype=torch.int64, device=eng.device)
         x = eng._embed(tok, rows)
-        eng.forward_rows(x, rows, range(eng.cfg.num_layers), eng.arena.c, st.batch_c,
-                         decode=True, max_kv=int(st.capacity.max()))
+        x = eng.forward_rows(x, rows, range(eng.cfg.num_layers), eng.arena.c, st.batch_c,
+                             decode=True, max_kv=int(st.capacity.max()))
         elig = st.eligible
         for p in pos:
             if p in self.reused:
@@ -326,7 +326,8 @@ def prefill_with_selection(model: ToyModel, tokens, reuse, config: SelectionConf
     capture = []
     x = eng._embed(st.tokens, rows)
     x0 = x.clone()
-    eng.forward_rows(x, rows, range(eng.cfg.num_layers), eng.arena.c, st.batch_c, capture=capture)
+    x = eng.forward_rows(x, rows, range(eng.cfg.num_layers), eng.arena.c, st.batch_c,
+                         capture=capture)
     st.rows = rows
     st.hidden_last = x[-1:]
     states = _states_from_capture(eng, st, rows, capture, x0)
