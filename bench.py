@@ -151,7 +151,7 @@ def build_engine(args, device):
     cfg = K.ModelConfig(**shape, seed=0, max_positions=max(8192, args.seq + 64))
     model = K.ToyModel(cfg, device=device, init="device")
     src_pages = args.sources * ((args.seq + 63) // 64)
-    step_pages = (args.steps + 1) * args.batch * ((args.seq + 63) // 64)
+    step_pages = 2 * args.batch * ((args.seq + 63) // 64)
     arena = KVArena(cfg, src_pages + step_pages + 64, device)
     pool = CachePool(cfg, K.HashParams(window_size=8), arena=arena, device=device)
     eng = Engine(model, pool)
@@ -169,7 +169,7 @@ def algorithmic_counts(eng, st, cfg):
     import torch
     H, d, G = cfg.num_heads, cfg.d_k, cfg.kv_heads
     pos = st.rows.row_pos.to(torch.float64)
-    sess = float(4 * H * d * (pos + 1).sum().item()) * cfg.num_layers
+    sess = (pos + 1).sum() * (4.0 * H * d * cfg.num_layers)     # device scalar, no sync
     probe = 0.0
     alpha = 0.0
     for n in st.lengths:
@@ -219,7 +219,7 @@ def run_gpu(args, rank, world, device):
     timers = {}
     launches0 = N.launch_count["kernels"]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    step_ms, states = [], []
+    step_ms, counts, n_hit = [], [], []
     if args.profile:
         torch.cuda.cudart().cudaProfilerStart()
     start.record()
@@ -230,16 +230,16 @@ def run_gpu(args, rank, world, device):
         st = step(i, timers)
         s1.record()
         step_ms.append((s0, s1))
-        states.append(st)
         eng.timers = None
+        counts.append(algorithmic_counts(eng, st, cfg))
+        n_hit.append(float(st.n_hit.sum()) / float(st.lengths.sum()))
+        eng.release(st)                     # pages are reused in stream order
     end.record()
     torch.cuda.synchronize()
     if args.profile:
         torch.cuda.cudart().cudaProfilerStop()
-    counts = [algorithmic_counts(eng, st, cfg) for st in states]
-    n_hit = [float(st.n_hit.sum()) / float(st.lengths.sum()) for st in states]
-    for st in states:
-        eng.release(st)
+    for c in counts:
+        c["attention_flops"] = float(c["attention_flops"])
     barrier()
     clk = clocks.stop()
     launches = N.launch_count["kernels"] - launches0
