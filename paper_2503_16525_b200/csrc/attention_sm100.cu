@@ -357,7 +357,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     tc_fence_after();
     const uint32_t tmem = sh.tmem_base;
     if (warp >= 8) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 96;");
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
     if (warp == 8) {
         if (lane == 0) {
             tma_prefetch(&map_q);
