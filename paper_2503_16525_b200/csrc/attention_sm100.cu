@@ -548,6 +548,241 @@ __global__ void __launch_bounds__(kThreads2, 1)
     }
 }
 
+// ------------------------------------------------------------------ A1, head pairs, P in TMEM
+// As fwd2 (two query heads of one GQA group share every K/V tile), with the
+// FA4 arrangement: the softmax writes P (bf16, two per column) back over its
+// own S columns and O += P.V runs with A from tensor memory, so no P goes
+// through shared memory and the K/V ring gets 5 slots.  The MMA warp issues
+// PV_a(kb), QK_a(kb+1), PV_b(kb), QK_b(kb+1): in-order tcgen05 execution
+// makes QK_t(kb+1) overwrite S/P only after PV_t(kb) has read P, and each
+// head's softmax overlaps the other head's two MMAs.
+constexpr int RING3 = 5;
+
+struct Smem3 {
+    uint64_t q_full;
+    uint64_t ring_full[RING3], ring_empty[RING3];
+    uint64_t s_full[2], p_full[2], pv_done[2];
+    uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(kThreads2, 1)
+    fwd3_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
+                Params p) {
+    extern __shared__ uint8_t dsmem[];
+    __shared__ Smem3 sh;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tile = blockIdx.x, h0 = 2 * blockIdx.y;
+    const int g = h0 / (p.num_heads / p.kv_heads);
+    const int req = p.tile_req[tile], row0 = p.tile_row0[tile], nrows = p.tile_rows[tile];
+    const int kmax = p.causal ? p.row_pos[row0 + nrows - 1] + 1 : p.kv_len[req];
+    const int n_kb = (kmax + BN - 1) / BN;
+    const int pages_needed = (kmax + p.page_size - 1) / p.page_size;
+
+    const uint32_t base = align1024(smem_u32(dsmem));
+    const uint32_t sQ = base;                          // 2 tiles
+    const uint32_t sR = sQ + 2 * TILE_BYTES;           // RING3 tiles
+    uint8_t *gbase = dsmem + (base - smem_u32(dsmem));
+
+    if (threadIdx.x == 0) {
+        mbar_init(&sh.q_full, 1);
+        for (int i = 0; i < RING3; ++i) {
+            mbar_init(&sh.ring_full[i], 1);
+            mbar_init(&sh.ring_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&sh.s_full[i], 1);
+            mbar_init(&sh.p_full[i], 128);
+            mbar_init(&sh.pv_done[i], 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 9) tmem_alloc(&sh.tmem_base, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sh.tmem_base;
+
+    if (warp >= 8) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+        if (warp == 8 && lane == 0) {
+            tma_prefetch(&map_q);
+            tma_prefetch(&map_kv);
+            mbar_expect_tx(&sh.q_full, 2 * TILE_BYTES);
+            for (int t = 0; t < 2; ++t)
+                for (int hf = 0; hf < 2; ++hf)
+                    tma_load_3d(gbase + (sQ - base) + t * TILE_BYTES + hf * HALF_BYTES, &map_q,
+                                &sh.q_full, hf * 64, h0 + t, row0);
+            const int32_t *bt = p.block_table + (int64_t)req * p.max_pages;
+            for (int it = 0; it < 2 * n_kb; ++it) {
+                const int kb = it >> 1, kv = it & 1, slot = it % RING3;
+                if (it >= RING3) mbar_wait(&sh.ring_empty[slot], (uint32_t)((it / RING3) - 1) & 1u);
+                mbar_expect_tx(&sh.ring_full[slot], TILE_BYTES);
+                for (int q = 0; q < 2; ++q) {
+                    const int pi = 2 * kb + q;
+                    const int pg = bt[pi < pages_needed ? pi : 2 * kb];
+                    for (int hf = 0; hf < 2; ++hf)
+                        tma_load_4d(gbase + (sR - base) + slot * TILE_BYTES + hf * HALF_BYTES +
+                                        q * (HALF_BYTES / 2),
+                                    &map_kv, &sh.ring_full[slot], hf * 64, g, 0,
+                                    (pg * p.num_layers + p.layer) * 2 + kv);
+                }
+            }
+        } else if (warp == 9 && lane == 0) {
+            const uint32_t idesc_qk = umma_idesc_bf16(BM, BN, false);
+            const uint32_t idesc_pv = umma_idesc_bf16(BM, HD, true);
+            mbar_wait(&sh.q_full, 0);
+            auto issue_qk = [&](int t, int kb) {
+                const int slot = (2 * kb) % RING3;
+#pragma unroll
+                for (int k = 0; k < HD / 16; ++k) {
+                    const uint64_t da = umma_desc_sw128(
+                        sQ + t * TILE_BYTES + (k >> 2) * HALF_BYTES + (k & 3) * 32, 16, 1024);
+                    const uint64_t db = umma_desc_sw128(
+                        sR + slot * TILE_BYTES + (k >> 2) * HALF_BYTES + (k & 3) * 32, 16, 1024);
+                    umma_bf16(tmem + 128 * t, da, db, idesc_qk, k > 0 ? 1u : 0u);
+                }
+                umma_commit(&sh.s_full[t]);
+            };
+            if (n_kb >= 1) {
+                mbar_wait(&sh.ring_full[0], 0);
+                tc_fence_after();
+                issue_qk(0, 0);
+                issue_qk(1, 0);
+                umma_commit(&sh.ring_empty[0]);
+            }
+            for (int kb = 0; kb < n_kb; ++kb) {
+                const int itv = 2 * kb + 1, vslot = itv % RING3;
+                const int itk = 2 * kb + 2, kslot = itk % RING3;
+                const bool more = kb + 1 < n_kb;
+                mbar_wait(&sh.ring_full[vslot], (uint32_t)(itv / RING3) & 1u);
+                for (int t = 0; t < 2; ++t) {
+                    mbar_wait(&sh.p_full[t], (uint32_t)kb & 1u);
+                    tc_fence_after();
+#pragma unroll
+                    for (int k = 0; k < BN / 16; ++k) {
+                        const uint64_t db = umma_desc_sw128(sR + vslot * TILE_BYTES + k * 2048,
+                                                            HALF_BYTES, 1024);
+                        umma_bf16_ts(tmem + 256 + 128 * t, tmem + 128 * t + 8 * k, db, idesc_pv,
+                                     (kb > 0 || k > 0) ? 1u : 0u);
+                    }
+                    umma_commit(&sh.pv_done[t]);
+                    if (more) {
+                        if (t == 0) mbar_wait(&sh.ring_full[kslot], (uint32_t)(itk / RING3) & 1u);
+                        issue_qk(t, kb + 1);
+                    }
+                }
+                umma_commit(&sh.ring_empty[vslot]);
+                if (more) umma_commit(&sh.ring_empty[kslot]);
+            }
+        }
+        __syncwarp();
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+        const int t = warp >> 2;                 // head of this warpgroup
+        const int i = threadIdx.x & 127;         // row within tile == TMEM lane
+        const bool valid = i < nrows;
+        const int kend = !valid ? 0 : (p.causal ? p.row_pos[row0 + i] + 1 : kmax);
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        const uint32_t tS = tmem + 128 * t + lane_off, tO = tmem + 256 + 128 * t + lane_off;
+        float m = -INFINITY, l = 0.f;
+        float s[BN];
+        for (int kb = 0; kb < n_kb; ++kb) {
+            mbar_wait(&sh.s_full[t], (uint32_t)kb & 1u);
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS + c * 32, s + c * 32);
+            tmem_ld_wait();
+            const int kbase = kb * BN;
+            float mx[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
+            if (kbase + BN <= kend) {
+#pragma unroll
+                for (int c = 0; c < BN; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < BN; ++c) {
+                    s[c] = (kbase + c < kend) ? s[c] : -INFINITY;
+                    mx[c & 7] = fmaxf(mx[c & 7], s[c]);
+                }
+            }
+            const float mloc = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                     fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) *
+                               p.scale_log2;
+            if (mloc > m + kRescaleThreshold || (m == -INFINITY && mloc > -INFINITY)) {
+                const float factor = (m == -INFINITY) ? 0.f : fast_exp2(m - mloc);
+                if (kb >= 1 && m != -INFINITY) {
+                    // PV_t(kb-1) retired before QK_t(kb) (in-order), so O is quiescent
+                    float o[32];
+#pragma unroll
+                    for (int c = 0; c < HD / 32; ++c) {
+                        tmem_ld32(tO + c * 32, o);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) o[e] *= factor;
+                        tmem_st32(tO + c * 32, o);
+                    }
+                }
+                l *= factor;
+                m = mloc;
+            }
+            const float mu = (m == -INFINITY) ? 0.f : m;
+            float ls[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) ls[j] = 0.f;
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                uint32_t pk[32];
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                    const float e0 = fast_exp2(fmaf(s[hf * 64 + 2 * q], p.scale_log2, -mu));
+                    const float e1 = fast_exp2(fmaf(s[hf * 64 + 2 * q + 1], p.scale_log2, -mu));
+                    ls[(2 * q) & 7] += e0;
+                    ls[(2 * q + 1) & 7] += e1;
+                    pk[q] = pack_bf16x2(e0, e1);
+                }
+                tmem_st32(tS + hf * 32, reinterpret_cast<const float *>(pk));
+            }
+            l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&sh.p_full[t]);
+        }
+        const int64_t grow = (int64_t)row0 + i;
+        if (n_kb >= 1) mbar_wait(&sh.pv_done[t], (uint32_t)(n_kb - 1) & 1u);
+        tc_fence_after();
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        float o[32];
+#pragma unroll
+        for (int c = 0; c < HD / 32; ++c) {
+            tmem_ld32(tO + c * 32, o);
+            tmem_ld_wait();
+            if (valid) {
+                uint4 *dst = reinterpret_cast<uint4 *>(p.out + (grow * p.num_heads + h0 + t) * HD +
+                                                       c * 32);
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    uint4 w;
+                    w.x = pack_bf16x2(o[8 * v + 0] * inv, o[8 * v + 1] * inv);
+                    w.y = pack_bf16x2(o[8 * v + 2] * inv, o[8 * v + 3] * inv);
+                    w.z = pack_bf16x2(o[8 * v + 4] * inv, o[8 * v + 5] * inv);
+                    w.w = pack_bf16x2(o[8 * v + 6] * inv, o[8 * v + 7] * inv);
+                    dst[v] = w;
+                }
+            }
+        }
+        if (valid && p.lse != nullptr)
+            p.lse[grow * p.num_heads + h0 + t] =
+                (l > 0.f) ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 9) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
 // ------------------------------------------------------------------ D1 pass 2
 // CTA = (key tile kt of request r, kv head g).  Loops over the group's query
 // heads and the query tiles that can see the keys; S^T lands with one key per
@@ -786,7 +1021,13 @@ kvs_status kvs_attention_fwd(const void *q, const int32_t *row_pos, int64_t n_ro
     p.n_rows = n_rows;
     cudaStream_t s = (cudaStream_t)stream;
     const int group = num_heads / arena->kv_heads;
-    if (out != nullptr && group % 2 == 0 && getenv("KVS_ATTN_V1") == nullptr) {
+    const char *variant = getenv("KVS_ATTN");
+    if (out != nullptr && group % 2 == 0 && (variant == nullptr || variant[0] == '3')) {
+        const size_t smem = 1024 + attn::TILE_BYTES * (2 + attn::RING3);
+        cudaFuncSetAttribute(attn::fwd3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        attn::fwd3_kernel<<<dim3(n_tiles, num_heads / 2), attn::kThreads2, smem, s>>>(mq, mkv, p);
+    } else if (out != nullptr && group % 2 == 0 && variant[0] == '2') {
         const size_t smem = 1024 + attn::TILE_BYTES * (2 + attn::RING + 2);
         cudaFuncSetAttribute(attn::fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
