@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu legs)")
     ap.add_argument("--mode", default="selective", choices=["selective", "full", "naive"])
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo stages the remote-row exchange through the host (1-GPU test)")
     return ap.parse_args()
 
 
@@ -138,7 +140,7 @@ def cpu_reference_sample(seq: int, layers: int, heads_sample: int = 4):
 
 
 # ---------------------------------------------------------------------------- GPU leg
-def build_engine(args, device):
+def build_engine(args, device, rank=0, world=1):
     import torch
 
     import paper_2503_16525_b200 as K
@@ -156,10 +158,24 @@ def build_engine(args, device):
     pool = CachePool(cfg, K.HashParams(window_size=8), arena=arena, device=device)
     eng = Engine(model, pool)
     sources = source_requests(args.sources, args.seq, cfg.vocab_size, seed=0)
-    for i in range(0, len(sources), 4):
-        chunk = sources[i:i + 4]
-        st = eng.prefill_batch(chunk, mode="full")
-        eng.write_back(st, [f"src{i + j}" for j in range(len(chunk))])
+    # sharded pool: source i is written by GPU i % world; every rank inserts
+    # every entry in the same global order (so slot ids agree across ranks)
+    mine = [i for i in range(len(sources)) if i % world == rank]
+    pages = {}
+    for c in range(0, len(mine), 4):
+        ids = mine[c:c + 4]
+        st = eng.prefill_batch([sources[i] for i in ids], mode="full")
+        for r, i in enumerate(ids):
+            pages[i] = st.pages[r]
+        st.pages = []
+    for i, toks in enumerate(sources):
+        if i in pages:
+            pool.insert_pages(f"src{i}", toks, pages[i])
+        else:
+            pool.insert_remote(f"src{i}", toks, owner=i % world)
+    if world > 1:
+        from paper_2503_16525_b200.shard import RemoteFetcher
+        eng.fetcher = RemoteFetcher(eng)
     torch.cuda.synchronize()
     return cfg, model, pool, eng, sources
 
@@ -175,10 +191,11 @@ def algorithmic_counts(eng, st, cfg):
     for n in st.lengths:
         probe += 4.0 * H * d * n * (n + 1) / 2.0
         alpha += 2.0 * H * d * n * (n + 1)
-    n_r = st.n_hit.astype(np.float64)
-    B = st.budgets.astype(np.float64) if st.budgets is not None else np.zeros_like(n_r)
-    sel_bytes = float((n_r * (2 * G * d * 2 + 12)).sum() + (4 * B).sum())
-    return {"attention_flops": sess + probe, "alpha_flops": alpha, "select_bytes": sel_bytes}
+    n_r = st.n_hit_dev.to(torch.float64).sum()
+    B = st.budgets_dev.to(torch.float64).sum() if st.budgets_dev is not None else 0.0
+    sel_bytes = n_r * (2 * G * d * 2 + 12) + 4 * B
+    return {"attention_flops": sess + probe, "alpha_flops": alpha, "select_bytes": sel_bytes,
+            "hit": n_r / float(st.lengths.sum())}      # device scalars: no sync in the loop
 
 
 def run_gpu(args, rank, world, device):
@@ -189,7 +206,7 @@ def run_gpu(args, rank, world, device):
     from paper_2503_16525_b200.workload import request_batches
 
     torch.cuda.set_device(device)
-    cfg, model, pool, eng, sources = build_engine(args, device)
+    cfg, model, pool, eng, sources = build_engine(args, device, rank, world)
     n_steps = args.warmup + args.steps
     batches = request_batches(sources, n_steps, args.batch, args.seq, args.hit, cfg.vocab_size,
                               seed=1 + rank)
@@ -219,7 +236,8 @@ def run_gpu(args, rank, world, device):
     timers = {}
     launches0 = N.launch_count["kernels"]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    step_ms, counts, n_hit = [], [], []
+    step_ms, counts = [], []
+    eng.reset_timer_events(reserve=args.steps * 160)
     if args.profile:
         torch.cuda.cudart().cudaProfilerStart()
     start.record()
@@ -232,14 +250,13 @@ def run_gpu(args, rank, world, device):
         step_ms.append((s0, s1))
         eng.timers = None
         counts.append(algorithmic_counts(eng, st, cfg))
-        n_hit.append(float(st.n_hit.sum()) / float(st.lengths.sum()))
         eng.release(st)                     # pages are reused in stream order
     end.record()
     torch.cuda.synchronize()
     if args.profile:
         torch.cuda.cudart().cudaProfilerStop()
-    for c in counts:
-        c["attention_flops"] = float(c["attention_flops"])
+    counts = [{k: float(v) for k, v in c.items()} for c in counts]
+    n_hit = [c["hit"] for c in counts]
     barrier()
     clk = clocks.stop()
     launches = N.launch_count["kernels"] - launches0
@@ -322,10 +339,14 @@ def main():
                     "d2h_bytes_per_step": 0}}))
         return
     import torch
+    ngpu = torch.cuda.device_count()
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    device = torch.device("cuda", local)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local % ngpu))
+        else:
+            dist.init_process_group("gloo")
+    device = torch.device("cuda", local % ngpu)
     res = run_gpu(args, rank, world, device)
     if rank != 0:
         if world > 1:
@@ -356,6 +377,8 @@ def main():
                               "ms_per_step": kern["dhd_alpha"]}
     if "gather" in kern:
         extra["gather_ms_per_step"] = kern["gather"]
+    if "remote_fetch" in kern:
+        extra["remote_fetch_ms_per_step"] = kern["remote_fetch"]
     line = {
         "metric": METRIC, "value": value, "unit": "tok/s", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,

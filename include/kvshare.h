@@ -143,6 +143,18 @@ kvs_status kvs_gather_kv(const kvs_kv_arena *arena, const kvs_batch *batch,
                          int32_t layer_begin, int32_t layer_end, const kvs_rope *rope,
                          kvs_stream_t stream);
 
+/* X1 remote-shard fetch (multi-GPU).  The owner packs the rows
+ * (slot, cand) a peer hit - all layers, K and V - into a dense buffer
+ * [n_rows][L][2][kv_heads*head_dim] bf16 that travels over NCCL send/recv;
+ * the requester unpacks them into its pages at flat positions flat_t,
+ * re-aligning K by (pos - cand) like kvs_gather_kv.                       */
+kvs_status kvs_pack_rows(const kvs_kv_arena *arena, const int32_t *slot, const int32_t *cand,
+                         int64_t n_rows, const int32_t *slot_pages, int32_t slot_max_pages,
+                         void *out, kvs_stream_t stream);
+kvs_status kvs_unpack_rows(const kvs_kv_arena *arena, const kvs_batch *batch,
+                           const int64_t *flat_t, const int32_t *cand, int64_t n_rows,
+                           const void *in, const kvs_rope *rope, kvs_stream_t stream);
+
 /* Post-GEMM step for a set of query rows: qkv[row] = [q (H*d) | k (kvh*d) | v (kvh*d)]
  * bf16.  Rotates q,k by position (rope nullable), writes q to q_out[row][H][d],
  * writes k,v into the arena at (row_req, row_pos, layer) when write_kv[row]

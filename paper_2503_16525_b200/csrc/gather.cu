@@ -233,6 +233,64 @@ __global__ void __launch_bounds__(1024) build_rows_kernel(
     if (threadIdx.x == 0 && counts != nullptr) counts[r] = carry;
 }
 
+// X1 pack: rows (slot, cand) of the local pool -> dense [row][layer][K/V][G*D]
+// for a peer that hit them (one CTA per row).
+__global__ void __launch_bounds__(128) pack_rows_kernel(
+    Arena A, const int32_t *__restrict__ slot, const int32_t *__restrict__ cand,
+    const int32_t *__restrict__ slot_pages, int32_t slot_max_pages, uint4 *__restrict__ out) {
+    const int64_t r = blockIdx.x;
+    const int32_t s = slot[r], c = cand[r];
+    const int64_t page = slot_pages[(int64_t)s * slot_max_pages + c / A.P];
+    const int vvec = A.G * A.D / 8;
+    uint4 *dst = out + r * (int64_t)A.L * 2 * vvec;
+    for (int layer = 0; layer < A.L; ++layer)
+        for (int kv = 0; kv < 2; ++kv) {
+            const uint4 *src = reinterpret_cast<const uint4 *>(A.row(page, layer, kv, c % A.P));
+            uint4 *d = dst + (layer * 2 + kv) * vvec;
+            for (int v = threadIdx.x; v < vvec; v += blockDim.x) d[v] = src[v];
+        }
+}
+
+// X1 unpack: dense rows received from peers -> the request's pages at flat
+// position t[r], K re-aligned by (pos - cand[r]) (G1 semantics).
+__global__ void __launch_bounds__(128) unpack_rows_kernel(
+    Arena A, const int64_t *__restrict__ req_off, int32_t n_req,
+    const int32_t *__restrict__ block_table, int32_t max_pages, const int64_t *__restrict__ flat_t,
+    const int32_t *__restrict__ cand, const uint4 *__restrict__ in,
+    const float *__restrict__ cos_t, const float *__restrict__ sin_t) {
+    const int64_t r = blockIdx.x;
+    const int64_t t = flat_t[r];
+    int lo = 0, hi = n_req;
+    while (hi - lo > 1) {
+        int mid = (lo + hi) >> 1;
+        if (req_off[mid] <= t) lo = mid; else hi = mid;
+    }
+    const int32_t pos = (int32_t)(t - req_off[lo]);
+    const int32_t delta = pos - cand[r];
+    const int64_t page = block_table[(int64_t)lo * max_pages + pos / A.P];
+    const int half = A.D / 2, chunks = half / 8, vvec = A.G * A.D / 8;
+    const uint4 *src = in + r * (int64_t)A.L * 2 * vvec;
+    for (int layer = 0; layer < A.L; ++layer) {
+        const uint4 *sk = src + (layer * 2 + 0) * vvec;
+        const uint4 *sv = src + (layer * 2 + 1) * vvec;
+        uint4 *dk = reinterpret_cast<uint4 *>(A.row(page, layer, 0, pos % A.P));
+        uint4 *dv = reinterpret_cast<uint4 *>(A.row(page, layer, 1, pos % A.P));
+        for (int v = threadIdx.x; v < vvec; v += blockDim.x) dv[v] = sv[v];
+        if (cos_t == nullptr || delta == 0) {
+            for (int v = threadIdx.x; v < vvec; v += blockDim.x) dk[v] = sk[v];
+        } else {
+            for (int it = threadIdx.x; it < A.G * chunks; it += blockDim.x) {
+                const int g = it / chunks, c = it % chunks;
+                const int vlo = g * (A.D / 8) + c, vhi = vlo + chunks;
+                uint4 lo_o, hi_o;
+                rope8(sk[vlo], sk[vhi], lo_o, hi_o, cos_t, sin_t, delta, half, c);
+                dk[vlo] = lo_o;
+                dk[vhi] = hi_o;
+            }
+        }
+    }
+}
+
 }  // namespace kvs
 
 using namespace kvs;
@@ -295,6 +353,31 @@ kvs_status kvs_build_rows(const int64_t *req_off, int32_t n_req, const int32_t *
     build_rows_kernel<<<n_req, 1024, 0, (cudaStream_t)stream>>>(
         req_off, src_slot, selected, counts, row_off, row_tok, row_req, row_pos, write_kv);
     KVS_CHECK_LAUNCH("kvs_build_rows");
+    return KVS_OK;
+}
+
+kvs_status kvs_pack_rows(const kvs_kv_arena *arena, const int32_t *slot, const int32_t *cand,
+                         int64_t n_rows, const int32_t *slot_pages, int32_t slot_max_pages,
+                         void *out, kvs_stream_t stream) {
+    KVS_REQUIRE(arena != nullptr, KVS_EPARAM, "null arena");
+    KVS_REQUIRE((arena->kv_heads * arena->head_dim) % 8 == 0, KVS_ESHAPE, "row width % 8 != 0");
+    if (n_rows <= 0) return KVS_OK;
+    pack_rows_kernel<<<(unsigned)n_rows, 128, 0, (cudaStream_t)stream>>>(
+        make_arena(arena), slot, cand, slot_pages, slot_max_pages, (uint4 *)out);
+    KVS_CHECK_LAUNCH("kvs_pack_rows");
+    return KVS_OK;
+}
+
+kvs_status kvs_unpack_rows(const kvs_kv_arena *arena, const kvs_batch *batch,
+                           const int64_t *flat_t, const int32_t *cand, int64_t n_rows,
+                           const void *in, const kvs_rope *rope, kvs_stream_t stream) {
+    KVS_REQUIRE(arena && batch, KVS_EPARAM, "null arena/batch");
+    KVS_REQUIRE(arena->head_dim % 16 == 0, KVS_ESHAPE, "head_dim must be a multiple of 16");
+    if (n_rows <= 0) return KVS_OK;
+    unpack_rows_kernel<<<(unsigned)n_rows, 128, 0, (cudaStream_t)stream>>>(
+        make_arena(arena), batch->req_off, batch->n_req, batch->block_table, batch->max_pages,
+        flat_t, cand, (const uint4 *)in, rope ? rope->cos : nullptr, rope ? rope->sin : nullptr);
+    KVS_CHECK_LAUNCH("kvs_unpack_rows");
     return KVS_OK;
 }
 

@@ -60,16 +60,18 @@ class RowSet:
     n_tiles: int = 0
 
     def build_tiles(self, device):
-        req, row0, rows = [], [], []
-        for r in range(len(self.row_off) - 1):
-            a, b = int(self.row_off[r]), int(self.row_off[r + 1])
-            for s in range(a, b, TILE):
-                req.append(r)
-                row0.append(s)
-                rows.append(min(TILE, b - s))
-        self.n_tiles = len(req)
-        self.tiles = torch.tensor([req, row0, rows], dtype=torch.int32, device=device) \
-            if req else torch.zeros((3, 1), dtype=torch.int32, device=device)
+        off = np.asarray(self.row_off, dtype=np.int64)
+        cnt = np.diff(off)
+        ntile = (cnt + TILE - 1) // TILE
+        req = np.repeat(np.arange(len(cnt), dtype=np.int64), ntile)
+        first = np.repeat(np.cumsum(ntile) - ntile, ntile)
+        k = np.arange(int(ntile.sum()), dtype=np.int64) - first
+        row0 = off[req] + k * TILE
+        rows = np.minimum(TILE, off[req + 1] - row0)
+        self.n_tiles = int(ntile.sum())
+        t = np.stack([req, row0, rows]).astype(np.int32) if self.n_tiles else \
+            np.zeros((3, 1), dtype=np.int32)
+        self.tiles = torch.from_numpy(t).to(device, non_blocking=True)
         return self
 
 
@@ -87,7 +89,7 @@ class BatchState:
     capacity: np.ndarray                # token capacity per request
     src_slot: torch.Tensor | None = None
     src_cand: torch.Tensor | None = None
-    n_hit: np.ndarray | None = None
+    n_hit_dev: torch.Tensor | None = None    # int32 [R] hit counts (device)
     selected: torch.Tensor | None = None   # uint8 flat
     dv_l1: torch.Tensor | None = None      # f32 flat (probe-layer deviation)
     alpha: torch.Tensor | None = None
@@ -98,6 +100,22 @@ class BatchState:
     hidden_last: torch.Tensor | None = None  # fp32 [R, d_model]
     ctx_len: np.ndarray | None = None
     tokens_host: list = field(default_factory=list)
+    budgets_dev: torch.Tensor | None = None
+
+    @property
+    def n_hit(self) -> np.ndarray:
+        """Host copy of the hit counts (synchronises; not used on the hot path)."""
+        if self.n_hit_dev is None:
+            return np.zeros(len(self.lengths), dtype=np.int64)
+        return self.n_hit_dev.cpu().numpy().astype(np.int64)
+
+    @n_hit.setter
+    def n_hit(self, value):
+        self.n_hit_dev = torch.as_tensor(np.asarray(value, dtype=np.int32)).to(self.req_off.device)
+
+    @property
+    def budgets(self):
+        return None if self.budgets_dev is None else self.budgets_dev.cpu().numpy()
 
 
 class _ProbeArena:
@@ -132,12 +150,28 @@ class Engine:
                                  self.cfg.max_positions)
         self.probe_layer = 1 if self.cfg.num_layers >= 2 else 0
         self.timers = None          # {name: [(start_event, end_event), ...]} when profiling
+        self.fetcher = None         # shard.RemoteFetcher when the pool is sharded over GPUs
+        self._events: list = []
+        self._ev_next = 0
 
     # ------------------------------------------------------------------ helpers
+    def reset_timer_events(self, reserve: int = 0):
+        """Reuse pre-created events (creating events inside a timed loop costs)."""
+        while len(self._events) < reserve:
+            self._events.append(torch.cuda.Event(enable_timing=True))
+        self._ev_next = 0
+
+    def _event(self):
+        if self._ev_next == len(self._events):
+            self._events.append(torch.cuda.Event(enable_timing=True))
+        ev = self._events[self._ev_next]
+        self._ev_next += 1
+        return ev
+
     def _timed(self, name, fn, *args):
         if self.timers is None:
             return fn(*args)
-        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s, e = self._event(), self._event()
         s.record()
         out = fn(*args)
         e.record()
@@ -247,17 +281,22 @@ class Engine:
 
     # ------------------------------------------------------------------ prefill
     def lookup(self, st: BatchState):
+        """R2 for the whole batch; hit counts stay on the device (no sync)."""
         res = self.pool.lookup_device(st.tokens, st.req_off, st.req_off_host)
         st.src_slot, st.src_cand = res.src_slot, res.src_cand
-        st.n_hit = res.n_hit.cpu().numpy().astype(np.int64)        # sync 1
+        st.n_hit_dev = res.n_hit
         st._contributed = res.contributed
         return st
 
     def gather(self, st: BatchState):
-        if st.n_hit is None or st.n_hit.sum() == 0:
+        if not self.pool.entries:
             return
         idx = self.pool._build_index()
-        self._timed("gather", N.call, "kvs_gather_kv", self.arena.c, st.batch_c, st.src_slot.data_ptr(),
+        slot = st.src_slot
+        if self.fetcher is not None:
+            slot = self.fetcher.local_mask(st.src_slot, idx)
+            self._timed("remote_fetch", self.fetcher.fetch, st, idx)
+        self._timed("gather", N.call, "kvs_gather_kv", self.arena.c, st.batch_c, slot.data_ptr(),
                st.src_cand.data_ptr(), idx["slot_pages"].data_ptr(), idx["slot_max_pages"], 0,
                self.cfg.num_layers, self._rope(), N.stream_ptr())
 
@@ -299,9 +338,10 @@ class Engine:
         self._scatter(qkv, rows, p, self.arena.c, st.batch_c, q1, write_kv=wk, v_out=v_true)
         return rows, q1, v_true
 
-    def _select(self, st: BatchState, v_true, alpha, budgets: np.ndarray):
+    def _select(self, st: BatchState, v_true, alpha, budgets):
         dev, n = self.device, int(st.req_off_host[-1])
-        bud = torch.from_numpy(budgets.astype(np.int32)).to(dev, non_blocking=True)
+        bud = budgets if torch.is_tensor(budgets) else \
+            torch.from_numpy(np.asarray(budgets, dtype=np.int32)).to(dev, non_blocking=True)
         dv = torch.empty(n, dtype=torch.float32, device=dev)
         score = torch.empty(n, dtype=torch.float32, device=dev)
         sel = torch.empty(n, dtype=torch.uint8, device=dev)
@@ -324,8 +364,15 @@ class Engine:
                rows.row_pos.data_ptr(), rows.tiles[0].data_ptr(), rows.tiles[1].data_ptr(),
                rows.tiles[2].data_ptr(), rows.n_tiles, None, self.scale, alpha.data_ptr(),
                ws.data_ptr(), ws.numel(), N.stream_ptr())
-        st.budgets = np.array([budget(ratio, int(h)) for h in st.n_hit], dtype=np.int32)
-        st.dv_l1, st.score, st.selected = self._select(st, v_true, alpha, st.budgets)
+        if getattr(st, "n_hit_dev", None) is not None:
+            # selection.py:51-52 on the device: IEEE-double product, ceil, clamp
+            nh = st.n_hit_dev.to(torch.float64)
+            bud = torch.minimum(torch.ceil(nh * float(ratio)), nh).to(torch.int32)
+        else:
+            bud = torch.from_numpy(np.array([budget(ratio, int(h)) for h in st.n_hit],
+                                            dtype=np.int32)).to(self.device)
+        st.budgets_dev = bud
+        st.dv_l1, st.score, st.selected = self._select(st, v_true, alpha, bud)
         st.alpha = alpha
         st._probe_q, st._probe_v_true = q1, v_true
         return st
@@ -369,7 +416,7 @@ class Engine:
             raise ParameterError(f"ratio must lie in [0, 1], got {ratio}")
         st = self.new_batch(token_lists, decode_capacity, tokens_dev)
         if mode == "full" or not self.pool.entries:
-            st.n_hit = np.zeros(len(st.lengths), dtype=np.int64)
+            st.n_hit_dev = torch.zeros(len(st.lengths), dtype=torch.int32, device=self.device)
             rows = self.build_rows(st, None)
             rows.write_kv.fill_(1)
             self.session_forward(st, rows)
@@ -377,7 +424,7 @@ class Engine:
             return st
         self.lookup(st)
         self.gather(st)
-        if mode == "selective" and ratio > 0 and st.n_hit.sum() > 0:
+        if mode == "selective" and ratio > 0:
             self.probe_and_select(st, ratio)
             rows = self.build_rows(st, st.selected)
         else:
@@ -402,7 +449,7 @@ class Engine:
         if st.dv_l1 is not None:
             return
         n = int(st.req_off_host[-1])
-        if st.src_slot is None or st.n_hit is None or st.n_hit.sum() == 0:
+        if st.src_slot is None or not bool((st.src_slot >= 0).any()):
             st.dv_l1 = torch.zeros(n, dtype=torch.float32, device=self.device)
             return
         _, _, v_true = self._probe(st, write_k=False)

@@ -82,6 +82,8 @@ class KVEntry:
     slot: int = -1
     last_access: int = 0
     insert_seq: int = 0
+    owner: int = -1          # GPU rank holding the K/V pages (-1 = this GPU)
+    owner_slot: int = -1     # the entry's slot id on its owner (remote entries)
 
     @property
     def n_tokens(self) -> int:
@@ -212,9 +214,22 @@ class CachePool:
         self._slots[entry.slot] = None
         self._slot_tokens[entry.slot] = None
         self._slot_hash[entry.slot] = None
-        if release:
+        if release and entry.owner < 0:
             self.arena.release(entry.pages)
         self._dirty = True
+
+    def insert_remote(self, request_id: str, tokens, owner: int,
+                      owner_slot: int | None = None) -> KVEntry:
+        """Replicate the token side of an entry whose K/V pages live on GPU
+        ``owner`` in its slot ``owner_slot`` (sharded pool).
+        Lookups see it like any other entry; its rows are fetched from the
+        owner by shard.RemoteFetcher.  ``owner_slot`` defaults to this pool's
+        slot, which is the owner's too when every rank inserts in one order."""
+        entry = self.insert_pages(request_id, tokens, [])
+        entry.owner = int(owner)
+        entry.owner_slot = entry.slot if owner_slot is None else int(owner_slot)
+        self._dirty = True
+        return entry
 
     def insert_pages(self, request_id: str, tokens, pages) -> KVEntry:
         """Register K/V already resident in arena pages (zero-copy write-back
@@ -311,11 +326,19 @@ class CachePool:
                                                         "slot_rank", "rank2slot")))
         max_pages = max([len(e.pages) for e in self._slots if e is not None] + [1])
         sp = np.zeros((max(n_slots, 1), max_pages), dtype=np.int32)
+        owner = np.full(max(n_slots, 1), -1, dtype=np.int32)
+        oslot = np.arange(max(n_slots, 1), dtype=np.int32)
         for s in live:
             pg = self._slots[s].pages
             sp[s, :len(pg)] = pg
+            owner[s] = self._slots[s].owner
+            if self._slots[s].owner >= 0:
+                oslot[s] = self._slots[s].owner_slot
         idx["slot_pages"] = torch.from_numpy(sp).to(dev)
         idx["slot_max_pages"] = max_pages
+        idx["slot_owner"] = owner
+        idx["slot_on_owner"] = oslot
+        idx["slot_owner_dev"] = torch.from_numpy(owner).to(dev)
         idx["c"] = c
         self._index = idx
         self._dirty = False
