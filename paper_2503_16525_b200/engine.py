@@ -95,7 +95,6 @@ class BatchState:
     alpha: torch.Tensor | None = None
     score: torch.Tensor | None = None
     eligible: torch.Tensor | None = None   # uint8 flat (decode-stage)
-    budgets: np.ndarray | None = None
     rows: RowSet | None = None
     hidden_last: torch.Tensor | None = None  # fp32 [R, d_model]
     ctx_len: np.ndarray | None = None
