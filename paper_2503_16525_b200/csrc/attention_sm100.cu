@@ -23,6 +23,25 @@
 namespace kvs {
 namespace attn {
 
+// Diagnostic timeline (KVS_ATTN_TRACE builds only): clock64 stamps of the
+// first CTA's pipeline events, read back with kvs_attn_trace_dump().
+#ifdef KVS_ATTN_TRACE
+__device__ long long g_trace[8192];
+__device__ int g_trace_n;
+#define TRACE(tag, kb)                                                              \
+    do {                                                                            \
+        if (blockIdx.x == gridDim.x - 1 && blockIdx.y == 0) {                      \
+            int _i = atomicAdd(&g_trace_n, 1);                                      \
+            if (_i < 4096) {                                                        \
+                g_trace[2 * _i] = clock64();                                        \
+                g_trace[2 * _i + 1] = ((long long)(tag) << 32) | (unsigned)(kb);    \
+            }                                                                       \
+        }                                                                           \
+    } while (0)
+#else
+#define TRACE(tag, kb) do {} while (0)
+#endif
+
 constexpr int BM = 128, BN = 128, HD = 128;
 constexpr int HALF_BYTES = 128 * 128;      // one [128 rows x 64 bf16] SW128 half tile
 constexpr int TILE_BYTES = 2 * HALF_BYTES; // [128 rows x 128 bf16]
@@ -655,8 +674,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 const int itk = 2 * kb + 2, kslot = itk % RING3;
                 const bool more = kb + 1 < n_kb;
                 mbar_wait(&sh.ring_full[vslot], (uint32_t)(itv / RING3) & 1u);
+                TRACE(10, kb);
                 for (int t = 0; t < 2; ++t) {
                     mbar_wait(&sh.p_full[t], (uint32_t)kb & 1u);
+                    TRACE(11 + t, kb);
                     tc_fence_after();
 #pragma unroll
                     for (int k = 0; k < BN / 16; ++k) {
@@ -668,6 +689,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
                     umma_commit(&sh.pv_done[t]);
                     if (more) {
                         if (t == 0) mbar_wait(&sh.ring_full[kslot], (uint32_t)(itk / RING3) & 1u);
+                        TRACE(13 + t, kb);
                         issue_qk(t, kb + 1);
                     }
                 }
@@ -688,10 +710,12 @@ __global__ void __launch_bounds__(kThreads2, 1)
         float s[BN];
         for (int kb = 0; kb < n_kb; ++kb) {
             mbar_wait(&sh.s_full[t], (uint32_t)kb & 1u);
+            if (i == 0) TRACE(20 + 10 * t, kb);
             tc_fence_after();
 #pragma unroll
             for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS + c * 32, s + c * 32);
             tmem_ld_wait();
+            if (i == 0) TRACE(21 + 10 * t, kb);
             const int kbase = kb * BN;
             float mx[8];
 #pragma unroll
@@ -745,6 +769,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
             }
             l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
             tmem_st_wait();
+            if (i == 0) TRACE(22 + 10 * t, kb);
             tc_fence_before();
             mbar_arrive(&sh.p_full[t]);
         }
@@ -1045,6 +1070,23 @@ kvs_status kvs_attention_fwd(const void *q, const int32_t *row_pos, int64_t n_ro
     }
     KVS_CHECK_LAUNCH("kvs_attention_fwd");
     return KVS_OK;
+}
+
+int32_t kvs_attn_trace_dump(int64_t *host, int32_t max_pairs) {
+#ifdef KVS_ATTN_TRACE
+    int n = 0;
+    cudaMemcpyFromSymbol(&n, attn::g_trace_n, sizeof(int));
+    if (n > max_pairs) n = max_pairs;
+    if (n > 4096) n = 4096;
+    cudaMemcpyFromSymbol(host, attn::g_trace, sizeof(long long) * 2 * n);
+    int zero = 0;
+    cudaMemcpyToSymbol(attn::g_trace_n, &zero, sizeof(int));
+    return n;
+#else
+    (void)host;
+    (void)max_pairs;
+    return -1;
+#endif
 }
 
 size_t kvs_dhd_alpha_workspace(int64_t n_total, int32_t num_heads, int32_t kv_heads) {
