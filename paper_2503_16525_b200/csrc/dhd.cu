@@ -142,6 +142,175 @@ __global__ void __launch_bounds__(1024) radix_select_kernel(
     }
 }
 
+// ---------------------------------------------------------------- D2 fused
+// One persistent launch: CTAs pull 64-row chunks (request-major) from an
+// atomic work counter and stream dv-L1 x alpha for them (8 warps x 8 rows,
+// 16-byte loads).  A per-request completion counter elects the CTA that
+// finished a request's last chunk to run that request's top-B selection while
+// the other CTAs keep streaming later requests.  Selection: 4 radix passes
+// (8-bit digits) over the descending-score key ~bits(score) of the reused
+// rows give the B-th score; rows strictly better are kept and the remaining
+// budget is filled with the equal-score rows in ascending position order
+// (selection.py:63-66 tie rule) by an ordered block scan.
+constexpr int kSelChunk = 64;
+constexpr int kSelThreads = 256;
+
+__device__ __forceinline__ uint32_t score_key(float sc) {
+    return ~__float_as_uint(fmaxf(sc, 0.f));
+}
+
+__device__ void select_request(const float *__restrict__ score, const int32_t *__restrict__ src_slot,
+                               int64_t s, int64_t n, int32_t B, uint8_t *__restrict__ selected,
+                               uint32_t *hist, uint32_t *sh) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (B <= 0) {
+        for (int64_t i = tid; i < n; i += kSelThreads) selected[s + i] = 0;
+        return;
+    }
+    // sh[0] = prefix, sh[1] = remaining k, sh[2] = count strictly better
+    if (tid == 0) { sh[0] = 0; sh[1] = (uint32_t)B; }
+    __syncthreads();
+    uint32_t mask = 0;
+    for (int pass = 0; pass < 4; ++pass) {
+        const int shift = 24 - 8 * pass;
+        hist[tid] = 0;
+        __syncthreads();
+        const uint32_t prefix = sh[0];
+        for (int64_t i = tid; i < n; i += kSelThreads) {
+            if (src_slot[s + i] < 0) continue;
+            const uint32_t key = score_key(score[s + i]);
+            if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 0xff], 1u);
+        }
+        __syncthreads();
+        // exclusive scan of the 256 bins (one per thread) -> digit holding the k-th key
+        const uint32_t c = hist[tid];
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        __shared__ uint32_t wsum[8];
+        if (lane == 31) wsum[wid] = incl;
+        __syncthreads();
+        uint32_t base = 0;
+        for (int w = 0; w < wid; ++w) base += wsum[w];
+        const uint32_t excl = base + incl - c;
+        const uint32_t k = sh[1];
+        __syncthreads();
+        if (c > 0 && excl < k && excl + c >= k) {
+            sh[0] = prefix | ((uint32_t)tid << shift);
+            sh[1] = k - excl;
+        }
+        mask |= 0xffu << shift;
+        __syncthreads();
+    }
+    const uint32_t thr = sh[0];          // key of the B-th best reused row
+    const uint32_t ties_needed = sh[1];  // how many rows with key == thr to keep
+    // ordered scan over positions: keep key < thr, and the first ties_needed ties
+    __shared__ uint32_t carry;
+    __shared__ uint32_t wcnt[8];
+    if (tid == 0) carry = 0;
+    __syncthreads();
+    for (int64_t b0 = 0; b0 < n; b0 += kSelThreads) {
+        const int64_t i = b0 + tid;
+        bool reused = false, tie = false, better = false;
+        if (i < n && src_slot[s + i] >= 0) {
+            reused = true;
+            const uint32_t key = score_key(score[s + i]);
+            better = key < thr;
+            tie = key == thr;
+        }
+        const uint32_t bal = __ballot_sync(0xffffffffu, tie);
+        if (lane == 0) wcnt[wid] = __popc(bal);
+        __syncthreads();
+        uint32_t before = carry;
+        for (int w = 0; w < wid; ++w) before += wcnt[w];
+        before += __popc(bal & ((1u << lane) - 1));
+        if (i < n) selected[s + i] = (reused && (better || (tie && before < ties_needed))) ? 1 : 0;
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t t = 0;
+            for (int w = 0; w < 8; ++w) t += wcnt[w];
+            carry += t;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kSelThreads) dhd_select_fused_kernel(
+    const __nv_bfloat16 *__restrict__ v_true, const float *__restrict__ alpha,
+    const int32_t *__restrict__ src_slot, int32_t layer, ArenaC A,
+    const int64_t *__restrict__ req_off, const int32_t *__restrict__ chunk_off, int32_t n_req,
+    const int32_t *__restrict__ budget, const int32_t *__restrict__ block_table,
+    int32_t max_pages, float *__restrict__ dv_l1, float *__restrict__ score,
+    uint8_t *__restrict__ selected, uint32_t *__restrict__ counters) {
+    // counters[0] = work cursor, counters[1 + r] = finished chunks of request r
+    __shared__ uint32_t hist[256];
+    __shared__ uint32_t sh[4];
+    __shared__ int s_item, s_last;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int total = chunk_off[n_req];
+    const int nvec = A.G * A.D / 8;
+    while (true) {
+        if (threadIdx.x == 0) s_item = (int)atomicAdd(&counters[0], 1u);
+        __syncthreads();
+        const int item = s_item;
+        if (item >= total) break;
+        int r = 0, hi = n_req;            // chunk_off[r] <= item < chunk_off[r+1]
+        while (hi - r > 1) {
+            const int mid = (r + hi) >> 1;
+            if (chunk_off[mid] <= item) r = mid; else hi = mid;
+        }
+        const int64_t s = req_off[r], n = req_off[r + 1] - s;
+        const int64_t i0 = (int64_t)(item - chunk_off[r]) * kSelChunk;
+        for (int j = wid; j < kSelChunk; j += kSelThreads / 32) {
+            const int64_t i = i0 + j;
+            if (i >= n) break;
+            const int64_t t = s + i;
+            if (src_slot[t] < 0) {
+                if (lane == 0) { dv_l1[t] = 0.f; score[t] = 0.f; }
+                continue;
+            }
+            const int64_t page = block_table[(int64_t)r * max_pages + i / A.P];
+            const uint4 *vc = reinterpret_cast<const uint4 *>(A.row(page, layer, 1, (int)(i % A.P)));
+            const uint4 *vt = reinterpret_cast<const uint4 *>(v_true + t * (int64_t)(A.G * A.D));
+            float acc = 0.f;
+            for (int v0 = 0; v0 < nvec; v0 += 128) {
+                uint4 a[4], b[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int v = v0 + k * 32 + lane;
+                    if (v < nvec) {
+                        a[k] = __ldcs(vc + v);
+                        b[k] = __ldcs(vt + v);
+                    }
+                }
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (v0 + k * 32 + lane < nvec) acc += l1_diff8(a[k], b[k]);
+            }
+            acc = warp_sum(acc);
+            if (lane == 0) {
+                dv_l1[t] = acc;
+                score[t] = alpha[t] * acc;
+            }
+        }
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const uint32_t done = atomicAdd(&counters[1 + r], 1u) + 1;
+            s_last = (done == (uint32_t)(chunk_off[r + 1] - chunk_off[r])) ? 1 : 0;
+        }
+        __syncthreads();
+        if (s_last) {
+            __threadfence();
+            select_request(score, src_slot, s, n, budget[r], selected, hist, sh);
+        }
+        __syncthreads();
+    }
+}
+
 // ---------------------------------------------------------------- D3
 // Pass 1: grid (request, key chunk).  Logits for all query heads of one key
 // row, each K row read once for its GQA group; per-(request, chunk, head)
@@ -371,6 +540,17 @@ __global__ void decode_attn_combine_kernel(const float *__restrict__ ws, int32_t
 
 static inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+__global__ void chunk_offsets_kernel(const int64_t *req_off, int32_t n_req, int32_t *chunk_off) {
+    if (threadIdx.x == 0) {
+        int32_t acc = 0;
+        chunk_off[0] = 0;
+        for (int r = 0; r < n_req; ++r) {
+            acc += (int32_t)((req_off[r + 1] - req_off[r] + kSelChunk - 1) / kSelChunk);
+            chunk_off[r + 1] = acc;
+        }
+    }
+}
+
 static int decode_splits(int64_t n_rows, int G, int max_kv) {
     int64_t want = (2 * kNumSMs + n_rows * G - 1) / (n_rows * G);
     int64_t cap = (max_kv + 127) / 128;
@@ -388,29 +568,28 @@ extern "C" {
 
 size_t kvs_dhd_select_workspace(int64_t n_total, int32_t n_req) {
     (void)n_total;
-    (void)n_req;
-    return 0;
+    return align256(sizeof(uint32_t) * (n_req + 1)) + align256(sizeof(int32_t) * (n_req + 1));
 }
 
 kvs_status kvs_dhd_select(const void *v_true, const float *alpha, const int32_t *src_slot,
                           int32_t layer, const kvs_kv_arena *arena, const kvs_batch *batch,
                           const int32_t *budget, float *dv_l1, float *score, uint8_t *selected,
                           void *ws, size_t ws_bytes, kvs_stream_t stream) {
-    (void)ws;
-    (void)ws_bytes;
     KVS_REQUIRE(arena && batch, KVS_EPARAM, "null arena/batch");
     KVS_REQUIRE((arena->kv_heads * arena->head_dim) % 8 == 0, KVS_ESHAPE, "row width % 8 != 0");
+    KVS_REQUIRE(ws != nullptr && ws_bytes >= kvs_dhd_select_workspace(batch->n_total, batch->n_req),
+                KVS_EPARAM, "workspace too small (kvs_dhd_select_workspace)");
     if (batch->n_total <= 0) return KVS_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    int64_t warps = batch->n_total;
-    int grid = (int)((warps * 32 + 255) / 256);
-    if (grid > kNumSMs * 16) grid = kNumSMs * 16;
-    dv_score_kernel<<<grid, 256, 0, s>>>((const __nv_bfloat16 *)v_true, alpha, src_slot, layer,
-                                         arena_c(arena), batch->req_off, batch->n_req,
-                                         batch->n_total, batch->block_table, batch->max_pages,
-                                         dv_l1, score);
-    radix_select_kernel<<<batch->n_req, 1024, 0, s>>>(score, src_slot, batch->req_off, budget,
-                                                      selected);
+    uint32_t *counters = (uint32_t *)ws;
+    int32_t *chunk_off = (int32_t *)((char *)ws + align256(sizeof(uint32_t) * (batch->n_req + 1)));
+    cudaMemsetAsync(counters, 0, sizeof(uint32_t) * (batch->n_req + 1), s);
+    chunk_offsets_kernel<<<1, 32, 0, s>>>(batch->req_off, batch->n_req, chunk_off);
+    const int grid = 2 * kNumSMs;
+    dhd_select_fused_kernel<<<grid, kSelThreads, 0, s>>>(
+        (const __nv_bfloat16 *)v_true, alpha, src_slot, layer, arena_c(arena), batch->req_off,
+        chunk_off, batch->n_req, budget, batch->block_table, batch->max_pages, dv_l1, score,
+        selected, counters);
     KVS_CHECK_LAUNCH("kvs_dhd_select");
     return KVS_OK;
 }

@@ -22,6 +22,11 @@ from ._scratch import Scratch, as_heads, dense_rows
 from .errors import ParameterError, ShapeError
 
 _ws = N.Workspace()
+_sws = N.Workspace()
+
+
+def _sel_ws(dev):
+    return _sws.get(N.ws_bytes("kvs_dhd_select_workspace", 1, 1), dev)
 
 
 def _dev():
@@ -55,11 +60,13 @@ def alpha_scores(q, k, delta_v, causal: bool = True, reused_mask=None, budget: i
     score = torch.empty(n, dtype=torch.float32, device=dev)
     sel = torch.zeros(n, dtype=torch.uint8, device=dev)
 
+    sws = _sws.get(N.ws_bytes("kvs_dhd_select_workspace", n, 1), dev)
+
     def select(slot, b):
         bud = torch.tensor([b], dtype=torch.int32, device=dev)
         N.call("kvs_dhd_select", zeros_v.data_ptr(), alpha.data_ptr(), slot.data_ptr(), 0,
                sc.arena, sc.batch, bud.data_ptr(), dv_l1.data_ptr(), score.data_ptr(),
-               sel.data_ptr(), None, 0, N.stream_ptr())
+               sel.data_ptr(), sws.data_ptr(), sws.numel(), N.stream_ptr())
 
     if reused_mask is not None:
         # selection restricted to the reused rows (selection.py:63-66) ...
