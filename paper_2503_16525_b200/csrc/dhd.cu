@@ -155,34 +155,47 @@ __global__ void __launch_bounds__(1024) radix_select_kernel(
 constexpr int kSelChunk = 64;
 constexpr int kSelThreads = 256;
 
-__device__ __forceinline__ uint32_t score_key(float sc) {
-    return ~__float_as_uint(fmaxf(sc, 0.f));
+constexpr int kSelSmemKeys = 16384;   // requests up to 16k tokens select from smem
+
+// Descending-score key; non-reused rows get the largest key.  (Scores are
+// finite and >= 0; a denormal score ties with 0 - below any bf16 signal.)
+__device__ __forceinline__ uint32_t sel_key32(const float *score, const int32_t *src_slot,
+                                              int64_t t) {
+    if (src_slot[t] < 0) return 0xFFFFFFFFu;
+    const uint32_t k = ~__float_as_uint(fmaxf(score[t], 0.f));
+    return k < 0xFFFFFFFEu ? k : 0xFFFFFFFEu;
 }
 
+template <bool kSmem>
 __device__ void select_request(const float *__restrict__ score, const int32_t *__restrict__ src_slot,
                                int64_t s, int64_t n, int32_t B, uint8_t *__restrict__ selected,
-                               uint32_t *hist, uint32_t *sh) {
+                               uint32_t *keys, uint32_t *hist, uint32_t *sh) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    constexpr int NW = kSelThreads / 32;
     if (B <= 0) {
         for (int64_t i = tid; i < n; i += kSelThreads) selected[s + i] = 0;
         return;
     }
-    // sh[0] = prefix, sh[1] = remaining k, sh[2] = count strictly better
+    if (kSmem)
+        for (int64_t i = tid; i < n; i += kSelThreads) keys[i] = sel_key32(score, src_slot, s + i);
+    auto key_at = [&](int64_t i) -> uint32_t {
+        return kSmem ? keys[i] : sel_key32(score, src_slot, s + i);
+    };
     if (tid == 0) { sh[0] = 0; sh[1] = (uint32_t)B; }
     __syncthreads();
     uint32_t mask = 0;
+    __shared__ uint32_t wsum[NW];
     for (int pass = 0; pass < 4; ++pass) {
         const int shift = 24 - 8 * pass;
         hist[tid] = 0;
         __syncthreads();
         const uint32_t prefix = sh[0];
         for (int64_t i = tid; i < n; i += kSelThreads) {
-            if (src_slot[s + i] < 0) continue;
-            const uint32_t key = score_key(score[s + i]);
-            if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 0xff], 1u);
+            const uint32_t key = key_at(i);
+            if (key != 0xFFFFFFFFu && (key & mask) == prefix)
+                atomicAdd(&hist[(key >> shift) & 0xff], 1u);
         }
         __syncthreads();
-        // exclusive scan of the 256 bins (one per thread) -> digit holding the k-th key
         const uint32_t c = hist[tid];
         uint32_t incl = c;
 #pragma unroll
@@ -190,7 +203,6 @@ __device__ void select_request(const float *__restrict__ score, const int32_t *_
             const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
             if (lane >= o) incl += y;
         }
-        __shared__ uint32_t wsum[8];
         if (lane == 31) wsum[wid] = incl;
         __syncthreads();
         uint32_t base = 0;
@@ -205,52 +217,59 @@ __device__ void select_request(const float *__restrict__ score, const int32_t *_
         mask |= 0xffu << shift;
         __syncthreads();
     }
-    const uint32_t thr = sh[0];          // key of the B-th best reused row
-    const uint32_t ties_needed = sh[1];  // how many rows with key == thr to keep
-    // ordered scan over positions: keep key < thr, and the first ties_needed ties
-    __shared__ uint32_t carry;
-    __shared__ uint32_t wcnt[8];
-    if (tid == 0) carry = 0;
+    const uint32_t thr = sh[0], ties_needed = sh[1];
+    // thread-contiguous segments: count ties, one block scan, then emit in order
+    const int64_t seg = (n + kSelThreads - 1) / kSelThreads;
+    const int64_t a = tid * seg, b = min(n, a + seg);
+    uint32_t mine = 0;
+    for (int64_t i = a; i < b; ++i) mine += key_at(i) == thr;
+    uint32_t incl = mine;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+    }
     __syncthreads();
-    for (int64_t b0 = 0; b0 < n; b0 += kSelThreads) {
-        const int64_t i = b0 + tid;
-        bool reused = false, tie = false, better = false;
-        if (i < n && src_slot[s + i] >= 0) {
-            reused = true;
-            const uint32_t key = score_key(score[s + i]);
-            better = key < thr;
-            tie = key == thr;
+    if (lane == 31) wsum[wid] = incl;
+    __syncthreads();
+    uint32_t before = incl - mine;
+    for (int w = 0; w < wid; ++w) before += wsum[w];
+    for (int64_t i = a; i < b; ++i) {
+        const uint32_t key = key_at(i);
+        bool keep = key < thr;
+        if (key == thr) {
+            keep = before < ties_needed;
+            ++before;
         }
-        const uint32_t bal = __ballot_sync(0xffffffffu, tie);
-        if (lane == 0) wcnt[wid] = __popc(bal);
-        __syncthreads();
-        uint32_t before = carry;
-        for (int w = 0; w < wid; ++w) before += wcnt[w];
-        before += __popc(bal & ((1u << lane) - 1));
-        if (i < n) selected[s + i] = (reused && (better || (tie && before < ties_needed))) ? 1 : 0;
-        __syncthreads();
-        if (tid == 0) {
-            uint32_t t = 0;
-            for (int w = 0; w < 8; ++w) t += wcnt[w];
-            carry += t;
-        }
-        __syncthreads();
+        selected[s + i] = keep ? 1 : 0;
     }
 }
 
 __global__ void __launch_bounds__(kSelThreads) dhd_select_fused_kernel(
     const __nv_bfloat16 *__restrict__ v_true, const float *__restrict__ alpha,
     const int32_t *__restrict__ src_slot, int32_t layer, ArenaC A,
-    const int64_t *__restrict__ req_off, const int32_t *__restrict__ chunk_off, int32_t n_req,
+    const int64_t *__restrict__ req_off, int32_t *__restrict__ chunk_off, int32_t n_req,
     const int32_t *__restrict__ budget, const int32_t *__restrict__ block_table,
     int32_t max_pages, float *__restrict__ dv_l1, float *__restrict__ score,
     uint8_t *__restrict__ selected, uint32_t *__restrict__ counters) {
     // counters[0] = work cursor, counters[1 + r] = finished chunks of request r
+    extern __shared__ uint32_t s_keys[];
     __shared__ uint32_t hist[256];
     __shared__ uint32_t sh[4];
     __shared__ int s_item, s_last;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int total = chunk_off[n_req];
+    // chunk prefix over requests: every CTA computes its own copy (n_req is small)
+    int32_t *co = chunk_off + (int64_t)blockIdx.x * (n_req + 1);
+    if (threadIdx.x == 0) {
+        int32_t acc = 0;
+        for (int r = 0; r < n_req; ++r) {
+            co[r] = acc;
+            acc += (int32_t)((req_off[r + 1] - req_off[r] + kSelChunk - 1) / kSelChunk);
+        }
+        co[n_req] = acc;
+    }
+    __syncthreads();
+    const int total = co[n_req];
     const int nvec = A.G * A.D / 8;
     while (true) {
         if (threadIdx.x == 0) s_item = (int)atomicAdd(&counters[0], 1u);
@@ -260,10 +279,10 @@ __global__ void __launch_bounds__(kSelThreads) dhd_select_fused_kernel(
         int r = 0, hi = n_req;            // chunk_off[r] <= item < chunk_off[r+1]
         while (hi - r > 1) {
             const int mid = (r + hi) >> 1;
-            if (chunk_off[mid] <= item) r = mid; else hi = mid;
+            if (co[mid] <= item) r = mid; else hi = mid;
         }
         const int64_t s = req_off[r], n = req_off[r + 1] - s;
-        const int64_t i0 = (int64_t)(item - chunk_off[r]) * kSelChunk;
+        const int64_t i0 = (int64_t)(item - co[r]) * kSelChunk;
         for (int j = wid; j < kSelChunk; j += kSelThreads / 32) {
             const int64_t i = i0 + j;
             if (i >= n) break;
@@ -300,12 +319,15 @@ __global__ void __launch_bounds__(kSelThreads) dhd_select_fused_kernel(
         __syncthreads();
         if (threadIdx.x == 0) {
             const uint32_t done = atomicAdd(&counters[1 + r], 1u) + 1;
-            s_last = (done == (uint32_t)(chunk_off[r + 1] - chunk_off[r])) ? 1 : 0;
+            s_last = (done == (uint32_t)(co[r + 1] - co[r])) ? 1 : 0;
         }
         __syncthreads();
         if (s_last) {
             __threadfence();
-            select_request(score, src_slot, s, n, budget[r], selected, hist, sh);
+            if (n <= kSelSmemKeys)
+                select_request<true>(score, src_slot, s, n, budget[r], selected, s_keys, hist, sh);
+            else
+                select_request<false>(score, src_slot, s, n, budget[r], selected, s_keys, hist, sh);
         }
         __syncthreads();
     }
@@ -568,7 +590,8 @@ extern "C" {
 
 size_t kvs_dhd_select_workspace(int64_t n_total, int32_t n_req) {
     (void)n_total;
-    return align256(sizeof(uint32_t) * (n_req + 1)) + align256(sizeof(int32_t) * (n_req + 1));
+    return align256(sizeof(uint32_t) * (n_req + 2)) +
+           align256(sizeof(int32_t) * (n_req + 1) * 2 * kNumSMs);
 }
 
 kvs_status kvs_dhd_select(const void *v_true, const float *alpha, const int32_t *src_slot,
@@ -582,11 +605,13 @@ kvs_status kvs_dhd_select(const void *v_true, const float *alpha, const int32_t 
     if (batch->n_total <= 0) return KVS_OK;
     cudaStream_t s = (cudaStream_t)stream;
     uint32_t *counters = (uint32_t *)ws;
-    int32_t *chunk_off = (int32_t *)((char *)ws + align256(sizeof(uint32_t) * (batch->n_req + 1)));
-    cudaMemsetAsync(counters, 0, sizeof(uint32_t) * (batch->n_req + 1), s);
-    chunk_offsets_kernel<<<1, 32, 0, s>>>(batch->req_off, batch->n_req, chunk_off);
+    int32_t *chunk_off = (int32_t *)((char *)ws + align256(sizeof(uint32_t) * (batch->n_req + 2)));
+    cudaMemsetAsync(counters, 0, sizeof(uint32_t) * (batch->n_req + 2), s);
     const int grid = 2 * kNumSMs;
-    dhd_select_fused_kernel<<<grid, kSelThreads, 0, s>>>(
+    const size_t smem = sizeof(uint32_t) * kSelSmemKeys;
+    cudaFuncSetAttribute(dhd_select_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    dhd_select_fused_kernel<<<grid, kSelThreads, smem, s>>>(
         (const __nv_bfloat16 *)v_true, alpha, src_slot, layer, arena_c(arena), batch->req_off,
         chunk_off, batch->n_req, budget, batch->block_table, batch->max_pages, dv_l1, score,
         selected, counters);
