@@ -145,8 +145,11 @@ class Workspace:
     def __init__(self):
         self.buf = None
 
-    def get(self, nbytes: int, device) -> torch.Tensor:
+    def get(self, nbytes: int, device, zero: bool = False) -> torch.Tensor:
+        """zero=True: a newly allocated buffer starts zeroed (kernels that keep
+        self-resetting counters in their workspace rely on it)."""
         nbytes = max(int(nbytes), 256)
         if self.buf is None or self.buf.numel() < nbytes or self.buf.device != torch.device(device):
-            self.buf = torch.empty(nbytes, dtype=torch.uint8, device=device)
+            self.buf = (torch.zeros if zero else torch.empty)(nbytes, dtype=torch.uint8,
+                                                             device=device)
         return self.buf

@@ -283,36 +283,47 @@ __global__ void __launch_bounds__(kSelThreads) dhd_select_fused_kernel(
         }
         const int64_t s = req_off[r], n = req_off[r + 1] - s;
         const int64_t i0 = (int64_t)(item - co[r]) * kSelChunk;
-        for (int j = wid; j < kSelChunk; j += kSelThreads / 32) {
-            const int64_t i = i0 + j;
-            if (i >= n) break;
-            const int64_t t = s + i;
-            if (src_slot[t] < 0) {
-                if (lane == 0) { dv_l1[t] = 0.f; score[t] = 0.f; }
-                continue;
+        // each warp streams 8 rows, two at a time (16 x 16-byte loads in flight per lane)
+        for (int j = wid * 8; j < wid * 8 + 8; j += 2) {
+            int64_t t2[2];
+            bool live[2];
+            const uint4 *vc[2], *vt[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int64_t i = i0 + j + u;
+                t2[u] = s + i;
+                live[u] = i < n && src_slot[s + i] >= 0;
+                if (i < n && !live[u] && lane == 0) { dv_l1[s + i] = 0.f; score[s + i] = 0.f; }
+                const int64_t page = live[u] ? block_table[(int64_t)r * max_pages + i / A.P] : 0;
+                vc[u] = reinterpret_cast<const uint4 *>(A.row(page, layer, 1, (int)(i % A.P)));
+                vt[u] = reinterpret_cast<const uint4 *>(v_true + t2[u] * (int64_t)(A.G * A.D));
             }
-            const int64_t page = block_table[(int64_t)r * max_pages + i / A.P];
-            const uint4 *vc = reinterpret_cast<const uint4 *>(A.row(page, layer, 1, (int)(i % A.P)));
-            const uint4 *vt = reinterpret_cast<const uint4 *>(v_true + t * (int64_t)(A.G * A.D));
-            float acc = 0.f;
+            float acc[2] = {0.f, 0.f};
             for (int v0 = 0; v0 < nvec; v0 += 128) {
-                uint4 a[4], b[4];
+                uint4 a[2][4], b[2][4];
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int v = v0 + k * 32 + lane;
-                    if (v < nvec) {
-                        a[k] = __ldcs(vc + v);
-                        b[k] = __ldcs(vt + v);
+                for (int u = 0; u < 2; ++u)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int v = v0 + k * 32 + lane;
+                        if (live[u] && v < nvec) {
+                            a[u][k] = __ldcs(vc[u] + v);
+                            b[u][k] = __ldcs(vt[u] + v);
+                        }
                     }
-                }
 #pragma unroll
-                for (int k = 0; k < 4; ++k)
-                    if (v0 + k * 32 + lane < nvec) acc += l1_diff8(a[k], b[k]);
+                for (int u = 0; u < 2; ++u)
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (live[u] && v0 + k * 32 + lane < nvec) acc[u] += l1_diff8(a[u][k], b[u][k]);
             }
-            acc = warp_sum(acc);
-            if (lane == 0) {
-                dv_l1[t] = acc;
-                score[t] = alpha[t] * acc;
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const float x = warp_sum(acc[u]);
+                if (live[u] && lane == 0) {
+                    dv_l1[t2[u]] = x;
+                    score[t2[u]] = alpha[t2[u]] * x;
+                }
             }
         }
         __threadfence();
@@ -330,6 +341,14 @@ __global__ void __launch_bounds__(kSelThreads) dhd_select_fused_kernel(
                 select_request<false>(score, src_slot, s, n, budget[r], selected, s_keys, hist, sh);
         }
         __syncthreads();
+    }
+    // the last CTA out leaves the counters zeroed for the next launch
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&counters[1 + n_req], 1u) + 1 == gridDim.x) {
+            for (int r = 0; r < n_req + 2; ++r) counters[r] = 0;
+            __threadfence();
+        }
     }
 }
 
@@ -594,6 +613,8 @@ size_t kvs_dhd_select_workspace(int64_t n_total, int32_t n_req) {
            align256(sizeof(int32_t) * (n_req + 1) * 2 * kNumSMs);
 }
 
+/* Workspace contract: the first kvs_dhd_select_workspace() bytes must be zero
+ * before the first call on a buffer; the kernel leaves them zero again. */
 kvs_status kvs_dhd_select(const void *v_true, const float *alpha, const int32_t *src_slot,
                           int32_t layer, const kvs_kv_arena *arena, const kvs_batch *batch,
                           const int32_t *budget, float *dv_l1, float *score, uint8_t *selected,
@@ -606,7 +627,7 @@ kvs_status kvs_dhd_select(const void *v_true, const float *alpha, const int32_t 
     cudaStream_t s = (cudaStream_t)stream;
     uint32_t *counters = (uint32_t *)ws;
     int32_t *chunk_off = (int32_t *)((char *)ws + align256(sizeof(uint32_t) * (batch->n_req + 2)));
-    cudaMemsetAsync(counters, 0, sizeof(uint32_t) * (batch->n_req + 2), s);
+    // counters start zeroed (Workspace.get(zero=True)) and are re-zeroed by the kernel
     const int grid = 2 * kNumSMs;
     const size_t smem = sizeof(uint32_t) * kSelSmemKeys;
     cudaFuncSetAttribute(dhd_select_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

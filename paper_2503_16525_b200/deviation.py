@@ -26,7 +26,7 @@ _sws = N.Workspace()
 
 
 def _sel_ws(dev):
-    return _sws.get(N.ws_bytes("kvs_dhd_select_workspace", 1, 1), dev)
+    return _sws.get(N.ws_bytes("kvs_dhd_select_workspace", 1, 1), dev, zero=True)
 
 
 def _dev():
@@ -60,7 +60,7 @@ def alpha_scores(q, k, delta_v, causal: bool = True, reused_mask=None, budget: i
     score = torch.empty(n, dtype=torch.float32, device=dev)
     sel = torch.zeros(n, dtype=torch.uint8, device=dev)
 
-    sws = _sws.get(N.ws_bytes("kvs_dhd_select_workspace", n, 1), dev)
+    sws = _sws.get(N.ws_bytes("kvs_dhd_select_workspace", n, 1), dev, zero=True)
 
     def select(slot, b):
         bud = torch.tensor([b], dtype=torch.int32, device=dev)

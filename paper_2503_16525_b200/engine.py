@@ -345,7 +345,7 @@ class Engine:
         score = torch.empty(n, dtype=torch.float32, device=dev)
         sel = torch.empty(n, dtype=torch.uint8, device=dev)
         ws = self._ws["select"].get(N.ws_bytes("kvs_dhd_select_workspace", n, len(st.lengths)),
-                                    dev)
+                                    dev, zero=True)
         self._timed("dhd_select", N.call, "kvs_dhd_select", v_true.data_ptr(), alpha.data_ptr(),
                     st.src_slot.data_ptr(), self.probe_layer, self.arena.c, st.batch_c,
                     bud.data_ptr(), dv.data_ptr(), score.data_ptr(), sel.data_ptr(),

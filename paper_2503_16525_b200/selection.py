@@ -82,7 +82,7 @@ _sws = N.Workspace()
 
 
 def _sel_ws(dev):
-    return _sws.get(N.ws_bytes("kvs_dhd_select_workspace", 1, 1), dev)
+    return _sws.get(N.ws_bytes("kvs_dhd_select_workspace", 1, 1), dev, zero=True)
 
 
 def select_decode_step(q_t, k, delta_v, eligible, n_extra: int) -> SelectionResult:
