@@ -176,8 +176,28 @@ __device__ void select_request(const float *__restrict__ score, const int32_t *_
         for (int64_t i = tid; i < n; i += kSelThreads) selected[s + i] = 0;
         return;
     }
-    if (kSmem)
-        for (int64_t i = tid; i < n; i += kSelThreads) keys[i] = sel_key32(score, src_slot, s + i);
+    if (kSmem) {
+        // 8 independent loads of each array in flight per thread
+        for (int64_t b0 = 0; b0 < n; b0 += 8 * kSelThreads) {
+            int32_t sl[8];
+            float sc[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int64_t i = b0 + u * kSelThreads + tid;
+                sl[u] = i < n ? __ldcg(src_slot + s + i) : -1;
+                sc[u] = i < n ? __ldcg(score + s + i) : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int64_t i = b0 + u * kSelThreads + tid;
+                if (i < n) {
+                    const uint32_t k = ~__float_as_uint(fmaxf(sc[u], 0.f));
+                    keys[i] = sl[u] < 0 ? 0xFFFFFFFFu : (k < 0xFFFFFFFEu ? k : 0xFFFFFFFEu);
+                }
+            }
+        }
+        __syncthreads();
+    }
     auto key_at = [&](int64_t i) -> uint32_t {
         return kSmem ? keys[i] : sel_key32(score, src_slot, s + i);
     };
