@@ -808,6 +808,234 @@ __global__ void __launch_bounds__(kThreads2, 1)
     }
 }
 
+// ------------------------------------------------------------------ A1, head pairs, 64-key blocks
+// fwd3 with BN = 64 and TWO S/P buffers per head: TMEM per head t is
+// S_t[0] | S_t[1] (64 fp32 columns each; P bf16 overwrites 32 of them) | O_t
+// (128).  The MMA warp issues QK_a(kb+1), QK_b(kb+1) before PV_a(kb), PV_b(kb),
+// so a head's next scores are computed while its softmax still runs and the
+// softmax warpgroups work back to back.  In-order tcgen05 execution protects
+// P(kb-1) (same buffer as S(kb+1)) until PV(kb-1) has read it.  K/V tiles are
+// one 64-row page each; 10-slot ring.
+constexpr int BN4 = 64;
+constexpr int TILE4 = BN4 * 256;        // [64 rows x 128 bf16] = 16 KB (two 8 KB halves)
+constexpr int HALF4 = BN4 * 128;
+constexpr int RING4 = 10;
+
+struct Smem4 {
+    uint64_t q_full;
+    uint64_t ring_full[RING4], ring_empty[RING4];
+    uint64_t s_full[2][2], p_full[2][2], pv_done[2];
+    uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(kThreads2, 1)
+    fwd4_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
+                Params p) {
+    extern __shared__ uint8_t dsmem[];
+    __shared__ Smem4 sh;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tile = blockIdx.x, h0 = 2 * blockIdx.y;
+    const int g = h0 / (p.num_heads / p.kv_heads);
+    const int req = p.tile_req[tile], row0 = p.tile_row0[tile], nrows = p.tile_rows[tile];
+    const int kmax = p.causal ? p.row_pos[row0 + nrows - 1] + 1 : p.kv_len[req];
+    const int n_kb = (kmax + BN4 - 1) / BN4;          // == pages touched (page_size 64)
+
+    const uint32_t base = align1024(smem_u32(dsmem));
+    const uint32_t sQ = base;                          // 2 x 32 KB
+    const uint32_t sR = sQ + 2 * TILE_BYTES;           // RING4 x 16 KB
+    uint8_t *gbase = dsmem + (base - smem_u32(dsmem));
+
+    if (threadIdx.x == 0) {
+        mbar_init(&sh.q_full, 1);
+        for (int i = 0; i < RING4; ++i) {
+            mbar_init(&sh.ring_full[i], 1);
+            mbar_init(&sh.ring_empty[i], 1);
+        }
+        for (int t = 0; t < 2; ++t) {
+            for (int b = 0; b < 2; ++b) {
+                mbar_init(&sh.s_full[t][b], 1);
+                mbar_init(&sh.p_full[t][b], 128);
+            }
+            mbar_init(&sh.pv_done[t], 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 9) tmem_alloc(&sh.tmem_base, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sh.tmem_base;
+    // TMEM columns: head t at 256*t: S buffers at +0 / +64, O at +128
+    if (warp >= 8) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+        if (warp == 8 && lane == 0) {
+            tma_prefetch(&map_q);
+            tma_prefetch(&map_kv);
+            mbar_expect_tx(&sh.q_full, 2 * TILE_BYTES);
+            for (int t = 0; t < 2; ++t)
+                for (int hf = 0; hf < 2; ++hf)
+                    tma_load_3d(gbase + (sQ - base) + t * TILE_BYTES + hf * HALF_BYTES, &map_q,
+                                &sh.q_full, hf * 64, h0 + t, row0);
+            const int32_t *bt = p.block_table + (int64_t)req * p.max_pages;
+            for (int it = 0; it < 2 * n_kb; ++it) {
+                const int kb = it >> 1, kv = it & 1, slot = it % RING4;
+                if (it >= RING4) mbar_wait(&sh.ring_empty[slot], (uint32_t)((it / RING4) - 1) & 1u);
+                mbar_expect_tx(&sh.ring_full[slot], TILE4);
+                const int pg = bt[kb];
+                for (int hf = 0; hf < 2; ++hf)
+                    tma_load_4d(gbase + (sR - base) + slot * TILE4 + hf * HALF4, &map_kv,
+                                &sh.ring_full[slot], hf * 64, g, 0,
+                                (pg * p.num_layers + p.layer) * 2 + kv);
+            }
+        } else if (warp == 9 && lane == 0) {
+            const uint32_t idesc_qk = umma_idesc_bf16(BM, BN4, false);
+            const uint32_t idesc_pv = umma_idesc_bf16(BM, HD, true);
+            mbar_wait(&sh.q_full, 0);
+            auto issue_qk = [&](int kb) {
+                const int it = 2 * kb, slot = it % RING4;
+                mbar_wait(&sh.ring_full[slot], (uint32_t)(it / RING4) & 1u);
+                tc_fence_after();
+                for (int t = 0; t < 2; ++t) {
+#pragma unroll
+                    for (int k = 0; k < HD / 16; ++k) {
+                        const uint64_t da = umma_desc_sw128(
+                            sQ + t * TILE_BYTES + (k >> 2) * HALF_BYTES + (k & 3) * 32, 16, 1024);
+                        const uint64_t db = umma_desc_sw128(
+                            sR + slot * TILE4 + (k >> 2) * HALF4 + (k & 3) * 32, 16, 1024);
+                        umma_bf16(tmem + 256 * t + 64 * (kb & 1), da, db, idesc_qk, k > 0 ? 1u : 0u);
+                    }
+                    umma_commit(&sh.s_full[t][kb & 1]);
+                }
+                umma_commit(&sh.ring_empty[slot]);
+            };
+            if (n_kb >= 1) issue_qk(0);
+            for (int kb = 0; kb < n_kb; ++kb) {
+                if (kb + 1 < n_kb) issue_qk(kb + 1);
+                const int it = 2 * kb + 1, slot = it % RING4;
+                mbar_wait(&sh.ring_full[slot], (uint32_t)(it / RING4) & 1u);
+                for (int t = 0; t < 2; ++t) {
+                    mbar_wait(&sh.p_full[t][kb & 1], (uint32_t)(kb >> 1) & 1u);
+                    tc_fence_after();
+#pragma unroll
+                    for (int k = 0; k < BN4 / 16; ++k) {
+                        const uint64_t db =
+                            umma_desc_sw128(sR + slot * TILE4 + k * 2048, HALF4, 1024);
+                        umma_bf16_ts(tmem + 256 * t + 128, tmem + 256 * t + 64 * (kb & 1) + 8 * k,
+                                     db, idesc_pv, (kb > 0 || k > 0) ? 1u : 0u);
+                    }
+                    umma_commit(&sh.pv_done[t]);
+                }
+                umma_commit(&sh.ring_empty[slot]);
+            }
+        }
+        __syncwarp();
+    } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+        const int t = warp >> 2;
+        const int i = threadIdx.x & 127;
+        const bool valid = i < nrows;
+        const int kend = !valid ? 0 : (p.causal ? p.row_pos[row0 + i] + 1 : kmax);
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        const uint32_t tH = tmem + 256 * t + lane_off, tO = tH + 128;
+        float m = -INFINITY, l = 0.f;
+        float s[BN4];
+        for (int kb = 0; kb < n_kb; ++kb) {
+            const int b = kb & 1;
+            mbar_wait(&sh.s_full[t][b], (uint32_t)(kb >> 1) & 1u);
+            tc_fence_after();
+            tmem_ld32(tH + 64 * b, s);
+            tmem_ld32(tH + 64 * b + 32, s + 32);
+            tmem_ld_wait();
+            const int kbase = kb * BN4;
+            float mx[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
+            if (kbase + BN4 <= kend) {
+#pragma unroll
+                for (int c = 0; c < BN4; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < BN4; ++c) {
+                    s[c] = (kbase + c < kend) ? s[c] : -INFINITY;
+                    mx[c & 7] = fmaxf(mx[c & 7], s[c]);
+                }
+            }
+            const float mloc = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                     fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) *
+                               p.scale_log2;
+            if (mloc > m + kRescaleThreshold || (m == -INFINITY && mloc > -INFINITY)) {
+                const float factor = (m == -INFINITY) ? 0.f : fast_exp2(m - mloc);
+                if (kb >= 1 && m != -INFINITY) {
+                    // PV(kb-1) may still be queued: O is touched only after it retired
+                    mbar_wait(&sh.pv_done[t], (uint32_t)(kb - 1) & 1u);
+                    tc_fence_after();
+                    float o[32];
+#pragma unroll
+                    for (int c = 0; c < HD / 32; ++c) {
+                        tmem_ld32(tO + c * 32, o);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) o[e] *= factor;
+                        tmem_st32(tO + c * 32, o);
+                    }
+                }
+                l *= factor;
+                m = mloc;
+            }
+            const float mu = (m == -INFINITY) ? 0.f : m;
+            float ls[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) ls[j] = 0.f;
+            uint32_t pk[32];
+#pragma unroll
+            for (int q = 0; q < 32; ++q) {
+                const float e0 = fast_exp2(fmaf(s[2 * q], p.scale_log2, -mu));
+                const float e1 = fast_exp2(fmaf(s[2 * q + 1], p.scale_log2, -mu));
+                ls[(2 * q) & 7] += e0;
+                ls[(2 * q + 1) & 7] += e1;
+                pk[q] = pack_bf16x2(e0, e1);
+            }
+            tmem_st32(tH + 64 * b, reinterpret_cast<const float *>(pk));
+            l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&sh.p_full[t][b]);
+        }
+        const int64_t grow = (int64_t)row0 + i;
+        if (n_kb >= 1) mbar_wait(&sh.pv_done[t], (uint32_t)(n_kb - 1) & 1u);
+        tc_fence_after();
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        float o[32];
+#pragma unroll
+        for (int c = 0; c < HD / 32; ++c) {
+            tmem_ld32(tO + c * 32, o);
+            tmem_ld_wait();
+            if (valid) {
+                uint4 *dst = reinterpret_cast<uint4 *>(p.out + (grow * p.num_heads + h0 + t) * HD +
+                                                       c * 32);
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    uint4 w;
+                    w.x = pack_bf16x2(o[8 * v + 0] * inv, o[8 * v + 1] * inv);
+                    w.y = pack_bf16x2(o[8 * v + 2] * inv, o[8 * v + 3] * inv);
+                    w.z = pack_bf16x2(o[8 * v + 4] * inv, o[8 * v + 5] * inv);
+                    w.w = pack_bf16x2(o[8 * v + 6] * inv, o[8 * v + 7] * inv);
+                    dst[v] = w;
+                }
+            }
+        }
+        if (valid && p.lse != nullptr)
+            p.lse[grow * p.num_heads + h0 + t] =
+                (l > 0.f) ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 9) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
 // ------------------------------------------------------------------ D1 pass 2
 // CTA = (key tile kt of request r, kv head g).  Loops over the group's query
 // heads and the query tiles that can see the keys; S^T lands with one key per
@@ -1047,7 +1275,12 @@ kvs_status kvs_attention_fwd(const void *q, const int32_t *row_pos, int64_t n_ro
     cudaStream_t s = (cudaStream_t)stream;
     const int group = num_heads / arena->kv_heads;
     const char *variant = getenv("KVS_ATTN");
-    if (out != nullptr && group % 2 == 0 && (variant == nullptr || variant[0] == '3')) {
+    if (out != nullptr && group % 2 == 0 && (variant == nullptr || variant[0] == '4')) {
+        const size_t smem = 1024 + 2 * attn::TILE_BYTES + attn::RING4 * attn::TILE4;
+        cudaFuncSetAttribute(attn::fwd4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        attn::fwd4_kernel<<<dim3(n_tiles, num_heads / 2), attn::kThreads2, smem, s>>>(mq, mkv, p);
+    } else if (out != nullptr && group % 2 == 0 && variant[0] == '3') {
         const size_t smem = 1024 + attn::TILE_BYTES * (2 + attn::RING3);
         cudaFuncSetAttribute(attn::fwd3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
