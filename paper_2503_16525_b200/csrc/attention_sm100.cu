@@ -1275,12 +1275,12 @@ kvs_status kvs_attention_fwd(const void *q, const int32_t *row_pos, int64_t n_ro
     cudaStream_t s = (cudaStream_t)stream;
     const int group = num_heads / arena->kv_heads;
     const char *variant = getenv("KVS_ATTN");
-    if (out != nullptr && group % 2 == 0 && (variant == nullptr || variant[0] == '4')) {
+    if (out != nullptr && group % 2 == 0 && variant != nullptr && variant[0] == '4') {
         const size_t smem = 1024 + 2 * attn::TILE_BYTES + attn::RING4 * attn::TILE4;
         cudaFuncSetAttribute(attn::fwd4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         attn::fwd4_kernel<<<dim3(n_tiles, num_heads / 2), attn::kThreads2, smem, s>>>(mq, mkv, p);
-    } else if (out != nullptr && group % 2 == 0 && variant[0] == '3') {
+    } else if (out != nullptr && group % 2 == 0 && (variant == nullptr || variant[0] == '3')) {
         const size_t smem = 1024 + attn::TILE_BYTES * (2 + attn::RING3);
         cudaFuncSetAttribute(attn::fwd3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);

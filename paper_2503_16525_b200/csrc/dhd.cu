@@ -205,16 +205,24 @@ __device__ void select_request(const float *__restrict__ score, const int32_t *_
     __syncthreads();
     uint32_t mask = 0;
     __shared__ uint32_t wsum[NW];
+    __shared__ uint32_t whist[NW][256];      // per-warp histograms (no cross-warp contention)
     for (int pass = 0; pass < 4; ++pass) {
         const int shift = 24 - 8 * pass;
-        hist[tid] = 0;
+        for (int w = 0; w < NW; ++w) whist[w][tid] = 0;
         __syncthreads();
         const uint32_t prefix = sh[0];
-        for (int64_t i = tid; i < n; i += kSelThreads) {
-            const uint32_t key = key_at(i);
-            if (key != 0xFFFFFFFFu && (key & mask) == prefix)
-                atomicAdd(&hist[(key >> shift) & 0xff], 1u);
+        const int64_t nr = (n + 31) & ~(int64_t)31;    // whole warps stay converged
+        for (int64_t i = tid; i < nr; i += kSelThreads) {
+            const uint32_t key = i < n ? key_at(i) : 0xFFFFFFFFu;
+            const bool in = key != 0xFFFFFFFFu && (key & mask) == prefix;
+            const uint32_t bin = in ? (key >> shift) & 0xff : 256u + lane;
+            const uint32_t peers = __match_any_sync(0xffffffffu, bin);
+            if (in && lane == __ffs(peers) - 1) whist[wid][bin] += __popc(peers);
         }
+        __syncthreads();
+        uint32_t tot = 0;
+        for (int w = 0; w < NW; ++w) tot += whist[w][tid];
+        hist[tid] = tot;
         __syncthreads();
         const uint32_t c = hist[tid];
         uint32_t incl = c;
