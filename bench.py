@@ -234,6 +234,7 @@ def run_gpu(args, rank, world, device):
     barrier()
     torch.cuda.synchronize()
     launches0 = N.launch_count["kernels"]
+    mallocs0 = torch.cuda.memory_stats(device).get("num_device_alloc", 0)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     step_ms, counts = [], []
     if args.profile:
@@ -246,7 +247,6 @@ def run_gpu(args, rank, world, device):
         st = step(i)
         s1.record()
         step_ms.append((s0, s1))
-        counts.append(algorithmic_counts(eng, st, cfg))
         eng.release(st)                     # pages are reused in stream order
     end.record()
     torch.cuda.synchronize()
@@ -255,8 +255,7 @@ def run_gpu(args, rank, world, device):
     barrier()
     clk = clocks.stop()
     launches = N.launch_count["kernels"] - launches0
-    counts = [{k: float(v) for k, v in c.items()} for c in counts]
-    n_hit = [c["hit"] for c in counts]
+    mallocs = torch.cuda.memory_stats(device).get("num_device_alloc", 0) - mallocs0
     elapsed = start.elapsed_time(end)
     per_step = [a.elapsed_time(b) for a, b in step_ms]
     # ---------------- same steps again with CUDA events around the hot kernels
@@ -266,8 +265,11 @@ def run_gpu(args, rank, world, device):
     for i in range(args.warmup, n_steps):
         st = step(i, timers)
         eng.timers = None
+        counts.append(algorithmic_counts(eng, st, cfg))     # same batches, outside the timing
         eng.release(st)
     torch.cuda.synchronize()
+    counts = [{k: float(v) for k, v in c.items()} for c in counts]
+    n_hit = [c["hit"] for c in counts]
     t = torch.tensor([elapsed], dtype=torch.float64, device=device)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -276,6 +278,9 @@ def run_gpu(args, rank, world, device):
     kern = {}
     for name, evs in timers.items():
         kern[name] = sum(a.elapsed_time(b) for a, b in evs) / args.steps     # ms per step
+    if os.environ.get("KVS_BENCH_DEBUG"):
+        print(json.dumps({"rank": rank, "step_ms": per_step, "elapsed_ms": elapsed,
+                          "cuda_mallocs_in_timed_loop": mallocs}), file=sys.stderr)
     res = {"elapsed_ms": elapsed, "tokens": tokens, "step_ms": per_step, "kernels_ms": kern,
            "counts": {k: float(np.mean([c[k] for c in counts])) for k in counts[0]},
            "hit": float(np.mean(n_hit)), "launches": launches // max(args.steps, 1),

@@ -166,9 +166,12 @@ kvs_status kvs_qkv_rope_scatter(const void *qkv, int64_t n_rows, int32_t num_hea
                                 const kvs_rope *rope, void *q_out, void *k_out, void *v_out,
                                 kvs_stream_t stream);
 
-/* Embedding rows: out[r] = table[ids[rows ? rows[r] : r]] (width bf16 each). */
+/* Embedding rows: out[r] = table[ids[rows ? rows[r] : r]] (width bf16 each);
+ * out_f32 (nullable) receives the same rows widened to fp32 (the residual
+ * stream, model.py:189 embed). */
 kvs_status kvs_embed_rows(const void *table, int64_t width, const int64_t *ids,
-                          const int32_t *rows, int64_t n_rows, void *out, kvs_stream_t stream);
+                          const int32_t *rows, int64_t n_rows, void *out, float *out_f32,
+                          kvs_stream_t stream);
 
 /* Recompute row set S = non-reused U selected U {n-1} per request (the rows a
  * partial prefill must compute).  Call once with

@@ -30,7 +30,7 @@ __device__ long long g_trace[8192];
 __device__ int g_trace_n;
 #define TRACE(tag, kb)                                                              \
     do {                                                                            \
-        if (blockIdx.x == gridDim.x - 1 && blockIdx.y == 0) {                      \
+        if (blockIdx.y == 0 && blockIdx.x == 0) {                                   \
             int _i = atomicAdd(&g_trace_n, 1);                                      \
             if (_i < 4096) {                                                        \
                 g_trace[2 * _i] = clock64();                                        \
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     extern __shared__ uint8_t dsmem[];
     __shared__ Smem sh;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tile = blockIdx.x, h = blockIdx.y;
+    const int tile = blockIdx.y, h = blockIdx.x;   // heads fastest: tiles in LPT order
     const int g = h / (p.num_heads / p.kv_heads);
     const int req = p.tile_req[tile], row0 = p.tile_row0[tile], nrows = p.tile_rows[tile];
     const int kmax = p.causal ? p.row_pos[row0 + nrows - 1] + 1 : p.kv_len[req];
@@ -233,26 +233,33 @@ __global__ void __launch_bounds__(kThreads, 1)
             const float mloc = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                                      fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) *
                                p.scale_log2;
-            if (mloc > m + kRescaleThreshold || (m == -INFINITY && mloc > -INFINITY)) {
-                const float factor = (m == -INFINITY) ? 0.f : fast_exp2(m - mloc);
-                if (kPV && kb >= 1 && m != -INFINITY) {
-                    // O must be quiescent: wait for the previous P.V
-                    mbar_wait(&sh.pv_done[(kb - 1) & 1], (uint32_t)((kb - 1) >> 1) & 1u);
-                    tc_fence_after();
-                    float o[32];
-#pragma unroll
-                    for (int c = 0; c < HD / 32; ++c) {
-                        tmem_ld32(tO + lane_off + c * 32, o);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) o[e] *= factor;
-                        tmem_st32(tO + lane_off + c * 32, o);
-                    }
-                    tmem_st_wait();
-                    tc_fence_before();
-                }
+            // lazy rescale: the decision is per row, but tcgen05.ld/st are
+            // warp-collective, so the O pass runs for the whole warp whenever
+            // any of its rows needs it (factor 1 on the others)
+            const bool grow = mloc > m + kRescaleThreshold || (m == -INFINITY && mloc > -INFINITY);
+            const bool touch_o = grow && kb >= 1 && m != -INFINITY;
+            float factor = 1.f;
+            if (grow) {
+                factor = (m == -INFINITY) ? 0.f : fast_exp2(m - mloc);
                 l *= factor;
                 m = mloc;
+            }
+            if (kPV && __any_sync(0xffffffffu, touch_o)) {
+                // O must be quiescent: wait for the previous P.V
+                mbar_wait(&sh.pv_done[(kb - 1) & 1], (uint32_t)((kb - 1) >> 1) & 1u);
+                tc_fence_after();
+                const float f = touch_o ? factor : 1.f;
+                float o[32];
+#pragma unroll
+                for (int c = 0; c < HD / 32; ++c) {
+                    tmem_ld32(tO + lane_off + c * 32, o);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) o[e] *= f;
+                    tmem_st32(tO + lane_off + c * 32, o);
+                }
+                tmem_st_wait();
+                tc_fence_before();
             }
             const float mu = (m == -INFINITY) ? 0.f : m;
             float ls[8];
@@ -343,7 +350,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     extern __shared__ uint8_t dsmem[];
     __shared__ Smem2 sh;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tile = blockIdx.x, h0 = 2 * blockIdx.y;
+    const int tile = blockIdx.y, h0 = 2 * blockIdx.x;
     const int g = h0 / (p.num_heads / p.kv_heads);
     const int req = p.tile_req[tile], row0 = p.tile_row0[tile], nrows = p.tile_rows[tile];
     const int kmax = p.causal ? p.row_pos[row0 + nrows - 1] + 1 : p.kv_len[req];
@@ -487,24 +494,28 @@ __global__ void __launch_bounds__(kThreads2, 1)
                                p.scale_log2;
             // P buffer (and O, if rescaling) are free once the previous P.V retired
             if (kb >= 1) mbar_wait(&sh.pv_done[t], (uint32_t)(kb - 1) & 1u);
-            if (mloc > m + kRescaleThreshold || (m == -INFINITY && mloc > -INFINITY)) {
-                const float factor = (m == -INFINITY) ? 0.f : fast_exp2(m - mloc);
-                if (kb >= 1 && m != -INFINITY) {
-                    tc_fence_after();
-                    float o[32];
-#pragma unroll
-                    for (int c = 0; c < HD / 32; ++c) {
-                        tmem_ld32(tO + lane_off + c * 32, o);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) o[e] *= factor;
-                        tmem_st32(tO + lane_off + c * 32, o);
-                    }
-                    tmem_st_wait();
-                    tc_fence_before();
-                }
+            const bool grow = mloc > m + kRescaleThreshold || (m == -INFINITY && mloc > -INFINITY);
+            const bool touch_o = grow && kb >= 1 && m != -INFINITY;
+            float factor = 1.f;
+            if (grow) {
+                factor = (m == -INFINITY) ? 0.f : fast_exp2(m - mloc);
                 l *= factor;
                 m = mloc;
+            }
+            if (__any_sync(0xffffffffu, touch_o)) {     // warp-collective tcgen05.ld/st
+                tc_fence_after();
+                const float f = touch_o ? factor : 1.f;
+                float o[32];
+#pragma unroll
+                for (int c = 0; c < HD / 32; ++c) {
+                    tmem_ld32(tO + lane_off + c * 32, o);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) o[e] *= f;
+                    tmem_st32(tO + lane_off + c * 32, o);
+                }
+                tmem_st_wait();
+                tc_fence_before();
             }
             const float mu = (m == -INFINITY) ? 0.f : m;
             float ls[8];
@@ -590,7 +601,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     extern __shared__ uint8_t dsmem[];
     __shared__ Smem3 sh;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tile = blockIdx.x, h0 = 2 * blockIdx.y;
+    const int tile = blockIdx.y, h0 = 2 * blockIdx.x;
     const int g = h0 / (p.num_heads / p.kv_heads);
     const int req = p.tile_req[tile], row0 = p.tile_row0[tile], nrows = p.tile_rows[tile];
     const int kmax = p.causal ? p.row_pos[row0 + nrows - 1] + 1 : p.kv_len[req];
@@ -733,22 +744,26 @@ __global__ void __launch_bounds__(kThreads2, 1)
             const float mloc = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                                      fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) *
                                p.scale_log2;
-            if (mloc > m + kRescaleThreshold || (m == -INFINITY && mloc > -INFINITY)) {
-                const float factor = (m == -INFINITY) ? 0.f : fast_exp2(m - mloc);
-                if (kb >= 1 && m != -INFINITY) {
-                    // PV_t(kb-1) retired before QK_t(kb) (in-order), so O is quiescent
-                    float o[32];
-#pragma unroll
-                    for (int c = 0; c < HD / 32; ++c) {
-                        tmem_ld32(tO + c * 32, o);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) o[e] *= factor;
-                        tmem_st32(tO + c * 32, o);
-                    }
-                }
+            const bool grow = mloc > m + kRescaleThreshold || (m == -INFINITY && mloc > -INFINITY);
+            const bool touch_o = grow && kb >= 1 && m != -INFINITY;
+            float factor = 1.f;
+            if (grow) {
+                factor = (m == -INFINITY) ? 0.f : fast_exp2(m - mloc);
                 l *= factor;
                 m = mloc;
+            }
+            if (__any_sync(0xffffffffu, touch_o)) {     // warp-collective tcgen05.ld/st
+                // PV_t(kb-1) retired before QK_t(kb) (in-order), so O is quiescent
+                const float f = touch_o ? factor : 1.f;
+                float o[32];
+#pragma unroll
+                for (int c = 0; c < HD / 32; ++c) {
+                    tmem_ld32(tO + c * 32, o);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) o[e] *= f;
+                    tmem_st32(tO + c * 32, o);
+                }
             }
             const float mu = (m == -INFINITY) ? 0.f : m;
             float ls[8];
@@ -834,7 +849,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     extern __shared__ uint8_t dsmem[];
     __shared__ Smem4 sh;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tile = blockIdx.x, h0 = 2 * blockIdx.y;
+    const int tile = blockIdx.y, h0 = 2 * blockIdx.x;
     const int g = h0 / (p.num_heads / p.kv_heads);
     const int req = p.tile_req[tile], row0 = p.tile_row0[tile], nrows = p.tile_rows[tile];
     const int kmax = p.causal ? p.row_pos[row0 + nrows - 1] + 1 : p.kv_len[req];
@@ -963,24 +978,28 @@ __global__ void __launch_bounds__(kThreads2, 1)
             const float mloc = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
                                      fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) *
                                p.scale_log2;
-            if (mloc > m + kRescaleThreshold || (m == -INFINITY && mloc > -INFINITY)) {
-                const float factor = (m == -INFINITY) ? 0.f : fast_exp2(m - mloc);
-                if (kb >= 1 && m != -INFINITY) {
-                    // PV(kb-1) may still be queued: O is touched only after it retired
-                    mbar_wait(&sh.pv_done[t], (uint32_t)(kb - 1) & 1u);
-                    tc_fence_after();
-                    float o[32];
-#pragma unroll
-                    for (int c = 0; c < HD / 32; ++c) {
-                        tmem_ld32(tO + c * 32, o);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) o[e] *= factor;
-                        tmem_st32(tO + c * 32, o);
-                    }
-                }
+            const bool grow = mloc > m + kRescaleThreshold || (m == -INFINITY && mloc > -INFINITY);
+            const bool touch_o = grow && kb >= 1 && m != -INFINITY;
+            float factor = 1.f;
+            if (grow) {
+                factor = (m == -INFINITY) ? 0.f : fast_exp2(m - mloc);
                 l *= factor;
                 m = mloc;
+            }
+            if (__any_sync(0xffffffffu, touch_o)) {     // warp-collective tcgen05.ld/st
+                // PV(kb-1) may still be queued: O is touched only after it retired
+                mbar_wait(&sh.pv_done[t], (uint32_t)(kb - 1) & 1u);
+                tc_fence_after();
+                const float f = touch_o ? factor : 1.f;
+                float o[32];
+#pragma unroll
+                for (int c = 0; c < HD / 32; ++c) {
+                    tmem_ld32(tO + c * 32, o);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) o[e] *= f;
+                    tmem_st32(tO + c * 32, o);
+                }
             }
             const float mu = (m == -INFINITY) ? 0.f : m;
             float ls[8];
@@ -1059,7 +1078,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __shared__ float s_lse[2][BM];
     __shared__ int32_t s_qn[2];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tile = blockIdx.x, g = blockIdx.y;
+    const int tile = blockIdx.y, g = blockIdx.x;
     const int hq = p.num_heads / p.kv_heads;
     const int req = p.tile_req[tile], k0 = p.row_pos[p.tile_row0[tile]];
     const int64_t s0 = p.req_off[req];
@@ -1251,6 +1270,7 @@ kvs_status kvs_attention_fwd(const void *q, const int32_t *row_pos, int64_t n_ro
     KVS_REQUIRE(batch != nullptr, KVS_EPARAM, "null batch");
     KVS_REQUIRE(causal || kv_len != nullptr, KVS_EPARAM, "non-causal attention needs kv_len");
     if (n_tiles <= 0 || n_rows <= 0) return KVS_OK;
+    KVS_REQUIRE(n_tiles <= 65535, KVS_ESHAPE, "more than 65535 row tiles in one launch");
     CUtensorMap mq, mkv;
     KVS_REQUIRE(make_q_map(&mq, q, n_rows, num_heads, 128), KVS_ECUDA, "Q tensor map");
     KVS_REQUIRE(make_kv_map(&mkv, arena), KVS_ECUDA, "KV tensor map");
@@ -1279,27 +1299,27 @@ kvs_status kvs_attention_fwd(const void *q, const int32_t *row_pos, int64_t n_ro
         const size_t smem = 1024 + 2 * attn::TILE_BYTES + attn::RING4 * attn::TILE4;
         cudaFuncSetAttribute(attn::fwd4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
-        attn::fwd4_kernel<<<dim3(n_tiles, num_heads / 2), attn::kThreads2, smem, s>>>(mq, mkv, p);
+        attn::fwd4_kernel<<<dim3(num_heads / 2, n_tiles), attn::kThreads2, smem, s>>>(mq, mkv, p);
     } else if (out != nullptr && group % 2 == 0 && (variant == nullptr || variant[0] == '3')) {
         const size_t smem = 1024 + attn::TILE_BYTES * (2 + attn::RING3);
         cudaFuncSetAttribute(attn::fwd3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
-        attn::fwd3_kernel<<<dim3(n_tiles, num_heads / 2), attn::kThreads2, smem, s>>>(mq, mkv, p);
+        attn::fwd3_kernel<<<dim3(num_heads / 2, n_tiles), attn::kThreads2, smem, s>>>(mq, mkv, p);
     } else if (out != nullptr && group % 2 == 0 && variant[0] == '2') {
         const size_t smem = 1024 + attn::TILE_BYTES * (2 + attn::RING + 2);
         cudaFuncSetAttribute(attn::fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
-        attn::fwd2_kernel<<<dim3(n_tiles, num_heads / 2), attn::kThreads2, smem, s>>>(mq, mkv, p);
+        attn::fwd2_kernel<<<dim3(num_heads / 2, n_tiles), attn::kThreads2, smem, s>>>(mq, mkv, p);
     } else if (out != nullptr) {
         const size_t smem = fwd_smem<true>();
         cudaFuncSetAttribute(attn::fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
-        attn::fwd_kernel<true><<<dim3(n_tiles, num_heads), attn::kThreads, smem, s>>>(mq, mkv, p);
+        attn::fwd_kernel<true><<<dim3(num_heads, n_tiles), attn::kThreads, smem, s>>>(mq, mkv, p);
     } else {
         const size_t smem = fwd_smem<false>();
         cudaFuncSetAttribute(attn::fwd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
-        attn::fwd_kernel<false><<<dim3(n_tiles, num_heads), attn::kThreads, smem, s>>>(mq, mkv, p);
+        attn::fwd_kernel<false><<<dim3(num_heads, n_tiles), attn::kThreads, smem, s>>>(mq, mkv, p);
     }
     KVS_CHECK_LAUNCH("kvs_attention_fwd");
     return KVS_OK;
@@ -1373,7 +1393,7 @@ kvs_status kvs_dhd_alpha(const void *q, int32_t num_heads, int32_t causal, int32
     const size_t smem = 1024 + attn::TILE_BYTES * (1 + attn::NS);
     cudaFuncSetAttribute(attn::colsum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    attn::colsum_kernel<<<dim3(n_tiles, arena->kv_heads), attn::kThreads, smem, s>>>(mq, mkv, cp);
+    attn::colsum_kernel<<<dim3(arena->kv_heads, n_tiles), attn::kThreads, smem, s>>>(mq, mkv, cp);
     attn::alpha_reduce_kernel<<<kNumSMs * 4, 256, 0, s>>>(part, n_total, arena->kv_heads,
                                                          num_heads, alpha);
     KVS_CHECK_LAUNCH("kvs_dhd_alpha");

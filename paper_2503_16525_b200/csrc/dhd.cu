@@ -143,16 +143,15 @@ __global__ void __launch_bounds__(1024) radix_select_kernel(
 }
 
 // ---------------------------------------------------------------- D2 fused
-// One persistent launch: CTAs pull 64-row chunks (request-major) from an
-// atomic work counter and stream dv-L1 x alpha for them (8 warps x 8 rows,
-// 16-byte loads).  A per-request completion counter elects the CTA that
+// One persistent launch: CTAs pull 16-row stages (request-major) from an
+// atomic work counter and stream dv-L1 x alpha for them (16 threads per row,
+// 16-byte loads, all of a stage's loads in flight at once).  A per-request completion counter elects the CTA that
 // finished a request's last chunk to run that request's top-B selection while
 // the other CTAs keep streaming later requests.  Selection: 4 radix passes
 // (8-bit digits) over the descending-score key ~bits(score) of the reused
 // rows give the B-th score; rows strictly better are kept and the remaining
 // budget is filled with the equal-score rows in ascending position order
 // (selection.py:63-66 tie rule) by an ordered block scan.
-constexpr int kSelChunk = 64;
 constexpr int kSelThreads = 256;
 
 constexpr int kSelSmemKeys = 16384;   // requests up to 16k tokens select from smem
@@ -161,13 +160,13 @@ constexpr int kSelSmemKeys = 16384;   // requests up to 16k tokens select from s
 // finite and >= 0; a denormal score ties with 0 - below any bf16 signal.)
 __device__ __forceinline__ uint32_t sel_key32(const float *score, const int32_t *src_slot,
                                               int64_t t) {
-    if (src_slot[t] < 0) return 0xFFFFFFFFu;
-    const uint32_t k = ~__float_as_uint(fmaxf(score[t], 0.f));
+    if (__ldcg(src_slot + t) < 0) return 0xFFFFFFFFu;
+    const uint32_t k = ~__float_as_uint(fmaxf(__ldcg(score + t), 0.f));   // written by other CTAs
     return k < 0xFFFFFFFEu ? k : 0xFFFFFFFEu;
 }
 
 template <bool kSmem>
-__device__ void select_request(const float *__restrict__ score, const int32_t *__restrict__ src_slot,
+__device__ __noinline__ void select_request(const float *__restrict__ score, const int32_t *__restrict__ src_slot,
                                int64_t s, int64_t n, int32_t B, uint8_t *__restrict__ selected,
                                uint32_t *keys, uint32_t *hist, uint32_t *sh) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -202,27 +201,31 @@ __device__ void select_request(const float *__restrict__ score, const int32_t *_
         return kSmem ? keys[i] : sel_key32(score, src_slot, s + i);
     };
     if (tid == 0) { sh[0] = 0; sh[1] = (uint32_t)B; }
-    __syncthreads();
-    uint32_t mask = 0;
     __shared__ uint32_t wsum[NW];
-    __shared__ uint32_t whist[NW][256];      // per-warp histograms (no cross-warp contention)
+    uint32_t mask = 0;
+    // 4 radix passes (8-bit digits, most significant first) find the B-th
+    // smallest key; histograms by plain shared atomics (same-bin lanes of a
+    // warp serialise in the atomic unit, far cheaper than match.any)
     for (int pass = 0; pass < 4; ++pass) {
         const int shift = 24 - 8 * pass;
-        for (int w = 0; w < NW; ++w) whist[w][tid] = 0;
+        hist[tid] = 0;
         __syncthreads();
         const uint32_t prefix = sh[0];
-        const int64_t nr = (n + 31) & ~(int64_t)31;    // whole warps stay converged
+        const int64_t nr = (n + 31) & ~(int64_t)31;      // whole warps stay converged
         for (int64_t i = tid; i < nr; i += kSelThreads) {
             const uint32_t key = i < n ? key_at(i) : 0xFFFFFFFFu;
             const bool in = key != 0xFFFFFFFFu && (key & mask) == prefix;
-            const uint32_t bin = in ? (key >> shift) & 0xff : 256u + lane;
-            const uint32_t peers = __match_any_sync(0xffffffffu, bin);
-            if (in && lane == __ffs(peers) - 1) whist[wid][bin] += __popc(peers);
+            const uint32_t bin = (key >> shift) & 0xff;
+            // scores cluster in a few digits (same exponent): the bin of the
+            // first active lane is counted with one atomic per warp, the
+            // rest individually
+            const uint32_t act = __ballot_sync(0xffffffffu, in);
+            if (act == 0) continue;
+            const uint32_t lead = __shfl_sync(0xffffffffu, bin, __ffs(act) - 1);
+            const uint32_t same = __ballot_sync(0xffffffffu, in && bin == lead);
+            if (lane == __ffs(act) - 1) atomicAdd(&hist[lead], (uint32_t)__popc(same));
+            if (in && bin != lead) atomicAdd(&hist[bin], 1u);
         }
-        __syncthreads();
-        uint32_t tot = 0;
-        for (int w = 0; w < NW; ++w) tot += whist[w][tid];
-        hist[tid] = tot;
         __syncthreads();
         const uint32_t c = hist[tid];
         uint32_t incl = c;
@@ -246,137 +249,376 @@ __device__ void select_request(const float *__restrict__ score, const int32_t *_
         __syncthreads();
     }
     const uint32_t thr = sh[0], ties_needed = sh[1];
-    // thread-contiguous segments: count ties, one block scan, then emit in order
-    const int64_t seg = (n + kSelThreads - 1) / kSelThreads;
-    const int64_t a = tid * seg, b = min(n, a + seg);
+    // ties at the threshold key are taken in ascending position order
+    // (selection.py:63-66): warp w owns the contiguous range [a, b) and walks
+    // it 32 keys at a time, so ballots give each tie its rank in order
+    const int64_t per = (n + NW - 1) / NW;
+    const int64_t a = wid * per, b = min(n, a + per);
     uint32_t mine = 0;
-    for (int64_t i = a; i < b; ++i) mine += key_at(i) == thr;
-    uint32_t incl = mine;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
+    for (int64_t i0 = a; i0 < b; i0 += 32) {
+        const int64_t i = i0 + lane;
+        mine += __popc(__ballot_sync(0xffffffffu, i < b && key_at(i) == thr));
     }
+    if (lane == 0) wsum[wid] = mine;
     __syncthreads();
-    if (lane == 31) wsum[wid] = incl;
-    __syncthreads();
-    uint32_t before = incl - mine;
+    uint32_t before = 0;
     for (int w = 0; w < wid; ++w) before += wsum[w];
-    for (int64_t i = a; i < b; ++i) {
-        const uint32_t key = key_at(i);
+    const uint32_t lt = (1u << lane) - 1u;
+    for (int64_t i0 = a; i0 < b; i0 += 32) {
+        const int64_t i = i0 + lane;
+        const uint32_t key = i < b ? key_at(i) : 0xFFFFFFFFu;
+        const uint32_t tie = __ballot_sync(0xffffffffu, i < b && key == thr);
         bool keep = key < thr;
-        if (key == thr) {
-            keep = before < ties_needed;
-            ++before;
-        }
-        selected[s + i] = keep ? 1 : 0;
+        if (i < b && key == thr) keep = before + __popc(tie & lt) < ties_needed;
+        before += __popc(tie);
+        if (i < b) selected[s + i] = keep ? 1 : 0;
     }
 }
 
-__global__ void __launch_bounds__(kSelThreads) dhd_select_fused_kernel(
+// Register-resident selection for requests of up to kRegKeys positions: each
+// thread holds its keys (i = tid + 256k), 4 radix passes with per-warp
+// histograms (one aggregated atomic per warp instruction for the dominant
+// digit), and the tie band at the threshold is resolved in position order
+// only when it is actually split (rare: scores are continuous).
+constexpr int kKPT = 16;
+constexpr int kRegKeys = kKPT * kSelThreads;
+
+template <bool kReg>
+__device__ __noinline__ void select_fast(const float *__restrict__ score,
+                                         const int32_t *__restrict__ src_slot, int64_t s, int64_t n,
+                                         int32_t B, uint8_t *__restrict__ selected,
+                                         uint32_t *whist /* [8][256] */, uint32_t *keys /* n, smem */,
+                                         uint32_t *sh) {
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    constexpr int NW = kSelThreads / 32;
+    __shared__ uint32_t wsum[NW];
+    // key of position tid + 256k: descending score, non-reused rows largest
+    const int nk = kReg ? kKPT : (int)((n + kSelThreads - 1) / kSelThreads);
+    uint32_t kr[kReg ? kKPT : 1];
+    auto key_of = [&](float sc, int32_t sl) -> uint32_t {
+        const uint32_t x = ~__float_as_uint(fmaxf(sc, 0.f));
+        return sl < 0 ? 0xFFFFFFFFu : (x < 0xFFFFFFFEu ? x : 0xFFFFFFFEu);
+    };
+    if constexpr (kReg) {
+        int32_t sl[kKPT];
+        float sc[kKPT];
+#pragma unroll
+        for (int k = 0; k < kKPT; ++k) {
+            const int64_t i = tid + (int64_t)k * kSelThreads;
+            sl[k] = i < n ? __ldcg(src_slot + s + i) : -1;
+            sc[k] = i < n ? __ldcg(score + s + i) : 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < kKPT; ++k) kr[k] = key_of(sc[k], sl[k]);
+    } else {
+        for (int k0 = 0; k0 < nk; k0 += 8) {
+            int32_t sl[8];
+            float sc[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int64_t i = tid + (int64_t)(k0 + u) * kSelThreads;
+                sl[u] = i < n ? __ldcg(src_slot + s + i) : -1;
+                sc[u] = i < n ? __ldcg(score + s + i) : 0.f;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (k0 + u < nk) keys[tid + (k0 + u) * kSelThreads] = key_of(sc[u], sl[u]);
+        }
+    }
+#define KEY(k) (kReg ? kr[(k) < kKPT ? (k) : 0] : keys[tid + (k) * kSelThreads])
+    if (B <= 0) {
+        for (int64_t i = tid; i < n; i += kSelThreads) selected[s + i] = 0;
+        return;
+    }
+    uint32_t prefix = 0, mask = 0, need = (uint32_t)B;
+    uint32_t *wh = whist + wid * 256;
+    for (int pass = 0; pass < 4; ++pass) {
+        const int shift = 24 - 8 * pass;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) whist[w * 256 + tid] = 0;
+        __syncthreads();
+#pragma unroll(kReg ? kKPT : 1)
+        for (int k = 0; k < nk; ++k) {
+            const uint32_t key = KEY(k);
+            const bool in = key != 0xFFFFFFFFu && (key & mask) == prefix;
+            const uint32_t bin = (key >> shift) & 0xff;
+            const uint32_t act = __ballot_sync(0xffffffffu, in);
+            if (act == 0) continue;
+            // scores cluster in a few digits (same exponent): the first active
+            // lane's digit is counted with one atomic, the others individually
+            const int first = __ffs(act) - 1;
+            const uint32_t lead = __shfl_sync(0xffffffffu, bin, first);
+            const uint32_t same = __ballot_sync(0xffffffffu, in && bin == lead);
+            if (lane == first) atomicAdd(&wh[lead], (uint32_t)__popc(same));
+            if (in && bin != lead) atomicAdd(&wh[bin], 1u);
+        }
+        __syncthreads();
+        uint32_t c = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) c += whist[w * 256 + tid];
+        uint32_t incl = c;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        if (lane == 31) wsum[wid] = incl;
+        __syncthreads();
+        uint32_t base = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) base += w < wid ? wsum[w] : 0u;
+        const uint32_t excl = base + incl - c;
+        if (c > 0 && excl < need && excl + c >= need) {
+            sh[0] = prefix | ((uint32_t)tid << shift);
+            sh[1] = need - excl;
+        }
+        __syncthreads();
+        prefix = sh[0];
+        need = sh[1];
+        mask |= 0xffu << shift;
+    }
+    const uint32_t thr = prefix;
+    // ties at the threshold: if every tie fits, no ordering is needed
+    uint32_t mine = 0;
+#pragma unroll(kReg ? kKPT : 1)
+    for (int k = 0; k < nk; ++k) mine += KEY(k) == thr;
+    uint32_t tot = mine;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, o);
+    if (lane == 0) wsum[wid] = tot;
+    __syncthreads();
+    uint32_t ties = 0;
+#pragma unroll
+    for (int w = 0; w < NW; ++w) ties += wsum[w];
+    __syncthreads();
+    if (ties == need) {
+#pragma unroll(kReg ? kKPT : 1)
+        for (int k = 0; k < nk; ++k) {
+            const int64_t i = tid + (int64_t)k * kSelThreads;
+            if (i < n) selected[s + i] = KEY(k) <= thr ? 1 : 0;
+        }
+        return;
+    }
+    // split tie band (selection.py:63-66, ascending position among equals):
+    // position i = tid + 256k, so the order is k-major, then tid
+#pragma unroll(kReg ? kKPT : 1)
+    for (int k = 0; k < nk; ++k) {
+        const uint32_t key = KEY(k);
+        const bool tie = key == thr;
+        const uint32_t bal = __ballot_sync(0xffffffffu, tie);
+        if (lane == 0) wsum[wid] = __popc(bal);
+        __syncthreads();
+        uint32_t before = __popc(bal & ((1u << lane) - 1u)), total_k = 0;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            before += w < wid ? wsum[w] : 0u;
+            total_k += wsum[w];
+        }
+        const int64_t i = tid + (int64_t)k * kSelThreads;
+        if (i < n) selected[s + i] = (key < thr || (tie && before < need)) ? 1 : 0;
+        need = need > total_k ? need - total_k : 0;
+        __syncthreads();
+    }
+#undef KEY
+}
+
+// Streaming: stage = 16 rows of one request (16 | page size: one arena page).
+// Thread t owns row t/16 and the 16-byte vectors v = t%16 + 16j of it in both
+// V rows.  Stages are assigned round-robin (no atomics); each thread copies
+// its own vectors with cp.async into a private slice of a kDepth-deep shared
+// ring and consumes exactly those bytes, so the pipeline needs no barriers:
+// stage k+kDepth-1's copies are in flight while stage k is reduced, and its
+// metadata (liveness, page, alpha) was loaded one stage earlier still.
+constexpr int kStageRows = 16;
+constexpr int kVecPerThread = 8;          // 16 threads x 8 x 16 B = one 2 KB V row
+constexpr int kDepth = 3;
+constexpr size_t kStageBytes = (size_t)kSelThreads * kVecPerThread * 2 * 16;   // 64 KB
+constexpr int kMetaStages = 64;           // metadata chunk: 1024 rows x 24 B
+// requests up to kSmemKeys positions select with their keys in the (then idle) ring
+constexpr int kSmemKeys = (int)((kDepth * kStageBytes - 8 * 1024) / 4) / kSelThreads * kSelThreads;
+
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+__global__ void __launch_bounds__(kSelThreads, 1) dhd_select_fused_kernel(
     const __nv_bfloat16 *__restrict__ v_true, const float *__restrict__ alpha,
     const int32_t *__restrict__ src_slot, int32_t layer, ArenaC A,
-    const int64_t *__restrict__ req_off, int32_t *__restrict__ chunk_off, int32_t n_req,
+    const int64_t *__restrict__ req_off, int32_t n_req,
     const int32_t *__restrict__ budget, const int32_t *__restrict__ block_table,
     int32_t max_pages, float *__restrict__ dv_l1, float *__restrict__ score,
     uint8_t *__restrict__ selected, uint32_t *__restrict__ counters) {
-    // counters[0] = work cursor, counters[1 + r] = finished chunks of request r
-    extern __shared__ uint32_t s_keys[];
-    __shared__ uint32_t hist[256];
+    // counters[0] = CTAs that published their rows, counters[1] = selectors
+    // done (the last one re-zeroes both)
+    extern __shared__ __align__(16) uint8_t s_ring[];            // kDepth x kStageBytes
+    int32_t *co = reinterpret_cast<int32_t *>(s_ring + kDepth * kStageBytes);   // n_req + 1
     __shared__ uint32_t sh[4];
-    __shared__ int s_item, s_last;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    // chunk prefix over requests: every CTA computes its own copy (n_req is small)
-    int32_t *co = chunk_off + (int64_t)blockIdx.x * (n_req + 1);
-    if (threadIdx.x == 0) {
-        int32_t acc = 0;
-        for (int r = 0; r < n_req; ++r) {
-            co[r] = acc;
-            acc += (int32_t)((req_off[r + 1] - req_off[r] + kSelChunk - 1) / kSelChunk);
+    __shared__ int s_ticket;
+    const int tid = threadIdx.x;
+    if (tid < 32) {                           // stage prefix over requests
+        int32_t carry = 0;
+        for (int r0 = 0; r0 < n_req; r0 += 32) {
+            const int r = r0 + tid;
+            const int32_t c = r < n_req ? (int32_t)((req_off[r + 1] - req_off[r] + kStageRows - 1) /
+                                                    kStageRows) : 0;
+            int32_t incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (tid >= o) incl += y;
+            }
+            if (r < n_req) co[r] = carry + incl - c;
+            carry += __shfl_sync(0xffffffffu, incl, 31);
         }
-        co[n_req] = acc;
+        if (tid == 0) co[n_req] = carry;
     }
     __syncthreads();
     const int total = co[n_req];
-    const int nvec = A.G * A.D / 8;
-    while (true) {
-        if (threadIdx.x == 0) s_item = (int)atomicAdd(&counters[0], 1u);
+    const int nvec = A.G * A.D / 8;           // 16-byte vectors per V row (<= 128)
+    const int row = tid / 16, sub = tid % 16;
+    const int my_stages = total > (int)blockIdx.x ? (total - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+
+    // Metadata (row index, liveness, page row, alpha) of up to kMetaStages of
+    // this CTA's stages is loaded cooperatively in one round of independent
+    // loads into shared memory, so the copy pipeline never waits on it.
+    struct RowMeta {
+        int64_t t;        // flat row (-1: none)
+        int64_t prow;     // page * P + row in page; -1 when not reused
+        float alpha;
+    };
+    RowMeta *meta = reinterpret_cast<RowMeta *>(co + n_req + 1 + ((n_req + 1) & 1));
+    __shared__ int s_live;
+    // returns the number of live (reused) rows of stages [k_first, k_first +
+    // k_count) of this CTA, compacted into meta[]; non-reused rows get their
+    // zero dv-L1 / score right here and never enter the copy pipeline
+    auto load_meta = [&](int k_first, int k_count) -> int {
+        if (tid == 0) s_live = 0;
         __syncthreads();
-        const int item = s_item;
-        if (item >= total) break;
-        int r = 0, hi = n_req;            // chunk_off[r] <= item < chunk_off[r+1]
-        while (hi - r > 1) {
-            const int mid = (r + hi) >> 1;
-            if (co[mid] <= item) r = mid; else hi = mid;
+        for (int j = tid; j < k_count * kStageRows; j += kSelThreads) {
+            const int k = k_first + j / kStageRows, rr = j % kStageRows;
+            const int item = (int)blockIdx.x + k * (int)gridDim.x;
+            int r = 0, hi = n_req;
+            while (hi - r > 1) {
+                const int mid = (r + hi) >> 1;
+                if (co[mid] <= item) r = mid; else hi = mid;
+            }
+            const int64_t s0 = req_off[r], n = req_off[r + 1] - s0;
+            const int64_t i = (int64_t)(item - co[r]) * kStageRows + rr;
+            if (i >= n) continue;
+            const int64_t t = s0 + i;
+            const bool live = __ldg(src_slot + t) >= 0;
+            const int64_t page = __ldg(block_table + (int64_t)r * max_pages + i / A.P);
+            const float al = __ldg(alpha + t);
+            if (live) {
+                const int at = atomicAdd(&s_live, 1);
+                meta[at] = RowMeta{t, page * A.P + i % A.P, al};
+            } else {
+                dv_l1[t] = 0.f;
+                score[t] = 0.f;
+            }
         }
-        const int64_t s = req_off[r], n = req_off[r + 1] - s;
-        const int64_t i0 = (int64_t)(item - co[r]) * kSelChunk;
-        // each warp streams 8 rows, two at a time (16 x 16-byte loads in flight per lane)
-        for (int j = wid * 8; j < wid * 8 + 8; j += 2) {
-            int64_t t2[2];
-            bool live[2];
-            const uint4 *vc[2], *vt[2];
+        __syncthreads();
+        return s_live;
+    };
+    // ring layout [stage][j][array][thread][16 B]: a warp's accesses to one
+    // (j, array) are 512 contiguous bytes (bank-conflict free)
+    const uint32_t my_slice = smem_u32(s_ring) + tid * 16;
+    auto issue = [&](int k_local, int slot, int n_live) {
+        const int e = k_local * kStageRows + row;
+        if (e < n_live) {
+            const RowMeta m = meta[e];
+            const uint4 *vc = reinterpret_cast<const uint4 *>(
+                A.row(m.prow / A.P, layer, 1, (int)(m.prow % A.P)));
+            const uint4 *vt = reinterpret_cast<const uint4 *>(v_true + m.t * (int64_t)(A.G * A.D));
+            const uint32_t dst = my_slice + (uint32_t)slot * (uint32_t)kStageBytes;
 #pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const int64_t i = i0 + j + u;
-                t2[u] = s + i;
-                live[u] = i < n && src_slot[s + i] >= 0;
-                if (i < n && !live[u] && lane == 0) { dv_l1[s + i] = 0.f; score[s + i] = 0.f; }
-                const int64_t page = live[u] ? block_table[(int64_t)r * max_pages + i / A.P] : 0;
-                vc[u] = reinterpret_cast<const uint4 *>(A.row(page, layer, 1, (int)(i % A.P)));
-                vt[u] = reinterpret_cast<const uint4 *>(v_true + t2[u] * (int64_t)(A.G * A.D));
-            }
-            float acc[2] = {0.f, 0.f};
-            for (int v0 = 0; v0 < nvec; v0 += 128) {
-                uint4 a[2][4], b[2][4];
-#pragma unroll
-                for (int u = 0; u < 2; ++u)
-#pragma unroll
-                    for (int k = 0; k < 4; ++k) {
-                        const int v = v0 + k * 32 + lane;
-                        if (live[u] && v < nvec) {
-                            a[u][k] = __ldcs(vc[u] + v);
-                            b[u][k] = __ldcs(vt[u] + v);
-                        }
-                    }
-#pragma unroll
-                for (int u = 0; u < 2; ++u)
-#pragma unroll
-                    for (int k = 0; k < 4; ++k)
-                        if (live[u] && v0 + k * 32 + lane < nvec) acc[u] += l1_diff8(a[u][k], b[u][k]);
-            }
-#pragma unroll
-            for (int u = 0; u < 2; ++u) {
-                const float x = warp_sum(acc[u]);
-                if (live[u] && lane == 0) {
-                    dv_l1[t2[u]] = x;
-                    score[t2[u]] = alpha[t2[u]] * x;
+            for (int j = 0; j < kVecPerThread; ++j) {
+                const int v = sub + 16 * j;
+                if (v < nvec) {
+                    cp_async16(dst + (2 * j) * (kSelThreads * 16), vc + v);
+                    cp_async16(dst + (2 * j + 1) * (kSelThreads * 16), vt + v);
                 }
             }
         }
+        cp_async_commit();
+    };
+
+    for (int c0 = 0; c0 < my_stages; c0 += kMetaStages) {
+        const int n_live = load_meta(c0, min(kMetaStages, my_stages - c0));
+        const int cn = (n_live + kStageRows - 1) / kStageRows;   // stages of live rows
+#pragma unroll
+        for (int j = 0; j < kDepth - 1; ++j) issue(j, j, n_live);
+        for (int k0 = 0; k0 < cn; k0 += kDepth) {
+#pragma unroll
+            for (int u = 0; u < kDepth; ++u) {      // unrolled: ring slots are static
+                const int k = k0 + u;
+                if (k >= cn) break;
+                // copies for stage k+depth-1 go out before stage k is reduced
+                issue(k + kDepth - 1, (u + kDepth - 1) % kDepth, n_live);
+                cp_async_wait<kDepth - 1>();
+                const int e = k * kStageRows + row;
+                float acc = 0.f;
+                if (e < n_live) {
+                    const uint8_t *src = s_ring + (size_t)u * kStageBytes + (size_t)tid * 16;
+#pragma unroll
+                    for (int j = 0; j < kVecPerThread; ++j)
+                        if (sub + 16 * j < nvec) {
+                            const uint4 a =
+                                *reinterpret_cast<const uint4 *>(src + (2 * j) * (kSelThreads * 16));
+                            const uint4 b = *reinterpret_cast<const uint4 *>(
+                                src + (2 * j + 1) * (kSelThreads * 16));
+                            acc += l1_diff8(a, b);
+                        }
+                }
+#pragma unroll
+                for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+                if (e < n_live && sub == 0) {
+                    const RowMeta m = meta[e];
+                    dv_l1[m.t] = acc;
+                    score[m.t] = m.alpha * acc;
+                }
+            }
+        }
+        cp_async_wait<0>();
+        __syncthreads();                     // meta[] is rewritten by the next chunk
+    }
+    // every CTA publishes its rows once; the last min(n_req, grid) CTAs to get
+    // here become selectors, wait until all CTAs have published, and run one
+    // request's top-B each (in parallel), so only one selection is exposed
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) s_ticket = (int)atomicAdd(&counters[0], 1u);
+    __syncthreads();
+    const int n_sel = n_req < (int)gridDim.x ? n_req : (int)gridDim.x;
+    const int sel = s_ticket - ((int)gridDim.x - n_sel);
+    if (sel < 0) return;
+    if (tid == 0) {
+        volatile uint32_t *done = counters;
+        while (*done < gridDim.x) __nanosleep(32);
         __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            const uint32_t done = atomicAdd(&counters[1 + r], 1u) + 1;
-            s_last = (done == (uint32_t)(co[r + 1] - co[r])) ? 1 : 0;
-        }
-        __syncthreads();
-        if (s_last) {
-            __threadfence();
-            if (n <= kSelSmemKeys)
-                select_request<true>(score, src_slot, s, n, budget[r], selected, s_keys, hist, sh);
-            else
-                select_request<false>(score, src_slot, s, n, budget[r], selected, s_keys, hist, sh);
-        }
+    }
+    __syncthreads();
+    uint32_t *whist = reinterpret_cast<uint32_t *>(s_ring);           // the ring is free now
+    uint32_t *keys = whist + kSelThreads / 32 * 256;
+    for (int r = sel; r < n_req; r += n_sel) {
+        const int64_t s0 = req_off[r], n = req_off[r + 1] - s0;
+        if (n <= kRegKeys)
+            select_fast<true>(score, src_slot, s0, n, budget[r], selected, whist, keys, sh);
+        else if (n <= kSmemKeys)
+            select_fast<false>(score, src_slot, s0, n, budget[r], selected, whist, keys, sh);
+        else
+            select_request<false>(score, src_slot, s0, n, budget[r], selected, keys,
+                                  keys + kSelSmemKeys, sh);
         __syncthreads();
     }
-    // the last CTA out leaves the counters zeroed for the next launch
-    if (threadIdx.x == 0) {
+    // the last selector out leaves the counters zeroed for the next launch
+    if (tid == 0 && atomicAdd(&counters[1], 1u) + 1 == (uint32_t)n_sel) {
+        counters[0] = 0;
+        counters[1] = 0;
         __threadfence();
-        if (atomicAdd(&counters[1 + n_req], 1u) + 1 == gridDim.x) {
-            for (int r = 0; r < n_req + 2; ++r) counters[r] = 0;
-            __threadfence();
-        }
     }
 }
 
@@ -609,17 +851,6 @@ __global__ void decode_attn_combine_kernel(const float *__restrict__ ws, int32_t
 
 static inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-__global__ void chunk_offsets_kernel(const int64_t *req_off, int32_t n_req, int32_t *chunk_off) {
-    if (threadIdx.x == 0) {
-        int32_t acc = 0;
-        chunk_off[0] = 0;
-        for (int r = 0; r < n_req; ++r) {
-            acc += (int32_t)((req_off[r + 1] - req_off[r] + kSelChunk - 1) / kSelChunk);
-            chunk_off[r + 1] = acc;
-        }
-    }
-}
-
 static int decode_splits(int64_t n_rows, int G, int max_kv) {
     int64_t want = (2 * kNumSMs + n_rows * G - 1) / (n_rows * G);
     int64_t cap = (max_kv + 127) / 128;
@@ -637,8 +868,8 @@ extern "C" {
 
 size_t kvs_dhd_select_workspace(int64_t n_total, int32_t n_req) {
     (void)n_total;
-    return align256(sizeof(uint32_t) * (n_req + 2)) +
-           align256(sizeof(int32_t) * (n_req + 1) * 2 * kNumSMs);
+    (void)n_req;
+    return 256;            // three self-resetting counters
 }
 
 /* Workspace contract: the first kvs_dhd_select_workspace() bytes must be zero
@@ -654,16 +885,18 @@ kvs_status kvs_dhd_select(const void *v_true, const float *alpha, const int32_t 
     if (batch->n_total <= 0) return KVS_OK;
     cudaStream_t s = (cudaStream_t)stream;
     uint32_t *counters = (uint32_t *)ws;
-    int32_t *chunk_off = (int32_t *)((char *)ws + align256(sizeof(uint32_t) * (batch->n_req + 2)));
     // counters start zeroed (Workspace.get(zero=True)) and are re-zeroed by the kernel
-    const int grid = 2 * kNumSMs;
-    const size_t smem = sizeof(uint32_t) * kSelSmemKeys;
+    KVS_REQUIRE(arena->kv_heads * arena->head_dim <= 16 * kVecPerThread * 8, KVS_ESHAPE,
+                "select: kv_heads * head_dim must be <= 1024");
+    const size_t smem = kDepth * kStageBytes + sizeof(int32_t) * (batch->n_req + 2) +
+                        24 * kMetaStages * kStageRows;
+    KVS_REQUIRE(smem <= 227 * 1024, KVS_EPARAM, "select: too many requests in one batch");
     cudaFuncSetAttribute(dhd_select_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    dhd_select_fused_kernel<<<grid, kSelThreads, smem, s>>>(
+    dhd_select_fused_kernel<<<kNumSMs, kSelThreads, smem, s>>>(
         (const __nv_bfloat16 *)v_true, alpha, src_slot, layer, arena_c(arena), batch->req_off,
-        chunk_off, batch->n_req, budget, batch->block_table, batch->max_pages, dv_l1, score,
-        selected, counters);
+        batch->n_req, budget, batch->block_table, batch->max_pages, dv_l1, score, selected,
+        counters);
     KVS_CHECK_LAUNCH("kvs_dhd_select");
     return KVS_OK;
 }

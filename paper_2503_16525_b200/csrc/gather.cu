@@ -95,26 +95,29 @@ __global__ void __launch_bounds__(128) gather_kv_kernel(
     }
 }
 
-// Rotate-half with the row's coefficients already in shared memory.
-__device__ __forceinline__ void rope8_smem(const uint4 &lo_in, const uint4 &hi_in, uint4 &lo_out,
-                                           uint4 &hi_out, const float *cs, const float *sn,
-                                           int c) {
-    const __nv_bfloat16 *x1 = reinterpret_cast<const __nv_bfloat16 *>(&lo_in);
-    const __nv_bfloat16 *x2 = reinterpret_cast<const __nv_bfloat16 *>(&hi_in);
+// Rotate-half on 8 dims with the coefficients in registers (two float4 each).
+__device__ __forceinline__ void rope8_reg(const uint4 &lo_in, const uint4 &hi_in, uint4 &lo_out,
+                                          uint4 &hi_out, const float4 c0, const float4 c1,
+                                          const float4 s0, const float4 s1) {
+    const __nv_bfloat162 *x1 = reinterpret_cast<const __nv_bfloat162 *>(&lo_in);
+    const __nv_bfloat162 *x2 = reinterpret_cast<const __nv_bfloat162 *>(&hi_in);
     uint32_t *o1 = reinterpret_cast<uint32_t *>(&lo_out);
     uint32_t *o2 = reinterpret_cast<uint32_t *>(&hi_out);
+    const float cs[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    const float sn[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
 #pragma unroll
-    for (int k = 0; k < 8; k += 2) {
-        const float c0 = cs[8 * c + k], c1 = cs[8 * c + k + 1];
-        const float s0 = sn[8 * c + k], s1 = sn[8 * c + k + 1];
-        const float a0 = bf2f(x1[k]), a1 = bf2f(x1[k + 1]);
-        const float b0 = bf2f(x2[k]), b1 = bf2f(x2[k + 1]);
-        o1[k / 2] = pack_bf16x2(a0 * c0 - b0 * s0, a1 * c1 - b1 * s1);
-        o2[k / 2] = pack_bf16x2(b0 * c0 + a0 * s0, b1 * c1 + a1 * s1);
+    for (int k = 0; k < 4; ++k) {
+        const float2 a = __bfloat1622float2(x1[k]), b = __bfloat1622float2(x2[k]);
+        o1[k] = pack_bf16x2(a.x * cs[2 * k] - b.x * sn[2 * k], a.y * cs[2 * k + 1] - b.y * sn[2 * k + 1]);
+        o2[k] = pack_bf16x2(b.x * cs[2 * k] + a.x * sn[2 * k], b.y * cs[2 * k + 1] + a.y * sn[2 * k + 1]);
     }
 }
 
-// One CTA per query row.  qkv row = [q (H*D) | k (G*D) | v (G*D)].
+// One CTA per query row.  qkv row = [q (H*D) | k (G*D) | v (G*D)].  Work
+// items: (H+G)*D/16 rotation items (two 16-byte vectors each) followed by
+// G*D/8 V vectors; a thread takes two items per round and issues all of its
+// loads (qkv vectors, then the row's cos/sin, which depend only on the
+// position) before any arithmetic, so a CTA waits on two memory latencies.
 __global__ void __launch_bounds__(256) qkv_rope_scatter_kernel(
     const __nv_bfloat16 *__restrict__ qkv, int32_t H, Arena A, const int32_t *__restrict__ row_req,
     const int32_t *__restrict__ row_pos, const uint8_t *__restrict__ write_kv, int32_t layer,
@@ -122,67 +125,95 @@ __global__ void __launch_bounds__(256) qkv_rope_scatter_kernel(
     const float *__restrict__ sin_t, __nv_bfloat16 *__restrict__ q_out,
     __nv_bfloat16 *__restrict__ k_out, __nv_bfloat16 *__restrict__ v_out) {
     const int64_t row = blockIdx.x;
-    const int G = A.G, D = A.D, half = D / 2, chunks = half / 8;
+    const int G = A.G, D = A.D, half = D / 2, chunks = half / 8, vph = D / 8;
     const int64_t width = (int64_t)(H + 2 * G) * D;
     const uint4 *src = reinterpret_cast<const uint4 *>(qkv + row * width);
-    const int32_t pos = row_pos[row];
+    const int32_t pos = __ldg(row_pos + row);
     const bool rope = cos_t != nullptr;
     const bool wkv = write_kv == nullptr || write_kv[row] != 0;
     uint4 *dk = nullptr, *dv = nullptr;
     if (wkv) {
         const int32_t r = row_req[row];
-        const int64_t page = block_table[(int64_t)r * max_pages + pos / A.P];
+        const int64_t page = __ldg(block_table + (int64_t)r * max_pages + pos / A.P);
         dk = reinterpret_cast<uint4 *>(A.row(page, layer, 0, pos % A.P));
         dv = reinterpret_cast<uint4 *>(A.row(page, layer, 1, pos % A.P));
     }
-    __shared__ float s_cos[128], s_sin[128];
-    if (rope)
-        for (int i = threadIdx.x; i < half; i += blockDim.x) {
-            s_cos[i] = cos_t[(size_t)pos * half + i];
-            s_sin[i] = sin_t[(size_t)pos * half + i];
-        }
-    __syncthreads();
     uint4 *qo = reinterpret_cast<uint4 *>(q_out + row * (int64_t)H * D);
     uint4 *ko = k_out ? reinterpret_cast<uint4 *>(k_out + row * (int64_t)G * D) : nullptr;
     uint4 *vo = v_out ? reinterpret_cast<uint4 *>(v_out + row * (int64_t)G * D) : nullptr;
-    const int vecs_per_head = D / 8;
-    // q and k: (H + G) heads x chunks rotation items
-    for (int it = threadIdx.x; it < (H + G) * chunks; it += blockDim.x) {
-        const int h = it / chunks, c = it % chunks;
-        const int vlo = h * vecs_per_head + c, vhi = vlo + chunks;
-        uint4 lo = src[vlo], hi = src[vhi];
-        if (rope) {
-            uint4 lo_o, hi_o;
-            rope8_smem(lo, hi, lo_o, hi_o, s_cos, s_sin, c);
-            lo = lo_o;
-            hi = hi_o;
+    const float4 *c4 = reinterpret_cast<const float4 *>(cos_t + (size_t)pos * half);
+    const float4 *s4 = reinterpret_cast<const float4 *>(sin_t + (size_t)pos * half);
+    const int n_rope = (H + G) * chunks, n_items = n_rope + G * vph, vbase = (H + G) * vph;
+    for (int base = 0; base < n_items; base += 2 * blockDim.x) {
+        uint4 lo[2], hi[2];
+        int it[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            it[u] = base + u * blockDim.x + threadIdx.x;
+            if (it[u] < n_rope) {
+                const int h = it[u] / chunks, c = it[u] % chunks;
+                lo[u] = __ldcs(src + h * vph + c);
+                hi[u] = __ldcs(src + h * vph + c + chunks);
+            } else if (it[u] < n_items) {
+                lo[u] = __ldcs(src + vbase + (it[u] - n_rope));
+            }
         }
-        if (h < H) {
-            qo[vlo] = lo;
-            qo[vhi] = hi;
-        } else {
-            const int kl = vlo - H * vecs_per_head, kh = vhi - H * vecs_per_head;
-            if (dk) { dk[kl] = lo; dk[kh] = hi; }
-            if (ko) { ko[kl] = lo; ko[kh] = hi; }
+        float4 cs[2][2], sn[2][2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+            if (rope && it[u] < n_rope) {
+                const int c = it[u] % chunks;
+                cs[u][0] = __ldg(c4 + 2 * c);
+                cs[u][1] = __ldg(c4 + 2 * c + 1);
+                sn[u][0] = __ldg(s4 + 2 * c);
+                sn[u][1] = __ldg(s4 + 2 * c + 1);
+            }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            if (it[u] < n_rope) {
+                const int h = it[u] / chunks, c = it[u] % chunks;
+                const int vlo = h * vph + c, vhi = vlo + chunks;
+                uint4 a = lo[u], b = hi[u];
+                if (rope) rope8_reg(lo[u], hi[u], a, b, cs[u][0], cs[u][1], sn[u][0], sn[u][1]);
+                if (h < H) {
+                    qo[vlo] = a;
+                    qo[vhi] = b;
+                } else {
+                    const int kl = vlo - H * vph, kh = vhi - H * vph;
+                    if (dk) { dk[kl] = a; dk[kh] = b; }
+                    if (ko) { ko[kl] = a; ko[kh] = b; }
+                }
+            } else if (it[u] < n_items) {
+                const int v = it[u] - n_rope;
+                if (dv) dv[v] = lo[u];
+                if (vo) vo[v] = lo[u];
+            }
         }
-    }
-    const int vbase = (H + G) * vecs_per_head;
-    for (int v = threadIdx.x; v < G * vecs_per_head; v += blockDim.x) {
-        const uint4 x = src[vbase + v];
-        if (dv) dv[v] = x;
-        if (vo) vo[v] = x;
     }
 }
 
-// out[r] = table[ids[r]] (rows of `width` bf16).
+// out[r] = table[ids[r]] (rows of `width` bf16); out_f32 (optional) gets the
+// same row widened to fp32 - the residual stream and the first layer's GEMM
+// operand come out of one pass over the table rows.
 __global__ void embed_rows_kernel(const __nv_bfloat16 *__restrict__ table, int64_t width,
                                   const int64_t *__restrict__ ids, const int32_t *__restrict__ rows,
-                                  __nv_bfloat16 *__restrict__ out) {
+                                  __nv_bfloat16 *__restrict__ out, float *__restrict__ out_f32) {
     const int64_t r = blockIdx.x;
     const int64_t id = ids[rows ? rows[r] : r];
     const uint4 *s = reinterpret_cast<const uint4 *>(table + id * width);
     uint4 *d = reinterpret_cast<uint4 *>(out + r * width);
-    for (int64_t v = threadIdx.x; v < width / 8; v += blockDim.x) d[v] = s[v];
+    float4 *f = reinterpret_cast<float4 *>(out_f32 + r * width);
+    for (int64_t v = threadIdx.x; v < width / 8; v += blockDim.x) {
+        const uint4 x = __ldg(s + v);
+        d[v] = x;
+        if (out_f32 != nullptr) {
+            const __nv_bfloat162 *h = reinterpret_cast<const __nv_bfloat162 *>(&x);
+            const float2 a = __bfloat1622float2(h[0]), b = __bfloat1622float2(h[1]);
+            const float2 c = __bfloat1622float2(h[2]), e = __bfloat1622float2(h[3]);
+            __stcs(f + 2 * v, make_float4(a.x, a.y, b.x, b.y));
+            __stcs(f + 2 * v + 1, make_float4(c.x, c.y, e.x, e.y));
+        }
+    }
 }
 
 // Row set S = non-reused U selected U {n-1} of each request.
@@ -336,11 +367,12 @@ kvs_status kvs_qkv_rope_scatter(const void *qkv, int64_t n_rows, int32_t num_hea
 }
 
 kvs_status kvs_embed_rows(const void *table, int64_t width, const int64_t *ids,
-                          const int32_t *rows, int64_t n_rows, void *out, kvs_stream_t stream) {
+                          const int32_t *rows, int64_t n_rows, void *out, float *out_f32,
+                          kvs_stream_t stream) {
     KVS_REQUIRE(width % 8 == 0, KVS_ESHAPE, "embedding width must be a multiple of 8");
     if (n_rows <= 0) return KVS_OK;
     embed_rows_kernel<<<(unsigned)n_rows, 128, 0, (cudaStream_t)stream>>>(
-        (const __nv_bfloat16 *)table, width, ids, rows, (__nv_bfloat16 *)out);
+        (const __nv_bfloat16 *)table, width, ids, rows, (__nv_bfloat16 *)out, out_f32);
     KVS_CHECK_LAUNCH("kvs_embed_rows");
     return KVS_OK;
 }

@@ -41,6 +41,31 @@ from .pool import PAGE_SIZE, CachePool, KVArena
 TILE = 128
 
 
+def h2d(a: np.ndarray, device) -> torch.Tensor:
+    """Host array -> device without a stream sync: staged through the pinned
+    caching host allocator (a pageable cudaMemcpyAsync waits for the stream)."""
+    return torch.from_numpy(np.ascontiguousarray(a)).pin_memory().to(device, non_blocking=True)
+
+
+class _Scratch:
+    """Grow-only named device buffers for per-pass intermediates (residual
+    stream, bf16 GEMM operand, QKV, Q, O).  Reuse is stream-ordered, like the
+    caching allocator's, but sizes never churn, so the hot loop never reaches
+    cudaMalloc."""
+
+    def __init__(self, device):
+        self.device = device
+        self.bufs: dict = {}
+
+    def get(self, name: str, shape, dtype) -> torch.Tensor:
+        numel = int(np.prod(shape))
+        b = self.bufs.get((name, dtype))
+        if b is None or b.numel() < numel:
+            b = torch.empty(max(numel, 1), dtype=dtype, device=self.device)
+            self.bufs[(name, dtype)] = b
+        return b[:numel].view(*shape)
+
+
 def budget(ratio: float, n_reused: int) -> int:
     """selection.py:51-52 with the reference's IEEE-double ceil."""
     return min(math.ceil(ratio * n_reused), n_reused)
@@ -59,19 +84,40 @@ class RowSet:
     tiles: torch.Tensor | None = None   # int32 [3, n_tiles]
     n_tiles: int = 0
 
-    def build_tiles(self, device):
+    def build_tiles(self, device, kv_len=None, partial_first: bool = False):
+        """128-row query tiles, ordered longest-first (LPT) so the CTAs with
+        the most keys start in the first wave and short tiles fill the tail.
+
+        partial_first puts each request's ragged remainder tile at the FRONT
+        (lowest positions, fewest keys) instead of the back (the tile that
+        sees the whole context); only for row sets that are not the probe's
+        aligned key tiles (D1's column-sum pass needs 128-aligned tiles).
+        kv_len (per request, host) estimates a tile's key count when rows are
+        a scattered subset; without it the cost is the row index itself."""
         off = np.asarray(self.row_off, dtype=np.int64)
         cnt = np.diff(off)
         ntile = (cnt + TILE - 1) // TILE
         req = np.repeat(np.arange(len(cnt), dtype=np.int64), ntile)
         first = np.repeat(np.cumsum(ntile) - ntile, ntile)
         k = np.arange(int(ntile.sum()), dtype=np.int64) - first
-        row0 = off[req] + k * TILE
-        rows = np.minimum(TILE, off[req + 1] - row0)
+        if partial_first:
+            rem = cnt[req] - (ntile[req] - 1) * TILE            # rows of the remainder tile
+            row0 = off[req] + np.where(k == 0, 0, rem + (k - 1) * TILE)
+            rows = np.where(k == 0, rem, TILE)
+        else:
+            row0 = off[req] + k * TILE
+            rows = np.minimum(TILE, off[req + 1] - row0)
         self.n_tiles = int(ntile.sum())
-        t = np.stack([req, row0, rows]).astype(np.int32) if self.n_tiles else \
-            np.zeros((3, 1), dtype=np.int32)
-        self.tiles = torch.from_numpy(t).to(device, non_blocking=True)
+        if self.n_tiles:
+            last = row0 + rows - off[req]                          # rows up to the tile's end
+            est = last.astype(np.float64)
+            if kv_len is not None:
+                est = est / np.maximum(cnt[req], 1) * np.asarray(kv_len, np.float64)[req]
+            order = np.argsort(-est, kind="stable")
+            t = np.stack([req[order], row0[order], rows[order]]).astype(np.int32)
+        else:
+            t = np.zeros((3, 1), dtype=np.int32)
+        self.tiles = h2d(t, device)
         return self
 
 
@@ -152,6 +198,8 @@ class Engine:
         self.fetcher = None         # shard.RemoteFetcher when the pool is sharded over GPUs
         self._events: list = []
         self._ev_next = 0
+        self.scratch = _Scratch(self.device)
+        self._xb_of = None
 
     # ------------------------------------------------------------------ helpers
     def reset_timer_events(self, reserve: int = 0):
@@ -194,15 +242,15 @@ class Engine:
             flat = np.concatenate([np.asarray(t, dtype=np.int64) for t in token_lists])
             for t in token_lists:
                 self.model.check_tokens(np.asarray(t, dtype=np.int64))
-            tokens_dev = torch.from_numpy(flat).to(dev, non_blocking=True)
+            tokens_dev = h2d(flat, dev)
         cap = lens + decode_capacity
         pages = [self.arena.alloc(self.arena.pages_for(int(c))) for c in cap]
         maxp = max(len(p) for p in pages)
         bt = np.zeros((len(lens), maxp), dtype=np.int32)
         for r, p in enumerate(pages):
             bt[r, :len(p)] = p
-        req_off = torch.from_numpy(off).to(dev, non_blocking=True)
-        block_table = torch.from_numpy(bt).to(dev, non_blocking=True)
+        req_off = h2d(off, dev)
+        block_table = h2d(bt, dev)
         bc = N.Batch(len(lens), int(off[-1]), req_off.data_ptr(), block_table.data_ptr(), maxp)
         st = BatchState(lens, off, req_off, tokens_dev, pages, block_table, bc, cap)
         st.ctx_len = lens.copy()
@@ -221,7 +269,7 @@ class Engine:
         req = np.repeat(np.arange(len(st.lengths), dtype=np.int32), st.lengths)
         pos = np.concatenate([np.arange(l, dtype=np.int32) for l in st.lengths])
         rs = RowSet(n, torch.arange(n, dtype=torch.int32, device=dev),
-                    torch.from_numpy(req).to(dev), torch.from_numpy(pos).to(dev), None,
+                    h2d(req, dev), h2d(pos, dev), None,
                     st.req_off_host.copy())
         return rs.build_tiles(dev)
 
@@ -248,22 +296,28 @@ class Engine:
                batch_c, self._rope(), q_out.data_ptr(), N.ptr(k_out), N.ptr(v_out),
                N.stream_ptr())
 
-    def _embed(self, tokens_flat, rows: RowSet) -> torch.Tensor:
-        x = torch.empty(rows.n_rows, self.cfg.d_model, dtype=torch.bfloat16, device=self.device)
-        N.call("kvs_embed_rows", self.model.embedding.data_ptr(), self.cfg.d_model,
-               tokens_flat.data_ptr(), rows.row_tok.data_ptr(), rows.n_rows, x.data_ptr(),
-               N.stream_ptr())
-        return x.float()
+    def _embed(self, tokens_flat, rows: RowSet, scratch: bool = False) -> torch.Tensor:
+        """fp32 residual stream of the rows.  scratch=True places it in the
+        engine's reusable buffer (the caller consumes it within the pass)."""
+        n, d = rows.n_rows, self.cfg.d_model
+        xb = self.scratch.get("xb", (n, d), torch.bfloat16)
+        x = self.scratch.get("x", (n, d), torch.float32) if scratch else \
+            torch.empty(n, d, dtype=torch.float32, device=self.device)
+        N.call("kvs_embed_rows", self.model.embedding.data_ptr(), d,
+               tokens_flat.data_ptr(), rows.row_tok.data_ptr(), n, xb.data_ptr(),
+               x.data_ptr(), N.stream_ptr())
+        self._xb_of = (x.data_ptr(), n)     # xb == bf16(x) until x changes
+        return x
 
     def forward_rows(self, x, rows: RowSet, layers, arena_c, batch_c, decode=False,
                      max_kv=0, write_kv_per_layer=None, capture=None):
         """Layer loop over a row set: x (fp32 [n, d_model]) updated in place."""
         cfg, m = self.cfg, self.model
         H, n = cfg.num_heads, rows.n_rows
-        q = torch.empty(n, H, HEAD_DIM, dtype=torch.bfloat16, device=self.device)
-        o = torch.empty_like(q)
+        q = self.scratch.get("q", (n, H, HEAD_DIM), torch.bfloat16)
+        o = self.scratch.get("o", (n, H, HEAD_DIM), torch.bfloat16)
         for layer in layers:
-            qkv = x.to(torch.bfloat16) @ m.w_qkv[layer]
+            qkv = self._qkv(x, layer)
             wk = write_kv_per_layer[layer] if write_kv_per_layer is not None else None
             self._scatter(qkv, rows, layer, arena_c, batch_c, q, write_kv=wk)
             if decode:
@@ -272,11 +326,28 @@ class Engine:
                 self._attention(q, rows, layer, arena_c, batch_c, o)
             if capture is not None:
                 capture.append((layer, q.clone(), o.clone()))
-            # residual add fused into the cuBLAS epilogue (fp32 C/D, bf16 A/B)
-            x = torch.addmm(x, o.view(n, H * HEAD_DIM), m.w_o[layer], out_dtype=torch.float32)
+            self._out_proj(x, o, layer)
             if capture is not None:
                 capture.append((layer, "hidden", x.clone()))
         return x
+
+    def _qkv(self, x: torch.Tensor, layer: int) -> torch.Tensor:
+        """bf16(x) @ W_qkv into scratch (model.py:193-195)."""
+        n = x.shape[0]
+        w = self.model.w_qkv[layer]
+        xb = self.scratch.get("xb", (n, x.shape[1]), torch.bfloat16)
+        if self._xb_of != (x.data_ptr(), n):
+            xb.copy_(x)
+            self._xb_of = (x.data_ptr(), n)
+        qkv = self.scratch.get("qkv", (n, w.shape[1]), torch.bfloat16)
+        return torch.matmul(xb, w, out=qkv)
+
+    def _out_proj(self, x: torch.Tensor, o: torch.Tensor, layer: int) -> None:
+        """x += merge(o) @ W_o in place (model.py:202): the residual add runs in
+        the cuBLAS epilogue with C = D = x (fp32), A/B bf16 - no copy of x."""
+        n = x.shape[0]
+        torch.addmm(x, o.view(n, -1), self.model.w_o[layer], out_dtype=torch.float32, out=x)
+        self._xb_of = None
 
     # ------------------------------------------------------------------ prefill
     def lookup(self, st: BatchState):
@@ -308,7 +379,7 @@ class Engine:
         H, G = cfg.num_heads, cfg.kv_heads
         rows = self._rows_all(st)
         n = rows.n_rows
-        x = self._embed(st.tokens, rows)
+        x = self._embed(st.tokens, rows, scratch=True)
         p = self.probe_layer
         if p == 1:
             npages = int(sum((l + PAGE_SIZE - 1) // PAGE_SIZE for l in st.lengths))
@@ -319,17 +390,17 @@ class Engine:
                 k = (l + PAGE_SIZE - 1) // PAGE_SIZE
                 bt[r, :k] = np.arange(base, base + k)
                 base += k
-            pbt = torch.from_numpy(bt).to(dev, non_blocking=True)
+            pbt = h2d(bt, dev)
             pbatch = N.Batch(st.batch_c.n_req, st.batch_c.n_total, st.req_off.data_ptr(),
                              pbt.data_ptr(), bt.shape[1])
-            q = torch.empty(n, H, HEAD_DIM, dtype=torch.bfloat16, device=dev)
-            o = torch.empty_like(q)
-            qkv = x.to(torch.bfloat16) @ m.w_qkv[0]
+            q = self.scratch.get("q", (n, H, HEAD_DIM), torch.bfloat16)
+            o = self.scratch.get("o", (n, H, HEAD_DIM), torch.bfloat16)
+            qkv = self._qkv(x, 0)
             self._scatter(qkv, rows, 0, parena, pbatch, q, use_write=False)
             self._attention(q, rows, 0, parena, pbatch, o)
-            x = torch.addmm(x, o.view(n, H * HEAD_DIM), m.w_o[0], out_dtype=torch.float32)
+            self._out_proj(x, o, 0)
             st._probe_keep = pbt
-        qkv = x.to(torch.bfloat16) @ m.w_qkv[p]
+        qkv = self._qkv(x, p)
         q1 = torch.empty(n, H, HEAD_DIM, dtype=torch.bfloat16, device=dev)
         v_true = torch.empty(n, G, HEAD_DIM, dtype=torch.bfloat16, device=dev)
         wk = (st.src_slot < 0).to(torch.uint8) if write_k else \
@@ -340,7 +411,7 @@ class Engine:
     def _select(self, st: BatchState, v_true, alpha, budgets):
         dev, n = self.device, int(st.req_off_host[-1])
         bud = budgets if torch.is_tensor(budgets) else \
-            torch.from_numpy(np.asarray(budgets, dtype=np.int32)).to(dev, non_blocking=True)
+            h2d(np.asarray(budgets, dtype=np.int32), dev)
         dv = torch.empty(n, dtype=torch.float32, device=dev)
         score = torch.empty(n, dtype=torch.float32, device=dev)
         sel = torch.empty(n, dtype=torch.uint8, device=dev)
@@ -389,7 +460,7 @@ class Engine:
         off = np.zeros(R + 1, dtype=np.int64)
         off[1:] = np.cumsum(c)
         n = int(off[-1])
-        row_off = torch.from_numpy(off).to(dev)
+        row_off = h2d(off, dev)
         rows = RowSet(n, torch.empty(n, dtype=torch.int32, device=dev),
                       torch.empty(n, dtype=torch.int32, device=dev),
                       torch.empty(n, dtype=torch.int32, device=dev),
@@ -398,16 +469,15 @@ class Engine:
                None, row_off.data_ptr(), rows.row_tok.data_ptr(), rows.row_req.data_ptr(),
                rows.row_pos.data_ptr(), rows.write_kv.data_ptr(), N.stream_ptr())
         rows._keep = (row_off, src)
-        return rows.build_tiles(dev)
+        return rows.build_tiles(dev, kv_len=st.lengths, partial_first=True)
 
     def session_forward(self, st: BatchState, rows: RowSet, capture=None):
-        x = self._embed(st.tokens, rows)
+        x = self._embed(st.tokens, rows, scratch=capture is None)
         x = self.forward_rows(x, rows, range(self.cfg.num_layers), self.arena.c, st.batch_c,
                               capture=capture)
-        last = torch.from_numpy(rows.row_off[1:] - 1).to(self.device)
+        last = h2d(rows.row_off[1:] - 1, self.device)
         st.rows = rows
         st.hidden_last = x[last]
-        st._x_rows = x
         return x
 
     def prefill_batch(self, token_lists, ratio: float = 0.2, mode: str = "selective",

@@ -109,3 +109,24 @@ def test_select_decode_step_vs_oracle(H, G, n):
     want, scores = O.select_decode_step(q_t, k, dv, elig, 3, group=H // G)
     assert_scores_close(res.scores, scores)
     assert_selection_tie_band(res.indices, want, scores, 3)
+
+
+@pytest.mark.parametrize("n", [1000, 4096, 5000, 20000, 60000])
+def test_select_exact_ties_large(n):
+    """D2 top-B with massive exact score ties at sizes that take the register
+    (<= 4096), shared-memory (<= 47104) and global key paths: uniform
+    attention (q = 0, non-causal) makes every alpha identical, and dv rows
+    drawn from three values make whole tie bands; the device must pick
+    exactly the (-score, position) order of selection.py:63-66."""
+    import paper_2503_16525_b200 as K
+    rng = np.random.default_rng(n)
+    d = 8
+    q = np.zeros((1, n, d))
+    k = _rand(rng, (1, n, d))
+    dv = np.repeat(rng.choice([0.0, 0.5, 1.0], size=n)[None, :, None], d, axis=2)
+    reused = sorted(rng.choice(n, size=n // 2, replace=False).tolist())
+    cfg = K.SelectionConfig(ratio=0.3)
+    res = K.select_prefill(q, k, dv, reused, cfg, causal=False)
+    s = np.asarray(res.scores)
+    want = sorted(sorted(reused, key=lambda i: (-s[i], i))[:cfg.budget(len(reused))])
+    assert list(res.indices) == want

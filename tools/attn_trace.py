@@ -55,6 +55,24 @@ t0 = ev[0, 0]
 names = {10: "mma:V ready", 11: "mma:p_full a -> PV_a", 12: "mma:p_full b -> PV_b",
          13: "mma:QK_a issue", 14: "mma:QK_b issue", 20: "smx a: S ready", 21: "smx a: S loaded",
          22: "smx a: P stored", 30: "smx b: S ready", 31: "smx b: S loaded", 32: "smx b: P stored"}
-print("last tile (n_kb = 32), head pair 0")
+print("longest tile (n_kb = 32), head pair 0; clock64 cycles")
+T = {}
 for t, tag in ev:
+    T.setdefault((int(tag >> 32), int(tag & 0xffffffff)), int(t - t0))
+for t, tag in ev[:60]:
     print(f"{t - t0:8d}  kb={tag & 0xffffffff:3d}  {names.get(int(tag >> 32), tag >> 32)}")
+kbs = sorted({kb for (_, kb) in T})
+mid = [kb for kb in kbs if 4 <= kb <= kbs[-1] - 4]
+def avg(f):
+    v = [f(kb) for kb in mid]
+    v = [x for x in v if x is not None]
+    return sum(v) / max(len(v), 1)
+g = lambda a, kb: T.get((a, kb))
+def d(a, ka, b, kb_):
+    return lambda kb: (g(b, kb + kb_) - g(a, kb + ka)) if g(b, kb + kb_) is not None and g(a, kb + ka) is not None else None
+print(f"period per kb (S ready a -> next S ready a): {avg(d(20, 0, 20, 1)):.0f}")
+print(f"softmax a: S ready -> S loaded {avg(d(20, 0, 21, 0)):.0f}, S loaded -> P stored {avg(d(21, 0, 22, 0)):.0f}, P stored -> next S ready {avg(d(22, 0, 20, 1)):.0f}")
+print(f"softmax b: S ready -> S loaded {avg(d(30, 0, 31, 0)):.0f}, S loaded -> P stored {avg(d(31, 0, 32, 0)):.0f}, P stored -> next S ready {avg(d(32, 0, 30, 1)):.0f}")
+print(f"P stored a -> mma sees p_full a {avg(d(22, 0, 11, 0)):.0f}; p_full a -> QK_a issue {avg(d(11, 0, 13, 0)):.0f}; QK_a issue -> S ready a(kb+1) {avg(d(13, 0, 20, 1)):.0f}")
+print(f"P stored b -> mma sees p_full b {avg(d(32, 0, 12, 0)):.0f}; p_full b -> QK_b issue {avg(d(12, 0, 14, 0)):.0f}; QK_b issue -> S ready b(kb+1) {avg(d(14, 0, 30, 1)):.0f}")
+print(f"softmax a start vs b start offset: {avg(d(20, 0, 30, 0)):.0f}")
