@@ -310,6 +310,18 @@ def run_gpu(args, rank, world, device):
     return res
 
 
+def ncu_traffic(kernel: str):
+    """DRAM bytes per launch of `kernel` from the committed ncu capture
+    (profiles/r1_ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")) as fh:
+            k = json.load(fh)["kernels"][kernel]
+        return {"dram_bytes_per_launch": k["dram_bytes"], "launch": k["launch"],
+                "source": "profiles/r1_ncu_traffic.json"}
+    except (OSError, KeyError, ValueError):
+        return None
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -372,7 +384,8 @@ def main():
     att_tflops = c["attention_flops"] / (att_ms / 1000.0) / 1e12 if att_ms == att_ms else None
     roof = {"kernel": "kvs_attention_fwd (A1 selective-recompute attention, tcgen05)",
             "bound": "tensor", "achieved": att_tflops, "peak": tflops_sus, "unit": "TFLOP/s",
-            "frac": att_tflops / tflops_sus if att_tflops else None, "traffic": None,
+            "frac": att_tflops / tflops_sus if att_tflops else None,
+            "traffic": ncu_traffic("kvs_attention_fwd"),
             "peak_kind": f"{kind} bf16 sustained (kernel timed inside a long step)",
             "ms_per_step": att_ms, "share_of_step": att_ms / ms_per_step,
             "launches_per_step": res["n_launch_attention"]}
@@ -380,7 +393,9 @@ def main():
     if "dhd_select" in kern:
         gbs = c["select_bytes"] / (kern["dhd_select"] / 1000.0) / 1e9
         extra["dhd_select"] = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
-                               "frac": gbs / hbm, "ms_per_step": kern["dhd_select"]}
+                               "frac": gbs / hbm, "ms_per_step": kern["dhd_select"],
+                               "algorithmic_bytes": c["select_bytes"],
+                               "traffic": ncu_traffic("kvs_dhd_select")}
     if "dhd_alpha" in kern:
         tf = c["alpha_flops"] / (kern["dhd_alpha"] / 1000.0) / 1e12
         extra["dhd_alpha"] = {"bound": "tensor", "achieved": tf, "peak": tflops_sus,

@@ -109,6 +109,17 @@ kvs_status kvs_pool_lookup(const kvs_token_index *index, const int64_t *req_toke
  * page p, layer l, kv (0 = K, 1 = V), row r (< page_size), head g, dim i at
  * element ((((p * L + l) * 2 + kv) * page_size + r) * kv_heads + g) * head_dim + i.
  * K is stored post-RoPE at the owning sequence's positions.                */
+/* F5 fixed-chunk baseline lookup (reference pool.py:125-161 with fixed_chunk,
+ * matching.py:171-194): per request, chunk-aligned blocks of `chunk` tokens
+ * (the trailing partial block never matches) claimed by the newest entry
+ * holding the identical block at a chunk-aligned offset (first offset wins).
+ * Same outputs as kvs_pool_lookup; max_len bounds the request lengths.     */
+kvs_status kvs_fixed_chunk_lookup(const kvs_token_index *index, const int64_t *req_tokens,
+                                  const int64_t *req_off, int32_t n_req, int64_t max_len,
+                                  int32_t chunk, int32_t *src_slot, int32_t *src_cand,
+                                  int32_t *n_hit, uint8_t *contributed, int64_t n_total,
+                                  kvs_stream_t stream);
+
 typedef struct {
     void *base;
     int64_t num_pages;
@@ -154,6 +165,16 @@ kvs_status kvs_pack_rows(const kvs_kv_arena *arena, const int32_t *slot, const i
 kvs_status kvs_unpack_rows(const kvs_kv_arena *arena, const kvs_batch *batch,
                            const int64_t *flat_t, const int32_t *cand, int64_t n_rows,
                            const void *in, const kvs_rope *rope, kvs_stream_t stream);
+
+/* F3/F1 pool-entry transfer (reference pool.py:100-123, 174-241): an entry's
+ * K and V as dense fp32 [num_layers][n_tokens][kv_heads][d_k] - the KVSH file
+ * order - to (import) or from (export) its arena pages (pages[i] holds tokens
+ * [i*page_size, (i+1)*page_size)).  Import rounds to bf16 (RNE) and zeroes
+ * the padded head lanes; export is exact.  k/v are device pointers.        */
+kvs_status kvs_entry_import(const kvs_kv_arena *arena, const int32_t *pages, int64_t n_tokens,
+                            int32_t d_k, const float *k, const float *v, kvs_stream_t stream);
+kvs_status kvs_entry_export(const kvs_kv_arena *arena, const int32_t *pages, int64_t n_tokens,
+                            int32_t d_k, float *k, float *v, kvs_stream_t stream);
 
 /* Post-GEMM step for a set of query rows: qkv[row] = [q (H*d) | k (kvh*d) | v (kvh*d)]
  * bf16.  Rotates q,k by position (rope nullable), writes q to q_out[row][H][d],

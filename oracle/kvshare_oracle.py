@@ -126,6 +126,33 @@ def pool_lookup(entries_newest_first, request, w: int = 8, b: int = 31,
     return se[:n], sc[:n], contrib[:len(toks)].astype(bool)
 
 
+def fixed_chunk_lookup(entries_newest_first, request, chunk: int):
+    """pool.py:139-159 with fixed_chunk -> matching.py:171-194, restated.
+    Entries are visited newest first; each entry's fixed_chunk_match claims
+    the still-unclaimed target chunks [i*c, (i+1)*c) for which the identical
+    block sits at an aligned candidate offset j*c (first j wins; trailing
+    partial chunks never match).  Returns (src_entry[n], src_cand[n],
+    contributed[E]) like pool_lookup."""
+    req = np.asarray(request, dtype=np.int64)
+    n, c = req.size, int(chunk)
+    se = np.full(n, -1, dtype=np.int32)
+    sc = np.full(n, -1, dtype=np.int32)
+    contrib = np.zeros(len(entries_newest_first), dtype=bool)
+    for e, ent in enumerate(entries_newest_first):
+        cand = np.asarray(ent, dtype=np.int64)
+        blocks = [(j, cand[j:j + c]) for j in range(0, cand.size - c + 1, c)]
+        for i in range(0, n - c + 1, c):
+            for j, blk in blocks:
+                if np.array_equal(req[i:i + c], blk):
+                    if (se[i:i + c] < 0).any():
+                        free = se[i:i + c] < 0
+                        se[i:i + c][free] = e
+                        sc[i:i + c][free] = np.arange(j, j + c)[free]
+                        contrib[e] = True
+                    break
+    return se, sc, contrib
+
+
 def hit_rate(n: int, n_hit: int) -> float:
     """matching.py:197-205 / pool.py:65-67."""
     return n_hit / n if n else 0.0

@@ -13,7 +13,7 @@ import torch
 from .errors import STATUS_ERRORS, DeviceError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libkvshare.so")
+LIB_PATH = os.environ.get("KVS_LIB") or os.path.join(_PKG, "libkvshare.so")   # KVS_LIB: experiment builds
 
 c_i32, c_i64, c_u64, c_f32 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64, ctypes.c_float
 c_size, c_vp = ctypes.c_size_t, ctypes.c_void_p
@@ -51,6 +51,10 @@ _SIGS = {
     "kvs_gather_kv": [P(KVArena), P(Batch), c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, P(Rope), c_vp],
     "kvs_qkv_rope_scatter": [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_i32, P(KVArena), P(Batch),
                              P(Rope), c_vp, c_vp, c_vp, c_vp],
+    "kvs_fixed_chunk_lookup": [P(TokenIndex), c_vp, c_vp, c_i32, c_i64, c_i32, c_vp, c_vp, c_vp,
+                               c_vp, c_i64, c_vp],
+    "kvs_entry_import": [P(KVArena), c_vp, c_i64, c_i32, c_vp, c_vp, c_vp],
+    "kvs_entry_export": [P(KVArena), c_vp, c_i64, c_i32, c_vp, c_vp, c_vp],
     "kvs_embed_rows": [c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp],
     "kvs_pack_rows": [P(KVArena), c_vp, c_vp, c_i64, c_vp, c_i32, c_vp, c_vp],
     "kvs_unpack_rows": [P(KVArena), P(Batch), c_vp, c_vp, c_i64, c_vp, P(Rope), c_vp],

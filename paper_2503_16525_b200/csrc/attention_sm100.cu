@@ -26,17 +26,13 @@ namespace attn {
 // Diagnostic timeline (KVS_ATTN_TRACE builds only): clock64 stamps of the
 // first CTA's pipeline events, read back with kvs_attn_trace_dump().
 #ifdef KVS_ATTN_TRACE
-__device__ long long g_trace[8192];
-__device__ int g_trace_n;
+// one slot per (tag < 64, kb < 256): a plain store, no atomics, so tracing
+// barely perturbs the pipeline it measures
+__device__ long long g_trace[64 * 256];
 #define TRACE(tag, kb)                                                              \
     do {                                                                            \
-        if (blockIdx.y == 0 && blockIdx.x == 0) {                                   \
-            int _i = atomicAdd(&g_trace_n, 1);                                      \
-            if (_i < 4096) {                                                        \
-                g_trace[2 * _i] = clock64();                                        \
-                g_trace[2 * _i + 1] = ((long long)(tag) << 32) | (unsigned)(kb);    \
-            }                                                                       \
-        }                                                                           \
+        if (blockIdx.y == 0 && blockIdx.x == 0 && (kb) < 256)                       \
+            g_trace[(tag) * 256 + (kb)] = clock64();                                \
     } while (0)
 #else
 #define TRACE(tag, kb) do {} while (0)
@@ -587,6 +583,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
 // makes QK_t(kb+1) overwrite S/P only after PV_t(kb) has read P, and each
 // head's softmax overlaps the other head's two MMAs.
 constexpr int RING3 = 5;
+#ifndef KVS_POLY_EVERY
+#define KVS_POLY_EVERY 0
+#endif
+constexpr int kPolyEvery = KVS_POLY_EVERY;   // 1 in kPolyEvery exp2 pairs emulated (0: none)
 
 struct Smem3 {
     uint64_t q_full;
@@ -774,8 +774,12 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 uint32_t pk[32];
 #pragma unroll
                 for (int q = 0; q < 32; ++q) {
-                    const float e0 = fast_exp2(fmaf(s[hf * 64 + 2 * q], p.scale_log2, -mu));
-                    const float e1 = fast_exp2(fmaf(s[hf * 64 + 2 * q + 1], p.scale_log2, -mu));
+                    const float x0 = fmaf(s[hf * 64 + 2 * q], p.scale_log2, -mu);
+                    const float x1 = fmaf(s[hf * 64 + 2 * q + 1], p.scale_log2, -mu);
+                    // every kPolyEvery-th pair on the FMA pipe, the rest on MUFU
+                    const bool poly = kPolyEvery > 0 && q % (kPolyEvery > 0 ? kPolyEvery : 1) == kPolyEvery - 1;
+                    const float e0 = poly ? exp2_poly(x0) : fast_exp2(x0);
+                    const float e1 = poly ? exp2_poly(x1) : fast_exp2(x1);
                     ls[(2 * q) & 7] += e0;
                     ls[(2 * q + 1) & 7] += e1;
                     pk[q] = pack_bf16x2(e0, e1);
@@ -1327,13 +1331,17 @@ kvs_status kvs_attention_fwd(const void *q, const int32_t *row_pos, int64_t n_ro
 
 int32_t kvs_attn_trace_dump(int64_t *host, int32_t max_pairs) {
 #ifdef KVS_ATTN_TRACE
+    static long long buf[64 * 256];
+    cudaMemcpyFromSymbol(buf, attn::g_trace, sizeof(buf));
     int n = 0;
-    cudaMemcpyFromSymbol(&n, attn::g_trace_n, sizeof(int));
-    if (n > max_pairs) n = max_pairs;
-    if (n > 4096) n = 4096;
-    cudaMemcpyFromSymbol(host, attn::g_trace, sizeof(long long) * 2 * n);
-    int zero = 0;
-    cudaMemcpyToSymbol(attn::g_trace_n, &zero, sizeof(int));
+    for (int i = 0; i < 64 * 256 && n < max_pairs; ++i)
+        if (buf[i] != 0) {
+            host[2 * n] = buf[i];
+            host[2 * n + 1] = ((long long)(i / 256) << 32) | (i % 256);
+            ++n;
+        }
+    static long long zero[64 * 256];
+    cudaMemcpyToSymbol(attn::g_trace, zero, sizeof(zero));
     return n;
 #else
     (void)host;

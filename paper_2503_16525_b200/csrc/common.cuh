@@ -54,6 +54,19 @@ __device__ __forceinline__ float fast_exp2(float x) {
     return y;
 }
 
+// 2^x on the FMA pipe (no MUFU): round-to-nearest split x = j + f with the
+// 1.5*2^23 magic add, cubic minimax for 2^f on [-0.5, 0.5] (relative error
+// 7.5e-5, far below the bf16 rounding of P), exponent add for 2^j.  Used for
+// a fraction of the softmax exponentials so MUFU and FMA pipes share the load.
+__device__ __forceinline__ float exp2_poly(float x) {
+    x = fmaxf(x, -126.f);
+    const float t = x + 12582912.f;
+    const float f = x - (t - 12582912.f);
+    const float p = fmaf(fmaf(fmaf(0.0551716685f, f, 0.242611155f), f, 0.693260968f), f,
+                         0.999928057f);
+    return __int_as_float(__float_as_int(p) + (__float_as_int(t) << 23));
+}
+
 // ---------------------------------------------------------------- smem / mbarrier
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));

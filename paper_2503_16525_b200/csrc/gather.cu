@@ -326,6 +326,38 @@ __global__ void __launch_bounds__(128) unpack_rows_kernel(
 
 using namespace kvs;
 
+// F3/F1 entry transfer (reference pool.py:100-123 insert, :174-241 KVSH
+// save/load): an entry's K/V as dense fp32 [layer][token][kv_head][d_k] (the
+// KVSH file order) <-> its arena pages (bf16, head dims in padded lanes:
+// first half -> [0, d/2), second half -> [64, 64 + d/2)).  One CTA per
+// (layer, token) row; both K and V.  Import rounds to bf16 (RNE) and zeroes
+// the padding lanes; export widens exactly.
+template <bool kImport>
+__global__ void __launch_bounds__(128) entry_rows_kernel(Arena A, const int32_t *__restrict__ pages,
+                                                         int64_t n, int32_t d_k, float *__restrict__ k,
+                                                         float *__restrict__ v) {
+    const int64_t row = blockIdx.x;                 // layer * n + token
+    const int layer = (int)(row / n);
+    const int64_t tok = row % n;
+    const int64_t page = pages[tok / A.P];
+    const int G = A.G;
+    for (int kv = 0; kv < 2; ++kv) {
+        __nv_bfloat16 *dst = A.row(page, layer, kv, (int)(tok % A.P));
+        float *x = (kv == 0 ? k : v) + row * (int64_t)G * d_k;
+        for (int e = threadIdx.x; e < G * A.D; e += blockDim.x) {
+            const int g = e / A.D, lane = e % A.D;
+            // which model dim sits in this lane (-1: padding)
+            const int half = d_k / 2;
+            const int d = lane < half ? lane : (lane >= 64 && lane < 64 + half ? half + lane - 64 : -1);
+            if (kImport) {
+                dst[e] = d >= 0 ? __float2bfloat16_rn(x[g * d_k + d]) : __float2bfloat16_rn(0.f);
+            } else if (d >= 0) {
+                x[g * d_k + d] = __bfloat162float(dst[e]);
+            }
+        }
+    }
+}
+
 extern "C" {
 
 kvs_status kvs_gather_kv(const kvs_kv_arena *arena, const kvs_batch *batch,
@@ -410,6 +442,31 @@ kvs_status kvs_unpack_rows(const kvs_kv_arena *arena, const kvs_batch *batch,
         make_arena(arena), batch->req_off, batch->n_req, batch->block_table, batch->max_pages,
         flat_t, cand, (const uint4 *)in, rope ? rope->cos : nullptr, rope ? rope->sin : nullptr);
     KVS_CHECK_LAUNCH("kvs_unpack_rows");
+    return KVS_OK;
+}
+
+kvs_status kvs_entry_import(const kvs_kv_arena *arena, const int32_t *pages, int64_t n_tokens,
+                            int32_t d_k, const float *k, const float *v, kvs_stream_t stream) {
+    KVS_REQUIRE(arena != nullptr && pages != nullptr, KVS_EPARAM, "null arena/pages");
+    KVS_REQUIRE(d_k >= 2 && d_k % 2 == 0 && d_k <= arena->head_dim, KVS_ESHAPE,
+                "d_k must be even and <= head_dim");
+    if (n_tokens <= 0) return KVS_OK;
+    entry_rows_kernel<true><<<(unsigned)(n_tokens * arena->num_layers), 128, 0,
+                              (cudaStream_t)stream>>>(make_arena(arena), pages, n_tokens, d_k,
+                                                      const_cast<float *>(k), const_cast<float *>(v));
+    KVS_CHECK_LAUNCH("kvs_entry_import");
+    return KVS_OK;
+}
+
+kvs_status kvs_entry_export(const kvs_kv_arena *arena, const int32_t *pages, int64_t n_tokens,
+                            int32_t d_k, float *k, float *v, kvs_stream_t stream) {
+    KVS_REQUIRE(arena != nullptr && pages != nullptr, KVS_EPARAM, "null arena/pages");
+    KVS_REQUIRE(d_k >= 2 && d_k % 2 == 0 && d_k <= arena->head_dim, KVS_ESHAPE,
+                "d_k must be even and <= head_dim");
+    if (n_tokens <= 0) return KVS_OK;
+    entry_rows_kernel<false><<<(unsigned)(n_tokens * arena->num_layers), 128, 0,
+                               (cudaStream_t)stream>>>(make_arena(arena), pages, n_tokens, d_k, k, v);
+    KVS_CHECK_LAUNCH("kvs_entry_export");
     return KVS_OK;
 }
 

@@ -263,6 +263,48 @@ static kvs_status check_hash_params(int32_t w, uint64_t b, uint64_t m) {
 
 using namespace kvs;
 
+// F5 fixed-chunk baseline (reference pool.py:139-159 with fixed_chunk ->
+// matching.py:171-194): target chunk i (positions [i*c, (i+1)*c), trailing
+// partial chunk never matches) is claimed by the newest entry holding the
+// identical block at a chunk-aligned offset, at the first such offset.  One
+// warp per (request, chunk): entries in recency order, aligned candidate
+// chunks ascending, lanes compare the block 32 tokens at a time.
+__global__ void __launch_bounds__(128) fixed_chunk_kernel(
+    kvs_token_index idx, const int64_t *__restrict__ tok, const int64_t *__restrict__ req_off,
+    int32_t c, int32_t *__restrict__ src_slot, int32_t *__restrict__ src_cand,
+    int32_t *__restrict__ n_hit, uint8_t *__restrict__ contributed) {
+    const int lane = threadIdx.x & 31;
+    const int r = blockIdx.y;
+    const int64_t chunk = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    const int64_t s0 = req_off[r], n = req_off[r + 1] - s0;
+    if ((chunk + 1) * c > n) return;
+    const int64_t *blk = tok + s0 + chunk * c;
+    for (int rank = 0; rank < idx.n_slots; ++rank) {
+        const int32_t slot = idx.rank2slot[rank];
+        if (idx.slot_rank[slot] != rank) break;          // past the live entries
+        const int64_t e0 = idx.tok_off[slot], ne = idx.tok_off[slot + 1] - e0;
+        for (int64_t j = 0; j + c <= ne; j += c) {
+            bool eq = true;
+            for (int k0 = 0; k0 < c && eq; k0 += 32) {
+                const int k = k0 + lane;
+                const bool ok = k >= c || blk[k] == idx.tokens[e0 + j + k];
+                eq = __all_sync(0xffffffffu, ok);
+            }
+            if (eq) {
+                for (int k = lane; k < c; k += 32) {
+                    src_slot[s0 + chunk * c + k] = slot;
+                    src_cand[s0 + chunk * c + k] = (int32_t)(j + k);
+                }
+                if (lane == 0) {
+                    atomicAdd(&n_hit[r], c);
+                    if (contributed) contributed[(int64_t)r * idx.n_slots + slot] = 1;
+                }
+                return;
+            }
+        }
+    }
+}
+
 extern "C" {
 
 kvs_status kvs_window_hashes(const int64_t *tokens, int64_t n, int32_t w, uint64_t b, uint64_t m,
@@ -418,6 +460,30 @@ kvs_status kvs_pool_lookup(const kvs_token_index *index, const int64_t *req_toke
                                                           index->rank2slot, index->n_slots,
                                                           src_slot, src_cand, n_hit, contributed);
     KVS_CHECK_LAUNCH("kvs_pool_lookup");
+    return KVS_OK;
+}
+
+kvs_status kvs_fixed_chunk_lookup(const kvs_token_index *index, const int64_t *req_tokens,
+                                  const int64_t *req_off, int32_t n_req, int64_t max_len,
+                                  int32_t chunk, int32_t *src_slot, int32_t *src_cand,
+                                  int32_t *n_hit, uint8_t *contributed, int64_t n_total,
+                                  kvs_stream_t stream) {
+    KVS_REQUIRE(index != nullptr, KVS_EPARAM, "null index");
+    KVS_REQUIRE(chunk >= 1, KVS_EPARAM, "chunk_size must be >= 1, got %d", chunk);
+    KVS_REQUIRE(n_req >= 1 && n_req <= 65535, KVS_EPARAM, "n_req must be in [1, 65535]");
+    cudaStream_t s = (cudaStream_t)stream;
+    cudaMemsetAsync(n_hit, 0, sizeof(int32_t) * n_req, s);
+    if (contributed && index->n_slots > 0)
+        cudaMemsetAsync(contributed, 0, (size_t)n_req * index->n_slots, s);
+    if (n_total <= 0) return KVS_OK;
+    cudaMemsetAsync(src_slot, 0xFF, sizeof(int32_t) * n_total, s);     // -1: miss
+    cudaMemsetAsync(src_cand, 0xFF, sizeof(int32_t) * n_total, s);
+    const int64_t chunks = max_len / chunk;
+    if (chunks > 0 && index->n_slots > 0) {
+        fixed_chunk_kernel<<<dim3((unsigned)((chunks + 3) / 4), n_req), 128, 0, s>>>(
+            *index, req_tokens, req_off, chunk, src_slot, src_cand, n_hit, contributed);
+    }
+    KVS_CHECK_LAUNCH("kvs_fixed_chunk_lookup");
     return KVS_OK;
 }
 

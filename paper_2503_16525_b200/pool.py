@@ -14,17 +14,20 @@ behaviour.  What changes is where things live:
 """
 from __future__ import annotations
 
+import struct
 from dataclasses import dataclass, field
 
 import numpy as np
 import torch
 
 from . import _native as N
-from .errors import CacheError, ParameterError
+from .errors import CacheError, FormatError, ParameterError
 from .matching import HashParams, window_hashes_device
 from .model import HEAD_DIM, ModelConfig
 
 PAGE_SIZE = 64
+_MAGIC = b"KVSH"          # pool file format of reference pool.py:8-17
+_VERSION = 1
 
 
 class KVArena:
@@ -96,14 +99,20 @@ class KVEntry:
         return (4 + len(self.request_id.encode()) + 4 + 4 * self.n_tokens + 12
                 + 2 * 4 * cfg.num_layers * cfg.kv_heads * self.n_tokens * cfg.d_k)
 
+    def export_f32(self) -> tuple[torch.Tensor, torch.Tensor]:
+        """Device fp32 K and V in KVSH order [L][n][kv_heads][d_k] (F3 kernel)."""
+        cfg, dev = self.pool.config, self.pool.device
+        shape = (cfg.num_layers, self.n_tokens, cfg.kv_heads, cfg.d_k)
+        k = torch.empty(shape, dtype=torch.float32, device=dev)
+        v = torch.empty(shape, dtype=torch.float32, device=dev)
+        pages = torch.as_tensor(np.asarray(self.pages, dtype=np.int32), device=dev)
+        N.call("kvs_entry_export", self.pool.arena.c, pages.data_ptr(), self.n_tokens, cfg.d_k,
+               k.data_ptr(), v.data_ptr(), N.stream_ptr())
+        return k, v
+
     def _kv(self, kv: int) -> np.ndarray:
-        arena, cfg = self.pool.arena, self.pool.config
-        out = []
-        for layer in range(cfg.num_layers):
-            rows = arena.rows(self.pages, self.n_tokens, layer, kv)   # [n, G, 128]
-            rows = rows[..., torch.as_tensor(self.pool.pad_index, device=rows.device)]
-            out.append(rows.float().permute(1, 0, 2).cpu().numpy())
-        return np.stack(out).astype(np.float64)                      # (L, G, n, d_k)
+        x = self.export_f32()[kv]                                     # L, n, G, d_k
+        return x.permute(0, 2, 1, 3).double().cpu().numpy()          # (L, G, n, d_k)
 
     @property
     def k(self) -> np.ndarray:
@@ -266,18 +275,99 @@ class CachePool:
         self.insert_pages(request_id, tokens, pages)
 
     def write_rows(self, pages, k: torch.Tensor, v: torch.Tensor) -> None:
-        """Copy (L, G, n, d_k) K/V into pages (padded lanes, bf16)."""
-        cfg, P = self.config, self.arena.page_size
-        n = k.shape[2]
-        pidx = torch.as_tensor(self.pad_index, device=self.device)
-        for kv, x in ((0, k), (1, v)):
-            x = x.to(self.device, torch.float32).permute(0, 2, 1, 3)   # L, n, G, d
-            full = torch.zeros(cfg.num_layers, len(pages) * P, cfg.kv_heads, HEAD_DIM,
-                               device=self.device)
-            full[:, :n][..., pidx] = x
-            full = full.reshape(cfg.num_layers, len(pages), P, cfg.kv_heads, HEAD_DIM)
-            pt = torch.as_tensor(list(pages), device=self.device, dtype=torch.long)
-            self.arena.data[pt, :, kv] = full.permute(1, 0, 2, 3, 4).to(torch.bfloat16)
+        """Copy (L, G, n, d_k) K/V into pages (bf16, padded lanes) with the F3
+        import kernel."""
+        dev = self.device
+        kf = k.to(dev, torch.float32).permute(0, 2, 1, 3).contiguous()     # L, n, G, d_k
+        vf = v.to(dev, torch.float32).permute(0, 2, 1, 3).contiguous()
+        self._import(pages, kf, vf)
+
+    def _import(self, pages, k_lnhd: torch.Tensor, v_lnhd: torch.Tensor) -> None:
+        pg = torch.as_tensor(np.asarray(list(pages), dtype=np.int32), device=self.device)
+        N.call("kvs_entry_import", self.arena.c, pg.data_ptr(), k_lnhd.shape[1],
+               self.config.d_k, k_lnhd.data_ptr(), v_lnhd.data_ptr(), N.stream_ptr())
+
+    # ------------------------------------------------------------------ KVSH file
+    def save(self, path) -> None:
+        """pool.py:174-189: entries in insertion order, K/V as little-endian
+        f32 [layer][token][head][dim].  Heads are the pool's kv_heads (the
+        reference's num_heads for a multi-head model).  Each entry's rows
+        leave the arena through the export kernel, one D2H copy per entry."""
+        cfg = self.config
+        with open(path, "wb") as fh:
+            fh.write(_MAGIC)
+            fh.write(struct.pack("<I", _VERSION))
+            fh.write(struct.pack("<Q", len(self.entries)))
+            for entry in self.entries.values():
+                ident = entry.request_id.encode()
+                fh.write(struct.pack("<I", len(ident)))
+                fh.write(ident)
+                fh.write(struct.pack("<I", entry.n_tokens))
+                fh.write(entry.tokens.astype("<u4").tobytes())
+                fh.write(struct.pack("<III", cfg.num_layers, cfg.kv_heads, cfg.d_k))
+                if entry.owner >= 0:
+                    raise CacheError(f"entry {entry.request_id!r} lives on GPU {entry.owner}")
+                k, v = entry.export_f32()
+                fh.write(k.cpu().numpy().astype("<f4").tobytes())
+                fh.write(v.cpu().numpy().astype("<f4").tobytes())
+
+    def load(self, path) -> "CachePool":
+        """pool.py:191-241: replace the pool contents from a KVSH file.  The
+        header is validated on the host with the reference's errors and byte
+        offsets; each entry's f32 block goes to the device once and the import
+        kernel writes it into fresh arena pages (bf16)."""
+        with open(path, "rb") as fh:
+            data = fh.read()
+        off = 0
+
+        def take(n: int, what: str) -> bytes:
+            nonlocal off
+            if off + n > len(data):
+                raise FormatError(f"truncated while reading {what}", off)
+            chunk = data[off:off + n]
+            off += n
+            return chunk
+
+        if take(4, "magic") != _MAGIC:
+            raise FormatError("bad magic bytes", 0)
+        (version,) = struct.unpack("<I", take(4, "version"))
+        if version != _VERSION:
+            raise FormatError(f"unsupported version {version}", 4)
+        (count,) = struct.unpack("<Q", take(8, "entry count"))
+        cfg = self.config
+        parsed = []
+        for _ in range(count):
+            (id_len,) = struct.unpack("<I", take(4, "id length"))
+            ident = take(id_len, "id").decode()
+            (n_tok,) = struct.unpack("<I", take(4, "token count"))
+            tokens = np.frombuffer(take(4 * n_tok, "tokens"), dtype="<u4").astype(np.int64)
+            layers, heads, d_k = struct.unpack("<III", take(12, "dimensions"))
+            if (layers, heads, d_k) != (cfg.num_layers, cfg.kv_heads, cfg.d_k):
+                raise CacheError(
+                    f"entry {ident!r} dims ({layers}, {heads}, {d_k}) do not match "
+                    f"pool config ({cfg.num_layers}, {cfg.kv_heads}, {cfg.d_k})")
+            if n_tok == 0:
+                raise CacheError(f"entry {ident!r} has no tokens")
+            size = layers * n_tok * heads * d_k
+            k_off = off
+            take(4 * size, "K")
+            v_off = off
+            take(4 * size, "V")
+            parsed.append((ident, tokens, k_off, v_off, size))
+        if off != len(data):
+            raise FormatError("trailing data after final entry", off)
+        for entry in list(self.entries.values()):
+            self._drop(entry)
+        shape = (cfg.num_layers, -1, cfg.kv_heads, cfg.d_k)
+        cap, self.capacity_bytes = self.capacity_bytes, None     # load never evicts
+        for ident, tokens, k_off, v_off, size in parsed:
+            k = torch.from_numpy(np.frombuffer(data, "<f4", size, k_off).reshape(shape).copy())
+            v = torch.from_numpy(np.frombuffer(data, "<f4", size, v_off).reshape(shape).copy())
+            pages = self.arena.alloc(self.arena.pages_for(tokens.size))
+            self._import(pages, k.to(self.device), v.to(self.device))
+            self.insert_pages(ident, tokens, pages)
+        self.capacity_bytes = cap
+        return self
 
     # ------------------------------------------------------------------ index
     def _build_index(self):
@@ -396,25 +486,28 @@ class CachePool:
         return reuse
 
     def _lookup_fixed(self, tokens: np.ndarray, chunk: int) -> ReuseMap:
-        """Fixed-chunk baseline (pool.py:148-149 -> matching.fixed_chunk_match)."""
-        from .matching import fixed_chunk_match
+        """Fixed-chunk baseline (pool.py:148-149 -> matching.fixed_chunk_match)
+        on the device: the F5 kernel claims each chunk-aligned block for the
+        newest entry holding it at an aligned offset."""
+        if chunk < 1:
+            raise ParameterError(f"chunk_size must be >= 1, got {chunk}")
         reuse = ReuseMap(length=int(tokens.size))
-        ordered = sorted(self.entries.values(), key=lambda e: -e.insert_seq)
-        contributors = []
-        for entry in ordered:
-            if len(reuse.sources) == reuse.length:
-                break
-            res = fixed_chunk_match(tokens, entry.tokens, chunk)
-            contributed = False
-            for t, c in zip(res.target_matches, res.candidate_matches):
-                if t not in reuse.sources:
-                    reuse.sources[t] = (entry, c)
-                    contributed = True
-            if contributed:
-                contributors.append(entry)
-        for entry in sorted(contributors, key=lambda e: e.last_access):
-            entry.last_access = self._tick()
-        reuse.sources = dict(sorted(reuse.sources.items()))
+        dev, n = self.device, int(tokens.size)
+        idx = self._build_index()
+        tok = torch.from_numpy(tokens).to(dev)
+        off = torch.tensor([0, n], dtype=torch.int64, device=dev)
+        slot = torch.empty(n, dtype=torch.int32, device=dev)
+        cand = torch.empty(n, dtype=torch.int32, device=dev)
+        n_hit = torch.zeros(1, dtype=torch.int32, device=dev)
+        contributed = torch.zeros((1, max(len(self._slots), 1)), dtype=torch.uint8, device=dev)
+        N.call("kvs_fixed_chunk_lookup", idx["c"], tok.data_ptr(), off.data_ptr(), 1, n, int(chunk),
+               slot.data_ptr(), cand.data_ptr(), n_hit.data_ptr(), contributed.data_ptr(), n,
+               N.stream_ptr())
+        self.refresh_lru(contributed[0].cpu().numpy())
+        sl, cd = slot.cpu().numpy(), cand.cpu().numpy()
+        for pos in np.nonzero(sl >= 0)[0]:
+            reuse.sources[int(pos)] = (self._slots[sl[pos]], int(cd[pos]))
+        reuse.src_slot, reuse.src_cand = slot, cand
         return reuse
 
     # ------------------------------------------------------------------ eviction

@@ -137,3 +137,54 @@ def test_most_recent_entry_wins_and_lru():
     reuse = pool.lookup(span)
     assert {e.request_id for e, _ in reuse.sources.values()} == {"new"}
     assert pool.entries["new"].last_access > pool.entries["old"].last_access
+
+
+def _fixed_doc():
+    import json
+    import os
+    return json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                       "golden_fixed_chunk.json")))
+
+
+@pytest.mark.parametrize("idx", range(40))
+def test_fixed_chunk_lookup_golden(idx):
+    """F5 kvs_fixed_chunk_lookup against the reference's fixed-chunk pool
+    lookups (pool.py:139-159, matching.py:171-194), bit-exact, including
+    which entries get their LRU tick refreshed and in what order."""
+    c = _fixed_doc()[idx]
+    cfg, pool = _pool(w=4)
+    ids = c["entry_ids_newest_first"]
+    for rid, tok in reversed(list(zip(ids, c["entries_newest_first"]))):
+        z = np.zeros((1, 1, len(tok), 2))
+        pool.insert(rid, tok, z, z)
+    before = {rid: e.last_access for rid, e in pool.entries.items()}
+    reuse = pool.lookup(c["request"], fixed_chunk=c["chunk"])
+    assert sorted(reuse.sources) == c["positions"]
+    assert [ids.index(reuse.sources[p][0].request_id) for p in sorted(reuse.sources)] == c["src_entry"]
+    assert [reuse.sources[p][1] for p in sorted(reuse.sources)] == c["src_cand"]
+    touched = sorted([r for r, e in pool.entries.items() if e.last_access != before[r]],
+                     key=lambda r: pool.entries[r].last_access)
+    assert touched == c["contributors_lru_order"]
+
+
+def test_fixed_chunk_lookup_vs_oracle_large():
+    """Long requests and entries with many aligned repeats: kernel == oracle."""
+    cfg, pool = _pool(w=8)
+    rng = np.random.default_rng(9)
+    entries = []
+    for e in range(6):
+        tok = rng.integers(0, 8, int(rng.integers(500, 3000)))
+        entries.append(tok)
+        z = np.zeros((1, 1, tok.size, 2))
+        pool.insert(f"e{e}", tok, z, z)
+    for c in (1, 4, 16, 64):
+        src = entries[2]
+        req = np.concatenate([rng.integers(0, 8, 3 * c), src[c * 5: c * 5 + 40 * c],
+                              rng.integers(0, 8, 77)])
+        order = sorted(pool.entries.values(), key=lambda e: -e.insert_seq)
+        se, sc, _ = O.fixed_chunk_lookup([e.tokens for e in order], req, c)
+        reuse = pool.lookup(req, fixed_chunk=c)
+        pos = np.nonzero(se >= 0)[0].tolist()
+        assert sorted(reuse.sources) == pos
+        assert [reuse.sources[p][1] for p in pos] == sc[pos].tolist()
+        assert [order.index(reuse.sources[p][0]) for p in pos] == se[pos].tolist()

@@ -129,3 +129,23 @@ def test_known_answer_selection():
     k[5] = [12.0, 0.0, 0.0, 0.0]
     sel, _ = O.select_decode_step(np.array([4.0, 0, 0, 0]), k, np.ones((n, d)), set(range(n)), 1)
     assert sel == (5,)
+
+
+def _fixed_doc():
+    import json
+    import os
+    return json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                       "golden_fixed_chunk.json")))
+
+
+@pytest.mark.parametrize("idx", range(40))
+def test_fixed_chunk_lookup_golden(idx):
+    """F5 restatement pinned to the reference's own fixed-chunk lookups."""
+    c = _fixed_doc()[idx]
+    se, sc, contrib = O.fixed_chunk_lookup(c["entries_newest_first"], c["request"], c["chunk"])
+    pos = np.nonzero(se >= 0)[0].tolist()
+    assert pos == c["positions"]
+    assert se[pos].tolist() == c["src_entry"]
+    assert sc[pos].tolist() == c["src_cand"]
+    ids = c["entry_ids_newest_first"]
+    assert sorted(ids[i] for i in np.nonzero(contrib)[0]) == sorted(c["contributors_lru_order"])
