@@ -185,7 +185,8 @@ def algorithmic_counts(eng, st, cfg):
     import torch
     H, d, G = cfg.num_heads, cfg.d_k, cfg.kv_heads
     pos = st.rows.row_pos.to(torch.float64)
-    sess = (pos + 1).sum() * (4.0 * H * d * cfg.num_layers)     # device scalar, no sync
+    layers = cfg.num_layers - getattr(st, "session_first", 0)     # layer 0 may come from the probe
+    sess = (pos + 1).sum() * (4.0 * H * d * layers)              # device scalar, no sync
     probe = 0.0
     alpha = 0.0
     for n in st.lengths:

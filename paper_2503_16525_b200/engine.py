@@ -200,6 +200,7 @@ class Engine:
         self._ev_next = 0
         self.scratch = _Scratch(self.device)
         self._xb_of = None
+        self.layer0_fast = True     # prefill_batch: probe layer 0 doubles as the prefill's
 
     # ------------------------------------------------------------------ helpers
     def reset_timer_events(self, reserve: int = 0):
@@ -358,30 +359,47 @@ class Engine:
         st._contributed = res.contributed
         return st
 
-    def gather(self, st: BatchState):
+    def gather(self, st: BatchState, layers=None, slot=None):
+        """G1 for layers [begin, end) (all by default); `slot` overrides the
+        hit map (e.g. with selected rows masked out)."""
         if not self.pool.entries:
             return
+        begin, end = layers if layers is not None else (0, self.cfg.num_layers)
         idx = self.pool._build_index()
-        slot = st.src_slot
+        slot = st.src_slot if slot is None else slot
         if self.fetcher is not None:
             slot = self.fetcher.local_mask(st.src_slot, idx)
             self._timed("remote_fetch", self.fetcher.fetch, st, idx)
         self._timed("gather", N.call, "kvs_gather_kv", self.arena.c, st.batch_c, slot.data_ptr(),
-               st.src_cand.data_ptr(), idx["slot_pages"].data_ptr(), idx["slot_max_pages"], 0,
-               self.cfg.num_layers, self._rope(), N.stream_ptr())
+               st.src_cand.data_ptr(), idx["slot_pages"].data_ptr(), idx["slot_max_pages"], begin,
+               end, self._rope(), N.stream_ptr())
 
-    def _probe(self, st: BatchState, write_k: bool = True):
-        """engine.py:182-207: fresh layers below the probe over ALL rows (on a
-        scratch arena), then the probe layer's q (dense), k_true (into the
-        arena for non-reused rows, so the arena layer holds k_pert) and
-        v_true (dense)."""
+    def _probe(self, st: BatchState, write_k: bool = True, layer0_in_place: bool = False):
+        """engine.py:182-207: fresh layers below the probe over ALL rows, then
+        the probe layer's q (dense), k_true (into the arena for non-reused
+        rows, so the arena layer holds k_pert) and v_true (dense).
+
+        Layer 0 runs on a scratch arena, or - layer0_in_place - on the
+        request's own layer-0 pages (fresh K/V for every row; the caller
+        gathers the cached rows back afterwards for the reused, unselected
+        positions).  In place, the layer-0 hidden rows are kept on the state
+        (st._x_probe): layer 0's K/V are context-free, so they equal the
+        partial prefill's layer 0 (reference test_model.py:121-128)."""
         cfg, m, dev = self.cfg, self.model, self.device
         H, G = cfg.num_heads, cfg.kv_heads
         rows = self._rows_all(st)
         n = rows.n_rows
         x = self._embed(st.tokens, rows, scratch=True)
         p = self.probe_layer
-        if p == 1:
+        if p == 1 and layer0_in_place:
+            q = self.scratch.get("q", (n, H, HEAD_DIM), torch.bfloat16)
+            o = self.scratch.get("o", (n, H, HEAD_DIM), torch.bfloat16)
+            qkv = self._qkv(x, 0)
+            self._scatter(qkv, rows, 0, self.arena.c, st.batch_c, q, use_write=False)
+            self._attention(q, rows, 0, self.arena.c, st.batch_c, o)
+            self._out_proj(x, o, 0)
+            st._x_probe = x
+        elif p == 1:
             npages = int(sum((l + PAGE_SIZE - 1) // PAGE_SIZE for l in st.lengths))
             parena = self._probe_arena.get(cfg, npages, dev)
             bt = np.zeros((len(st.lengths), st.block_table.shape[1]), dtype=np.int32)
@@ -424,11 +442,11 @@ class Engine:
         st._bud = bud
         return dv, score, sel
 
-    def probe_and_select(self, st: BatchState, ratio: float):
+    def probe_and_select(self, st: BatchState, ratio: float, layer0_in_place: bool = False):
         """engine.py:233-243 (PRACTICAL): fresh probe, D1 alpha, D2 select."""
         cfg, dev = self.cfg, self.device
         H, G = cfg.num_heads, cfg.kv_heads
-        rows, q1, v_true = self._probe(st)
+        rows, q1, v_true = self._probe(st, layer0_in_place=layer0_in_place)
         n = rows.n_rows
         alpha = torch.empty(n, dtype=torch.float32, device=dev)
         ws = self._ws["alpha"].get(N.ws_bytes("kvs_dhd_alpha_workspace", n, H, G), dev)
@@ -471,10 +489,19 @@ class Engine:
         rows._keep = (row_off, src)
         return rows.build_tiles(dev, kv_len=st.lengths, partial_first=True)
 
-    def session_forward(self, st: BatchState, rows: RowSet, capture=None):
-        x = self._embed(st.tokens, rows, scratch=capture is None)
-        x = self.forward_rows(x, rows, range(self.cfg.num_layers), self.arena.c, st.batch_c,
-                              capture=capture)
+    def session_forward(self, st: BatchState, rows: RowSet, capture=None, x_probe=None):
+        """Layers over rows S.  With x_probe (the probe's all-row hidden state
+        after layer 0) the pass starts at layer 1 from rows S of it."""
+        if x_probe is not None:
+            x = self.scratch.get("x_s", (rows.n_rows, self.cfg.d_model), torch.float32)
+            torch.index_select(x_probe, 0, rows.row_tok.long(), out=x)
+            first = 1
+        else:
+            x = self._embed(st.tokens, rows, scratch=capture is None)
+            first = 0
+        st.session_first = first
+        x = self.forward_rows(x, rows, range(first, self.cfg.num_layers), self.arena.c,
+                              st.batch_c, capture=capture)
         last = h2d(rows.row_off[1:] - 1, self.device)
         st.rows = rows
         st.hidden_last = x[last]
@@ -494,14 +521,28 @@ class Engine:
             st.selected = None
             return st
         self.lookup(st)
-        self.gather(st)
-        if mode == "selective" and ratio > 0:
-            self.probe_and_select(st, ratio)
+        L = self.cfg.num_layers
+        if (mode == "selective" and ratio > 0 and self.probe_layer == 1 and self.fetcher is None
+                and self.layer0_fast):
+            # layers >= 1 gathered first; the probe's fresh layer 0 runs in
+            # place and doubles as the partial prefill's layer 0; cached layer-0
+            # rows return for the reused, unselected positions after selection
+            self.gather(st, (1, L))
+            self.probe_and_select(st, ratio, layer0_in_place=True)
+            keep = torch.where(st.selected.bool(), torch.full_like(st.src_slot, -1), st.src_slot)
+            self.gather(st, (0, 1), slot=keep)
             rows = self.build_rows(st, st.selected)
+            self.session_forward(st, rows, x_probe=st._x_probe)
+            st._x_probe = None
         else:
-            rows = self.build_rows(st, None)
-            st.selected = None
-        self.session_forward(st, rows)
+            self.gather(st)
+            if mode == "selective" and ratio > 0:
+                self.probe_and_select(st, ratio)
+                rows = self.build_rows(st, st.selected)
+            else:
+                rows = self.build_rows(st, None)
+                st.selected = None
+            self.session_forward(st, rows)
         reused = st.src_slot >= 0
         sel = st.selected.bool() if st.selected is not None else torch.zeros_like(reused)
         st.eligible = (reused & ~sel).to(torch.uint8)
