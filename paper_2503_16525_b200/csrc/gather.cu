@@ -138,13 +138,15 @@ __global__ void __launch_bounds__(256) qkv_rope_scatter_kernel(
         dk = reinterpret_cast<uint4 *>(A.row(page, layer, 0, pos % A.P));
         dv = reinterpret_cast<uint4 *>(A.row(page, layer, 1, pos % A.P));
     }
-    uint4 *qo = reinterpret_cast<uint4 *>(q_out + row * (int64_t)H * D);
+    uint4 *qo = q_out ? reinterpret_cast<uint4 *>(q_out + row * (int64_t)H * D) : nullptr;
     uint4 *ko = k_out ? reinterpret_cast<uint4 *>(k_out + row * (int64_t)G * D) : nullptr;
     uint4 *vo = v_out ? reinterpret_cast<uint4 *>(v_out + row * (int64_t)G * D) : nullptr;
     const float4 *c4 = reinterpret_cast<const float4 *>(cos_t + (size_t)pos * half);
     const float4 *s4 = reinterpret_cast<const float4 *>(sin_t + (size_t)pos * half);
+    // q_out == nullptr: the query heads are left to the attention kernel
+    const int item0 = q_out != nullptr ? 0 : H * chunks;
     const int n_rope = (H + G) * chunks, n_items = n_rope + G * vph, vbase = (H + G) * vph;
-    for (int base = 0; base < n_items; base += 2 * blockDim.x) {
+    for (int base = item0; base < n_items; base += 2 * blockDim.x) {
         uint4 lo[2], hi[2];
         int it[2];
 #pragma unroll
