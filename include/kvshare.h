@@ -166,6 +166,24 @@ kvs_status kvs_unpack_rows(const kvs_kv_arena *arena, const kvs_batch *batch,
                            const int64_t *flat_t, const int32_t *cand, int64_t n_rows,
                            const void *in, const kvs_rope *rope, kvs_stream_t stream);
 
+/* F4 comparison strategies (selection.py:133-186).
+ * kvs_topk_select: per request r (positions [req_off[r], req_off[r+1]),
+ *   length <= max_len <= 47104), selected[t] = 1 for the budget[r] candidates
+ *   (cand[t] >= 0) with the largest scores[t] >= 0, ties to the lower
+ *   position (_take_top, selection.py:63-66).
+ * kvs_ideal_scores: IDEAL leave-one-in scores (selection.py:172-183):
+ *   scores[i] = ||attn(q, k + e_i dk, v + e_i dv) - attn(q, k, v)||_F over
+ *   heads, rows and dims; q [H][n][d], k/v/dk/dv [kv_heads][n][d] fp32
+ *   (GQA: query head h uses kv head h / (H / kv_heads)), d <= 256.        */
+kvs_status kvs_topk_select(const float *scores, const int32_t *cand, const int64_t *req_off,
+                           int32_t n_req, int64_t max_len, const int32_t *budget,
+                           uint8_t *selected, kvs_stream_t stream);
+size_t kvs_ideal_scores_workspace(int32_t num_heads, int32_t n, int32_t d);
+kvs_status kvs_ideal_scores(const float *q, const float *k, const float *v, const float *dk,
+                            const float *dv, int32_t num_heads, int32_t kv_heads, int32_t n,
+                            int32_t d, int32_t causal, float softmax_scale, float *scores,
+                            void *ws, size_t ws_bytes, kvs_stream_t stream);
+
 /* F3/F1 pool-entry transfer (reference pool.py:100-123, 174-241): an entry's
  * K and V as dense fp32 [num_layers][n_tokens][kv_heads][d_k] - the KVSH file
  * order - to (import) or from (export) its arena pages (pages[i] holds tokens

@@ -405,6 +405,59 @@ def select_prefill(q, k, delta_v, reused, ratio, causal=True, group=1):
     return take_top(scores, reused, budget(ratio, len(reused))), scores
 
 
+def _spans(positions):
+    runs = []
+    for p in positions:
+        if runs and p == runs[-1][-1] + 1:
+            runs[-1].append(p)
+        else:
+            runs.append([p])
+    return runs
+
+
+def select_baseline(strategy, q, k, v, dk, dv, reused, ratio, seed=0, causal=True, group=1):
+    """selection.py:133-186 restated for the comparison strategies.
+    Returns (indices tuple, scores[n]).  IDEAL is the reference's literal
+    leave-one-in loop (one attention pass per reused position)."""
+    reused = sorted(set(int(i) for i in reused))
+    q, k, v, dk, dv = (np.asarray(x, float) for x in (q, k, v, dk, dv))
+    if q.ndim == 2:
+        q, k, v, dk, dv = (x[None] for x in (q, k, v, dk, dv))
+    n = k.shape[1]
+    b = budget(ratio, len(reused))
+    if strategy == "attention_weighted":
+        return select_prefill(q, k + dk, dv, reused, ratio, causal=causal, group=group)
+    if strategy == "magnitude":
+        scores = np.abs(dv).sum(axis=(0, 2)) + np.abs(dk).sum(axis=(0, 2))
+        return take_top(scores, reused, b), scores
+    if strategy == "positional":
+        chosen = []
+        for span in _spans(reused):
+            chosen.extend(span[: math.ceil(ratio * len(span))])
+        if len(chosen) > b:
+            chosen = sorted(chosen)[:b]
+        elif len(chosen) < b:
+            taken = set(chosen)
+            chosen.extend([p for p in reused if p not in taken][: b - len(chosen)])
+        return tuple(sorted(chosen)), np.zeros(n)
+    if strategy == "random":
+        gen = np.random.Generator(np.random.Philox(key=seed))
+        scores = np.zeros(n)
+        scores[reused] = gen.uniform(size=len(reused))
+        return take_top(scores, reused, b), scores
+    if strategy == "ideal":
+        base, _ = attention(q, k, v, causal=causal, group=group)
+        scores = np.zeros(n)
+        for i in reused:
+            k1, v1 = k.copy(), v.copy()
+            k1[:, i, :] += dk[:, i, :]
+            v1[:, i, :] += dv[:, i, :]
+            pert, _ = attention(q, k1, v1, causal=causal, group=group)
+            scores[i] = np.linalg.norm(pert - base)
+        return take_top(scores, reused, b), scores
+    raise ValueError(f"unknown strategy {strategy!r}")
+
+
 def select_decode_step(q_t, k, delta_v, eligible, n_extra, group=1):
     """selection.py:80-105 (+GQA): unmasked softmax over the whole context,
     mean over query heads, times the delta_v L1 summed over kv heads."""

@@ -53,6 +53,9 @@ _SIGS = {
                              P(Rope), c_vp, c_vp, c_vp, c_vp],
     "kvs_fixed_chunk_lookup": [P(TokenIndex), c_vp, c_vp, c_i32, c_i64, c_i32, c_vp, c_vp, c_vp,
                                c_vp, c_i64, c_vp],
+    "kvs_topk_select": [c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, c_vp, c_vp],
+    "kvs_ideal_scores": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_f32,
+                         c_vp, c_vp, c_size, c_vp],
     "kvs_entry_import": [P(KVArena), c_vp, c_i64, c_i32, c_vp, c_vp, c_vp],
     "kvs_entry_export": [P(KVArena), c_vp, c_i64, c_i32, c_vp, c_vp, c_vp],
     "kvs_embed_rows": [c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp],
@@ -76,6 +79,7 @@ _WS_SIGS = {
     "kvs_pool_lookup_workspace": [c_i64],
     "kvs_decode_attention_workspace": [c_i64, c_i32, c_i32, c_i32, c_i32],
     "kvs_dhd_alpha_workspace": [c_i64, c_i32, c_i32],
+    "kvs_ideal_scores_workspace": [c_i32, c_i32, c_i32],
     "kvs_dhd_select_workspace": [c_i64, c_i32],
     "kvs_dhd_decode_select_workspace": [c_i32, c_i32, c_i32],
 }
@@ -87,7 +91,7 @@ KERNELS_PER_CALL = {
     "kvs_window_hashes": 1, "kvs_match_pairs": 9, "kvs_index_sort": 5, "kvs_pool_lookup": 4,
     "kvs_gather_kv": 1, "kvs_qkv_rope_scatter": 1, "kvs_embed_rows": 1, "kvs_build_rows": 1,
     "kvs_attention_fwd": 1, "kvs_decode_attention": 2, "kvs_dhd_alpha": 3,
-    "kvs_dhd_select": 1, "kvs_dhd_decode_select": 2, "kvs_pack_rows": 1, "kvs_unpack_rows": 1,
+    "kvs_dhd_select": 1, "kvs_ideal_scores": 3, "kvs_dhd_decode_select": 2, "kvs_pack_rows": 1, "kvs_unpack_rows": 1,
 }
 launch_count = {"kernels": 0}
 

@@ -622,6 +622,25 @@ __global__ void __launch_bounds__(kSelThreads, 1) dhd_select_fused_kernel(
     }
 }
 
+// F4: top-B over caller-given scores (reference selection.py:63-66 _take_top
+// for the MAGNITUDE / RANDOM / IDEAL strategies, selection.py:154-183): one
+// CTA per request; candidates are positions with cand >= 0, scores >= 0.
+__global__ void __launch_bounds__(kSelThreads) topk_kernel(const float *__restrict__ score,
+                                                           const int32_t *__restrict__ cand,
+                                                           const int64_t *__restrict__ req_off,
+                                                           const int32_t *__restrict__ budget,
+                                                           uint8_t *__restrict__ selected) {
+    extern __shared__ uint32_t s_topk[];
+    __shared__ uint32_t sh[4];
+    const int r = blockIdx.x;
+    const int64_t s = req_off[r], n = req_off[r + 1] - s;
+    uint32_t *whist = s_topk, *keys = s_topk + 8 * 256;
+    if (n <= kRegKeys)
+        select_fast<true>(score, cand, s, n, budget[r], selected, whist, keys, sh);
+    else
+        select_fast<false>(score, cand, s, n, budget[r], selected, whist, keys, sh);
+}
+
 // ---------------------------------------------------------------- D3
 // Pass 1: grid (request, key chunk).  Logits for all query heads of one key
 // row, each K row read once for its GQA group; per-(request, chunk, head)
@@ -972,6 +991,19 @@ kvs_status kvs_decode_attention(const void *q, const int32_t *row_req, const int
     decode_attn_combine_kernel<<<dim3((unsigned)n_rows, num_heads), 128, 0, s>>>(
         (const float *)ws, num_heads, D, splits, (__nv_bfloat16 *)out);
     KVS_CHECK_LAUNCH("kvs_decode_attention");
+    return KVS_OK;
+}
+
+kvs_status kvs_topk_select(const float *scores, const int32_t *cand, const int64_t *req_off,
+                           int32_t n_req, int64_t max_len, const int32_t *budget,
+                           uint8_t *selected, kvs_stream_t stream) {
+    KVS_REQUIRE(n_req >= 1 && n_req <= 65535, KVS_EPARAM, "n_req must be in [1, 65535]");
+    KVS_REQUIRE(max_len <= kSmemKeys, KVS_ESHAPE, "requests longer than %d positions", kSmemKeys);
+    const int smem = (int)(sizeof(uint32_t) * (8 * 256 + (max_len > kRegKeys ? max_len : 0)));
+    cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    topk_kernel<<<n_req, kSelThreads, smem, (cudaStream_t)stream>>>(scores, cand, req_off, budget,
+                                                                    selected);
+    KVS_CHECK_LAUNCH("kvs_topk_select");
     return KVS_OK;
 }
 

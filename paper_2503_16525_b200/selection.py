@@ -4,9 +4,9 @@ Drop-in for reference pkg/src/kvlab/selection.py: ``Strategy``,
 ``SelectionMode``, ``SelectionConfig`` (:37-52, budget with the exact
 IEEE-double ceil), ``SelectionResult``, ``select_prefill`` (:69-77, D1 + D2
 radix top-B) and ``select_decode_step`` (:80-105, D3).  ``select_baseline``
-keeps the ATTENTION_WEIGHTED branch the hot path uses (:156-157); the
-comparison baselines (MAGNITUDE/POSITIONAL/RANDOM/IDEAL) are the SURVEY's
-next row F4 and raise ParameterError here.
+(:133-186) runs all five strategies: the hot path's ATTENTION_WEIGHTED and
+the comparison baselines of the SURVEY's row F4 (MAGNITUDE / POSITIONAL /
+RANDOM / IDEAL) with device scoring and the kvs_topk_select top-B.
 """
 from __future__ import annotations
 
@@ -134,16 +134,98 @@ def select_decode_step(q_t, k, delta_v, eligible, n_extra: int) -> SelectionResu
                            scores[0].double().cpu().numpy())
 
 
+def _spans(positions: list[int]) -> list[list[int]]:
+    """Contiguous runs of an ascending position list (selection.py:108-116)."""
+    runs: list[list[int]] = []
+    for p in positions:
+        if runs and p == runs[-1][-1] + 1:
+            runs[-1].append(p)
+        else:
+            runs.append([p])
+    return runs
+
+
+def _positional_selection(reused: list[int], config: SelectionConfig) -> tuple[int, ...]:
+    """Leading positions of each reused span, trimmed/padded to the budget
+    (selection.py:119-130); pure index logic on the host."""
+    budget = config.budget(len(reused))
+    chosen: list[int] = []
+    for span in _spans(reused):
+        chosen.extend(span[: math.ceil(config.ratio * len(span))])
+    if len(chosen) > budget:
+        chosen = sorted(chosen)[:budget]
+    elif len(chosen) < budget:
+        taken = set(chosen)
+        rest = [p for p in reused if p not in taken]
+        chosen.extend(rest[: budget - len(chosen)])
+    return tuple(sorted(chosen))
+
+
+def _device_top(scores: torch.Tensor, reused: list[int], budget: int) -> tuple[int, ...]:
+    """_take_top (selection.py:63-66) on the device: kvs_topk_select over the
+    reused positions, score descending, position ascending."""
+    dev, n = scores.device, scores.numel()
+    cand = torch.full((n,), -1, dtype=torch.int32, device=dev)
+    cand[torch.as_tensor(reused, dtype=torch.long, device=dev)] = 0
+    off = torch.tensor([0, n], dtype=torch.int64, device=dev)
+    bud = torch.tensor([budget], dtype=torch.int32, device=dev)
+    sel = torch.zeros(n, dtype=torch.uint8, device=dev)
+    N.call("kvs_topk_select", scores.data_ptr(), cand.data_ptr(), off.data_ptr(), 1, n,
+           bud.data_ptr(), sel.data_ptr(), N.stream_ptr())
+    return tuple(int(i) for i in torch.nonzero(sel).flatten().cpu().tolist())
+
+
 def select_baseline(strategy, q, k, v, delta_k, delta_v, reused, config: SelectionConfig,
                     causal: bool = True) -> SelectionResult:
-    """selection.py:133-186, ATTENTION_WEIGHTED branch (scores against the
-    perturbed keys k + delta_k, as served)."""
+    """selection.py:133-186: run one of the comparison strategies over the
+    same reuse scenario.  ``k``/``v`` are the fresh matrices and
+    ``delta_k``/``delta_v`` the cached-minus-fresh increments (rows outside
+    ``reused`` zero), (H, n, d) or (n, d).
+
+    ATTENTION_WEIGHTED: D1 + D2 against the perturbed keys (as served).
+    MAGNITUDE: sum |dv| + |dk| on the device, kvs_topk_select.
+    POSITIONAL: span heads (host index logic).
+    RANDOM: the reference's Philox(key=seed) uniforms, kvs_topk_select.
+    IDEAL: kvs_ideal_scores (leave-one-in deviation in closed form),
+    kvs_topk_select."""
     try:
         strategy = Strategy(strategy)
     except ValueError:
         raise ParameterError(f"unknown strategy: {strategy!r}") from None
-    if strategy is not Strategy.ATTENTION_WEIGHTED:
-        raise ParameterError(f"strategy {strategy.value} is a comparison baseline, not on the "
-                             "device hot path (SURVEY.md F4)")
-    k = np.asarray(k, float) + np.asarray(delta_k, float)
-    return select_prefill(q, k, delta_v, reused, config, causal=causal)
+    reused = sorted(set(int(i) for i in reused))
+    if not reused:
+        raise ParameterError("reused set is empty")
+    if strategy is Strategy.ATTENTION_WEIGHTED:
+        kp = np.asarray(k, float) + np.asarray(delta_k, float)
+        return select_prefill(q, kp, delta_v, reused, config, causal=causal)
+    qh, kh, vh = as_heads(q), as_heads(k), as_heads(v)
+    dkh, dvh = as_heads(delta_k), as_heads(delta_v)
+    n = kh.shape[1]
+    budget = config.budget(len(reused))
+    if strategy is Strategy.POSITIONAL:
+        return SelectionResult(_positional_selection(reused, config), np.zeros(n))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    N.load()
+    if strategy is Strategy.MAGNITUDE:
+        dk_t = torch.as_tensor(dkh, dtype=torch.float32, device=dev)
+        dv_t = torch.as_tensor(dvh, dtype=torch.float32, device=dev)
+        scores = (dv_t.abs().sum(dim=(0, 2)) + dk_t.abs().sum(dim=(0, 2))).contiguous()
+    elif strategy is Strategy.RANDOM:
+        gen = np.random.Generator(np.random.Philox(key=config.seed))
+        host = np.zeros(n)
+        host[reused] = gen.uniform(size=len(reused))
+        scores = torch.as_tensor(host, dtype=torch.float32, device=dev)
+    else:                                                       # IDEAL
+        H, G, d = qh.shape[0], kh.shape[0], qh.shape[2]
+        t = [torch.as_tensor(np.ascontiguousarray(x), dtype=torch.float32, device=dev)
+             for x in (qh, kh, vh, dkh, dvh)]
+        scores = torch.empty(n, dtype=torch.float32, device=dev)
+        ws = torch.empty(N.ws_bytes("kvs_ideal_scores_workspace", H, n, d), dtype=torch.uint8,
+                         device=dev)
+        N.call("kvs_ideal_scores", *(x.data_ptr() for x in t), H, G, n, d, 1 if causal else 0,
+               1.0 / math.sqrt(d), scores.data_ptr(), ws.data_ptr(), ws.numel(), N.stream_ptr())
+        mask = torch.zeros(n, dtype=torch.bool, device=dev)
+        mask[torch.as_tensor(reused, dtype=torch.long, device=dev)] = True
+        scores = torch.where(mask, scores, torch.zeros_like(scores))
+    indices = _device_top(scores, reused, budget)
+    return SelectionResult(indices, scores.double().cpu().numpy())

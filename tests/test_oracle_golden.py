@@ -149,3 +149,22 @@ def test_fixed_chunk_lookup_golden(idx):
     assert sc[pos].tolist() == c["src_cand"]
     ids = c["entry_ids_newest_first"]
     assert sorted(ids[i] for i in np.nonzero(contrib)[0]) == sorted(c["contributors_lru_order"])
+
+
+def _strategies():
+    import os
+    return np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_strategies.npz"))
+
+
+@pytest.mark.parametrize("strategy", ["magnitude", "positional", "random", "ideal",
+                                      "attention_weighted"])
+def test_select_baseline_golden(strategy):
+    """F4 restatement pinned to the reference's select_baseline outputs."""
+    z = _strategies()
+    for c in range(int(z["n_cases"])):
+        g = lambda k: z[f"c{c}_{k}"]  # noqa: E731
+        ratio, seed = g("meta")
+        idx, scores = O.select_baseline(strategy, g("q"), g("k"), g("v"), g("dk"), g("dv"),
+                                        g("reused").tolist(), float(ratio), int(seed))
+        assert list(idx) == g(f"{strategy}_idx").tolist()
+        np.testing.assert_allclose(scores, g(f"{strategy}_scores"), rtol=1e-9, atol=1e-12)
