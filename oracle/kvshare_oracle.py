@@ -458,6 +458,42 @@ def select_baseline(strategy, q, k, v, dk, dv, reused, ratio, seed=0, causal=Tru
     raise ValueError(f"unknown strategy {strategy!r}")
 
 
+def oracle_prefill(tokens, W, cfg, reuse, strategy, ratio, ref_states, table=None, seed=0):
+    """engine.py:245-285 ORACLE mode restated: per layer, fresh q/k/v for all
+    rows, cached rows substituted (k_pert, v_pert), deviations against the
+    reference pass's k/v restricted to the reused rows, select_baseline on
+    them, the layer's selected rows restored to fresh, attention, residual.
+    Returns (sets per layer, hidden (L+1, n, d_model))."""
+    tokens = np.asarray(tokens, dtype=np.int64)
+    x = W["embedding"][tokens]
+    n = x.shape[0]
+    pos = np.arange(n)
+    reused = reuse.reused
+    keep = np.zeros(n, bool)
+    keep[reused] = True
+    sets, hid = [], [x]
+    for layer in range(cfg.num_layers):
+        w = W["layers"][layer]
+        q, k_fresh, v_fresh = _qkv(x, w, cfg, table, pos)
+        kp, vp = k_fresh.copy(), v_fresh.copy()
+        rpos, kr, vr = reuse.cached_rows(layer, table)
+        for idx, p in enumerate(rpos):
+            kp[:, p, :] = kr[:, idx, :]
+            vp[:, p, :] = vr[:, idx, :]
+        dk = (kp - ref_states["k"][layer]) * keep[None, :, None]
+        dv = (vp - ref_states["v"][layer]) * keep[None, :, None]
+        idx, _ = select_baseline(strategy, q, ref_states["k"][layer], ref_states["v"][layer],
+                                 dk, dv, reused, ratio, seed=seed, group=cfg.group)
+        for p in idx:
+            kp[:, p, :] = k_fresh[:, p, :]
+            vp[:, p, :] = v_fresh[:, p, :]
+        sets.append(set(idx))
+        out, _ = attention(q, kp, vp, causal=True, group=cfg.group)
+        x = x + merge_heads(out) @ w[3]
+        hid.append(x)
+    return sets, np.stack(hid)
+
+
 def select_decode_step(q_t, k, delta_v, eligible, n_extra, group=1):
     """selection.py:80-105 (+GQA): unmasked softmax over the whole context,
     mean over query heads, times the delta_v L1 summed over kv heads."""

@@ -374,7 +374,8 @@ class Engine:
                st.src_cand.data_ptr(), idx["slot_pages"].data_ptr(), idx["slot_max_pages"], begin,
                end, self._rope(), N.stream_ptr())
 
-    def _probe(self, st: BatchState, write_k: bool = True, layer0_in_place: bool = False):
+    def _probe(self, st: BatchState, write_k: bool = True, layer0_in_place: bool = False,
+               k_out: torch.Tensor | None = None):
         """engine.py:182-207: fresh layers below the probe over ALL rows, then
         the probe layer's q (dense), k_true (into the arena for non-reused
         rows, so the arena layer holds k_pert) and v_true (dense).
@@ -423,7 +424,8 @@ class Engine:
         v_true = torch.empty(n, G, HEAD_DIM, dtype=torch.bfloat16, device=dev)
         wk = (st.src_slot < 0).to(torch.uint8) if write_k else \
             torch.zeros(n, dtype=torch.uint8, device=dev)
-        self._scatter(qkv, rows, p, self.arena.c, st.batch_c, q1, write_kv=wk, v_out=v_true)
+        self._scatter(qkv, rows, p, self.arena.c, st.batch_c, q1, write_kv=wk, k_out=k_out,
+                      v_out=v_true)
         return rows, q1, v_true
 
     def _select(self, st: BatchState, v_true, alpha, budgets):

@@ -309,10 +309,10 @@ def prefill_with_selection(model: ToyModel, tokens, reuse, config: SelectionConf
     if not reused:
         session = ReuseSession(model, tokens, reuse, decode_capacity=decode_capacity)
         return PrefillResult(session, session.recomputed)
-    if config.mode is not SelectionMode.PRACTICAL:
-        raise ParameterError("ORACLE selection mode is not on the device hot path (SURVEY.md F4)")
+    if config.mode is SelectionMode.ORACLE:
+        return _oracle_prefill(model, tokens, reuse, config, ref_states, decode_capacity)
     if Strategy(config.strategy) is not Strategy.ATTENTION_WEIGHTED:
-        raise ParameterError("only the ATTENTION_WEIGHTED strategy is on the device hot path")
+        return _practical_baseline(model, tokens, reuse, config, decode_capacity)
     tokens = np.asarray(tokens, dtype=np.int64)
     model.check_tokens(tokens)
     pool = _pool_of(reuse)
@@ -335,6 +335,113 @@ def prefill_with_selection(model: ToyModel, tokens, reuse, config: SelectionConf
     session = ReuseSession(model, tokens, reuse, set(selected), _engine_state=(eng, st, states))
     eligible = set(reused) - set(selected)
     return PrefillResult(session, session.recomputed, selected, eligible)
+
+
+def _probe_states(eng: Engine, st: BatchState):
+    """The perturbed probe (engine.py:195-207) as host arrays:
+    (q, k_true, v_true, k_pert, v_pert), heads unpadded, kv at kv_heads."""
+    cfg, m = eng.cfg, eng.model
+    n = int(st.lengths[0])
+    k_true = torch.empty(n, cfg.kv_heads, 128, dtype=torch.bfloat16, device=eng.device)
+    _, q1, v_true = eng._probe(st, k_out=k_true)
+    p = eng.probe_layer
+
+    def host(x):                                             # [n, heads, 128] -> (heads, n, d)
+        return m.unpad_heads(x).float().permute(1, 0, 2).double().cpu().numpy()
+
+    kp = host(eng.arena.rows(st.pages[0], n, p, 0))
+    vp = host(eng.arena.rows(st.pages[0], n, p, 1))
+    return host(q1), host(k_true), host(v_true), kp, vp
+
+
+def _restrict(delta: np.ndarray, keep) -> np.ndarray:
+    """engine.py:210-214: zero every row outside `keep`."""
+    out = np.zeros_like(delta)
+    idx = sorted(keep)
+    out[:, idx, :] = delta[:, idx, :]
+    return out
+
+
+def _practical_baseline(model, tokens, reuse, config, decode_capacity):
+    """engine.py:233-243 PRACTICAL mode with a comparison strategy: the
+    layer-1 probe's deviations scored by select_baseline (F4), the same set
+    recomputed at every layer."""
+    from .selection import select_baseline
+    tokens = np.asarray(tokens, dtype=np.int64)
+    model.check_tokens(tokens)
+    reused = sorted(reuse.sources)
+    pool = _pool_of(reuse)
+    eng = get_engine(model, pool)
+    st = eng.new_batch([tokens], 0)
+    st.src_slot, st.src_cand = _device_hits(reuse, tokens.size, eng.device)
+    eng.gather(st)
+    qp, kt, vt, kp, vp = _probe_states(eng, st)
+    eng.release(st)
+    keep = set(reused)
+    result = select_baseline(config.strategy, qp, kt, vt, _restrict(kp - kt, keep),
+                             _restrict(vp - vt, keep), reused, config)
+    selected = result.indices
+    session = ReuseSession(model, tokens, reuse, set(selected), decode_capacity=decode_capacity)
+    return PrefillResult(session, session.recomputed, selected, set(reused) - set(selected))
+
+
+def _oracle_prefill(model, tokens, reuse, config, ref_states, decode_capacity):
+    """engine.py:245-285 ORACLE mode: per layer, the true deviation of the
+    perturbed K/V against a fresh reference pass (ref_states) is scored by
+    the configured strategy (select_baseline) and that layer's selected rows
+    are restored to fresh before the layer's attention runs."""
+    from .selection import select_baseline
+    if ref_states is None:
+        raise ParameterError("oracle-mode prefill needs reference layer states")
+    tokens = np.asarray(tokens, dtype=np.int64)
+    model.check_tokens(tokens)
+    reused = sorted(reuse.sources)
+    keep = set(reused)
+    cfg, m = model.config, model
+    pool = _pool_of(reuse)
+    n = tokens.size
+    eng = get_engine(model, pool, n + decode_capacity)
+    st = eng.new_batch([tokens], decode_capacity)
+    st.src_slot, st.src_cand = _device_hits(reuse, n, eng.device)
+    st.n_hit = np.array([len(reused)])
+    eng.gather(st)                                    # cached (re-aligned) K/V, every layer
+    rows = eng._rows_all(st)
+    dev, H, G = eng.device, cfg.num_heads, cfg.kv_heads
+    fresh_rows = (st.src_slot < 0).to(torch.uint8)
+    q = torch.empty(n, H, 128, dtype=torch.bfloat16, device=dev)
+    o = torch.empty_like(q)
+    x = eng._embed(st.tokens, rows)
+    x0 = x.clone()
+    capture, sets = [], []
+
+    def host(t):
+        return m.unpad_heads(t).float().permute(1, 0, 2).double().cpu().numpy()
+
+    for layer in range(cfg.num_layers):
+        qkv = eng._qkv(x, layer)
+        eng._scatter(qkv, rows, layer, eng.arena.c, st.batch_c, q, write_kv=fresh_rows)
+        kp = host(eng.arena.rows(st.pages[0], n, layer, 0))
+        vp = host(eng.arena.rows(st.pages[0], n, layer, 1))
+        dk = _restrict(kp - ref_states.k[layer], keep)
+        dv = _restrict(vp - ref_states.v[layer], keep)
+        result = select_baseline(config.strategy, host(q), ref_states.k[layer],
+                                 ref_states.v[layer], dk, dv, reused, config)
+        sel = set(result.indices)
+        if sel:
+            mask = torch.zeros(n, dtype=torch.uint8, device=dev)
+            mask[torch.as_tensor(sorted(sel), dtype=torch.long, device=dev)] = 1
+            eng._scatter(qkv, rows, layer, eng.arena.c, st.batch_c, q, write_kv=mask)
+        sets.append(sel)
+        eng._attention(q, rows, layer, eng.arena.c, st.batch_c, o)
+        capture.append((layer, q.clone(), o.clone()))
+        eng._out_proj(x, o, layer)
+        capture.append((layer, "hidden", x.clone()))
+    st.rows = rows
+    st.hidden_last = x[-1:]
+    states = _states_from_capture(eng, st, rows, capture, x0)
+    session = ReuseSession(model, tokens, reuse, sets, _engine_state=(eng, st, states))
+    eligible = keep - set.intersection(*sets) if sets else set()
+    return PrefillResult(session, session.recomputed, tuple(sorted(set.union(*sets))), eligible)
 
 
 @dataclass

@@ -16,7 +16,7 @@ import sys
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-REF = sys.argv[1] if len(sys.argv) > 1 else "/root/reference/pkg/src"
+REF = next((a for a in sys.argv[1:] if not a.startswith("--")), "/root/reference/pkg/src")
 sys.path.insert(0, REF)
 os.environ["KVLAB_MATCH_BACKEND"] = "pure"
 
@@ -57,3 +57,56 @@ def main():
 
 if __name__ == "__main__":
     main()
+
+
+def oracle_mode_cases():
+    """golden_oracle_mode.npz: reference prefill_with_selection in ORACLE mode
+    (engine.py:245-285) for every strategy on one small reuse scenario, with
+    the scenario inputs the restatement needs."""
+    from kvlab import engine
+    from kvlab.matching import HashParams
+    from kvlab.model import ModelConfig, init_model, model_forward
+    from kvlab.pool import CachePool
+    from kvlab.selection import SelectionMode
+    cfg = ModelConfig(num_layers=3, num_heads=2, d_model=16, vocab_size=256, seed=4)
+    model = init_model(cfg)
+    rng = np.random.default_rng(8)
+    pool = CachePool(cfg, HashParams(window_size=4))
+    srcs = []
+    for s in range(2):
+        src = rng.integers(0, 256, int(rng.integers(25, 40))).tolist()
+        st = model_forward(src, model)
+        pool.insert(f"s{s}", src, st.k, st.v)
+        srcs.append(src)
+    target = (rng.integers(0, 256, 4).tolist() + srcs[0][2:20] + rng.integers(0, 256, 3).tolist()
+              + srcs[1][4:16] + rng.integers(0, 256, 2).tolist())
+    reuse = pool.lookup(target)
+    ref = model_forward(target, model)
+    order = [e.request_id for e in sorted(pool.entries.values(), key=lambda e: -e.insert_seq)]
+    n = len(target)
+    src_entry = np.full(n, -1, np.int32)
+    src_cand = np.full(n, -1, np.int32)
+    for p, (e, c) in reuse.sources.items():
+        src_entry[p] = order.index(e.request_id)
+        src_cand[p] = c
+    out = {"target": np.array(target), "src_entry": src_entry, "src_cand": src_cand,
+           "ref_k": ref.k, "ref_v": ref.v,
+           "config": np.array([cfg.num_layers, cfg.num_heads, cfg.d_model, cfg.vocab_size,
+                               cfg.seed])}
+    for i, r in enumerate(order):
+        out[f"entry_tokens_{i}"] = pool.entries[r].tokens
+        out[f"entry_k_{i}"] = pool.entries[r].k
+        out[f"entry_v_{i}"] = pool.entries[r].v
+    out["n_entries"] = np.array(len(order))
+    for s in STRATS:
+        scfg = SelectionConfig(ratio=0.3, mode=SelectionMode.ORACLE, strategy=Strategy(s), seed=5)
+        res = engine.prefill_with_selection(model, target, reuse, scfg, ref_states=ref)
+        for layer, st in enumerate(res.recompute_sets):
+            out[f"{s}_set{layer}"] = np.array(sorted(st), dtype=np.int64)
+        out[f"{s}_hidden"] = res.session.prefill_states.hidden
+    np.savez_compressed(os.path.join(HERE, "golden_oracle_mode.npz"), **out)
+    print("oracle-mode golden written")
+
+
+if __name__ == "__main__" and "--oracle-mode" in sys.argv:
+    oracle_mode_cases()

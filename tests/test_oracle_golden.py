@@ -168,3 +168,27 @@ def test_select_baseline_golden(strategy):
                                         g("reused").tolist(), float(ratio), int(seed))
         assert list(idx) == g(f"{strategy}_idx").tolist()
         np.testing.assert_allclose(scores, g(f"{strategy}_scores"), rtol=1e-9, atol=1e-12)
+
+
+def _oracle_mode_case():
+    import os
+    z = np.load(os.path.join(os.path.dirname(__file__), "golden", "golden_oracle_mode.npz"))
+    L, H, d_model, vocab, seed = (int(x) for x in z["config"])
+    ocfg = O.OracleConfig(L, H, d_model, vocab, seed)
+    W = O.draw_weights(ocfg)
+    E = int(z["n_entries"])
+    reuse = O.Reuse(z["src_entry"], z["src_cand"], [z[f"entry_k_{i}"] for i in range(E)],
+                    [z[f"entry_v_{i}"] for i in range(E)])
+    return z, ocfg, W, reuse
+
+
+@pytest.mark.parametrize("strategy", ["magnitude", "positional", "random", "ideal",
+                                      "attention_weighted"])
+def test_oracle_mode_prefill_golden(strategy):
+    """ORACLE-mode restatement (engine.py:245-285) pinned to the reference run."""
+    z, ocfg, W, reuse = _oracle_mode_case()
+    ref = {"k": z["ref_k"], "v": z["ref_v"]}
+    sets, hidden = O.oracle_prefill(z["target"], W, ocfg, reuse, strategy, 0.3, ref, seed=5)
+    for layer, st in enumerate(sets):
+        assert sorted(st) == z[f"{strategy}_set{layer}"].tolist()
+    np.testing.assert_allclose(hidden, z[f"{strategy}_hidden"], rtol=1e-9, atol=1e-9)
