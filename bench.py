@@ -308,7 +308,51 @@ def run_gpu(args, rank, world, device):
     res["e2e_ms"] = float(te.item())
     res["h2d_bytes"] = args.batch * args.seq * 8
     res["d2h_bytes"] = args.batch * cfg.d_model * 4
+    res["decode"] = decode_leg(args, eng, batches[args.warmup], cfg)
     return res
+
+
+def decode_leg(args, eng, batch, cfg, n_tokens: int = 8):
+    """Decode-stage DHD (reference engine.py:298-328) on one
+    scheduled batch after its DHD prefill: per step, the probe query of every
+    request's new token, D3 (kvs_dhd_decode_select: unmasked softmax over the
+    whole context at the probe layer x prefill dv-L1, top n_extra over the
+    still-stale rows), and one layer-batched pass over chosen U {new} rows.
+    Device time per token step with CUDA events; D3's HBM roofline from its
+    own events.  Not part of the headline metric (a prefill throughput)."""
+    import torch
+    rng = np.random.default_rng(5)
+    st = eng.prefill_batch(batch, ratio=args.ratio, decode_capacity=n_tokens + 1)
+    toks = rng.integers(0, cfg.vocab_size, (n_tokens, len(batch)))
+    eng.decode_step(st, toks[0], 3)                             # warm-up step
+    torch.cuda.synchronize()
+    timers = {}
+    eng.reset_timer_events(reserve=8 * n_tokens)
+    eng.timers = timers
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ctx0 = st.ctx_len.copy()
+    e0.record()
+    for t in range(1, n_tokens):
+        eng.decode_step(st, toks[t], 3)
+    e1.record()
+    torch.cuda.synchronize()
+    eng.timers = None
+    steps = n_tokens - 1
+    ms = e0.elapsed_time(e1) / steps
+    d3 = [a.elapsed_time(b) for a, b in timers.get("dhd_decode", [])]
+    G, d = cfg.kv_heads, 128
+    # SURVEY 8d D3 bytes per request-step: K at the probe layer over the context,
+    # dv-L1 and eligibility of the prefill rows, the chosen indices
+    ctx = ctx0 + np.arange(steps)[:, None]                       # context per step, request
+    lens = np.asarray(st.lengths)
+    d3_bytes = float((ctx * G * d * 2 + 4 * lens + lens / 8 + 12).sum()) / max(len(d3), 1)
+    d3_ms = float(np.mean(d3)) if d3 else float("nan")
+    eng.release(st)
+    return {"tokens_per_step": len(batch), "ms_per_token_step": ms,
+            "tok_s": len(batch) / (ms / 1000.0), "n_extra": 3,
+            "dhd_decode_select": {"bound": "hbm", "ms_per_call": d3_ms,
+                                  "algorithmic_bytes": d3_bytes,
+                                  "achieved": d3_bytes / (d3_ms / 1000.0) / 1e9, "unit": "GB/s"}}
 
 
 def ncu_traffic(kernel: str):
@@ -415,6 +459,11 @@ def main():
         "roofline": roof, "kernels": extra, "gpu_launches": res["launches"] * args.steps,
         "clocks": res["clocks"],
     }
+    if "decode" in res:
+        dec = res["decode"]
+        dec["dhd_decode_select"]["peak"] = hbm
+        dec["dhd_decode_select"]["frac"] = dec["dhd_decode_select"]["achieved"] / hbm
+        extra["decode"] = dec
     if "e2e_ms" in res:
         line["e2e"] = {"value": res["tokens"] / (res["e2e_ms"] / 1000.0), "unit": "tok/s",
                        "h2d_bytes_per_step": res["h2d_bytes"],

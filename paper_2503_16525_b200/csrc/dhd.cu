@@ -645,109 +645,141 @@ __global__ void __launch_bounds__(kSelThreads) topk_kernel(const float *__restri
 // Pass 1: grid (request, key chunk).  Logits for all query heads of one key
 // row, each K row read once for its GQA group; per-(request, chunk, head)
 // partial max / sum-exp.
-constexpr int kDecChunk = 256;
+constexpr int kDecChunk = 256;    // keys per CTA of the logits pass (8 warps x 32)
+
+// Pass 1: grid (key chunk, request), 8 warps, each a 32-key tile with one
+// key per lane (a tile lies in one page).  For every kv head the lane loads
+// its key's 256-byte slice and forms the HQ query heads' logits with q from
+// shared memory; logits [request][head][key] (log2 domain) are written
+// coalesced (consecutive keys per head).
+template <int HQ>
 __global__ void __launch_bounds__(256) decode_logits_kernel(
     const __nv_bfloat16 *__restrict__ q_t, int32_t H, const int32_t *__restrict__ ctx_len,
     int32_t max_ctx, int32_t layer, ArenaC A, const int32_t *__restrict__ block_table,
-    int32_t max_pages, float scale_log2, float *__restrict__ logits, float2 *__restrict__ part) {
-    extern __shared__ float sq[];  // [H][D] fp32
-    __shared__ float smax[8][64], ssum[8][64];
-    const int r = blockIdx.y, chunk = blockIdx.x;
+    int32_t max_pages, float scale_log2, float *__restrict__ logits,
+    float2 *__restrict__ part /* [request][tile][H] (max, sum) */) {
+    constexpr int D = 128;
+    extern __shared__ __align__(16) float sq[];  // [H][D] fp32
+    const int r = blockIdx.y;
     const int n = ctx_len[r];
-    const int D = A.D, G = A.G, hq = H / G;
     for (int i = threadIdx.x; i < H * D; i += blockDim.x)
         sq[i] = bf2f(q_t[(int64_t)r * H * D + i]);
     __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int k0 = chunk * kDecChunk;
-    float mloc[64], lloc[64];  // per head (H <= 64), lane-redundant
-    for (int h = 0; h < H; ++h) { mloc[h] = -INFINITY; lloc[h] = 0.f; }
-    for (int k = k0 + wid; k < min(n, k0 + kDecChunk); k += 8) {
-        const int64_t page = block_table[(int64_t)r * max_pages + k / A.P];
-        const __nv_bfloat16 *krow = A.row(page, layer, 0, k % A.P);
-        for (int g = 0; g < G; ++g) {
-            // lane holds D/32 elements of head g
-            float kv[8];
-            const int per = D / 32;
-            for (int e = 0; e < per; ++e) kv[e] = bf2f(krow[g * D + lane * per + e]);
-            for (int hh = 0; hh < hq; ++hh) {
-                const int h = g * hq + hh;
-                float p = 0.f;
-                for (int e = 0; e < per; ++e) p += kv[e] * sq[h * D + lane * per + e];
-                p = warp_sum(p) * scale_log2;  // log2-domain logit
-                if (lane == 0) logits[((int64_t)r * H + h) * max_ctx + k] = p;
-                const float mn = fmaxf(mloc[h], p);
-                lloc[h] = lloc[h] * fast_exp2(mloc[h] - mn) + fast_exp2(p - mn);
-                mloc[h] = mn;
+    const int t0 = blockIdx.x * kDecChunk + wid * 32;
+    if (t0 >= n) return;
+    const int k = t0 + lane;
+    const bool live = k < n;
+    const int64_t page = block_table[(int64_t)r * max_pages + t0 / A.P];
+    const __nv_bfloat16 *krow = A.row(page, layer, 0, t0 % A.P) + (int64_t)lane * A.G * D;
+    for (int g = 0; g < A.G; ++g) {
+        uint4 kx[D / 8];
+        if (live) {
+            const uint4 *kr = reinterpret_cast<const uint4 *>(krow + g * D);
+#pragma unroll
+            for (int c = 0; c < D / 8; ++c) kx[c] = __ldg(kr + c);
+        }
+        float p[HQ];
+#pragma unroll
+        for (int hh = 0; hh < HQ; ++hh) p[hh] = 0.f;
+#pragma unroll
+        for (int c = 0; c < D / 8; ++c) {
+            const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&kx[c]);
+            float kf[8];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const float2 f = __bfloat1622float2(h2[u]);
+                kf[2 * u] = f.x;
+                kf[2 * u + 1] = f.y;
+            }
+#pragma unroll
+            for (int hh = 0; hh < HQ; ++hh) {
+                const float *qh = sq + (g * HQ + hh) * D + 8 * c;
+                const float4 qa = *reinterpret_cast<const float4 *>(qh);
+                const float4 qb = *reinterpret_cast<const float4 *>(qh + 4);
+                p[hh] += kf[0] * qa.x + kf[1] * qa.y + kf[2] * qa.z + kf[3] * qa.w +
+                         kf[4] * qb.x + kf[5] * qb.y + kf[6] * qb.z + kf[7] * qb.w;
             }
         }
-    }
-    if (lane == 0)
-        for (int h = 0; h < H; ++h) { smax[wid][h] = mloc[h]; ssum[wid][h] = lloc[h]; }
-    __syncthreads();
-    for (int h = threadIdx.x; h < H; h += blockDim.x) {
-        float m = -INFINITY, l = 0.f;
-        for (int w = 0; w < 8; ++w) {
-            const float mw = smax[w][h];
-            if (mw == -INFINITY) continue;
-            const float mn = fmaxf(m, mw);
-            l = l * fast_exp2(m - mn) + ssum[w][h] * fast_exp2(mw - mn);
-            m = mn;
+        const int tile = t0 / 32, n_tiles = (max_ctx + 31) / 32;
+#pragma unroll
+        for (int hh = 0; hh < HQ; ++hh) {
+            const float x = live ? p[hh] * scale_log2 : -INFINITY;
+            if (live) logits[((int64_t)r * H + g * HQ + hh) * max_ctx + k] = x;
+            const float mt = warp_max(x);
+            const float z = warp_sum(live ? fast_exp2(x - mt) : 0.f);
+            if (lane == 0) part[((int64_t)r * n_tiles + tile) * H + g * HQ + hh] = make_float2(mt, z);
         }
-        part[((int64_t)r * gridDim.x + chunk) * H + h] = make_float2(m, l);
     }
 }
 
-// Pass 2: one CTA per request: combine partials, score eligible prefill rows,
-// n_extra rounds of block argmax on (score desc, pos asc).
+// Pass 2: one CTA per request: per-head softmax statistics over the whole
+// context (unmasked, selection.py:100-102) by block reductions, the mean
+// head weight x dv-L1 of every prefill row into shared memory (decode rows
+// have zero deviation, engine.py:145-147), then n_extra block-argmax rounds
+// on (score desc, position asc) over the still-eligible rows.
 __global__ void __launch_bounds__(1024) decode_select_kernel(
-    int32_t H, const int32_t *__restrict__ ctx_len, int32_t max_ctx, int32_t n_chunks,
+    int32_t H, const int32_t *__restrict__ ctx_len, int32_t max_ctx,
     const float *__restrict__ logits, const float2 *__restrict__ part,
-    const float *__restrict__ dv_l1, uint8_t *__restrict__ eligible,
-    const int64_t *__restrict__ req_off, int32_t n_extra, int32_t *__restrict__ chosen,
-    int32_t *__restrict__ n_chosen, float *__restrict__ scores_out) {
+    const float *__restrict__ dv_l1,
+    uint8_t *__restrict__ eligible, const int64_t *__restrict__ req_off, int32_t n_extra,
+    int32_t *__restrict__ chosen, int32_t *__restrict__ n_chosen, float *__restrict__ scores_out) {
+    extern __shared__ float sc[];            // [max_ctx] scores of this request
     __shared__ float sm[64], sz[64];
-    __shared__ uint64_t red[32];
+    __shared__ uint64_t redk[32];
     __shared__ int32_t s_pick[64];
     const int r = blockIdx.x;
     const int n = ctx_len[r];
     const int64_t s = req_off[r];
     const int n_pre = (int)(req_off[r + 1] - s);
-    for (int h = threadIdx.x; h < H; h += blockDim.x) {
-        float m = -INFINITY, l = 0.f;
-        for (int c = 0; c < n_chunks; ++c) {
-            const float2 p = part[((int64_t)r * n_chunks + c) * H + h];
-            if (p.x == -INFINITY) continue;
-            const float mn = fmaxf(m, p.x);
-            l = l * fast_exp2(m - mn) + p.y * fast_exp2(p.x - mn);
-            m = mn;
+    {
+        // warp w combines head w's per-tile (max, sum) partials of the logits pass
+        const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+        const int n_tiles = (max_ctx + 31) / 32, used = (n + 31) / 32;
+        for (int h = wid; h < H; h += blockDim.x >> 5) {
+            float m = -INFINITY, z = 0.f;
+            for (int t = lane; t < used; t += 32) {
+                const float2 pz = part[((int64_t)r * n_tiles + t) * H + h];
+                if (pz.x == -INFINITY) continue;
+                const float mn = fmaxf(m, pz.x);
+                z = z * fast_exp2(m - mn) + pz.y * fast_exp2(pz.x - mn);
+                m = mn;
+            }
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const float mo = __shfl_xor_sync(0xffffffffu, m, o);
+                const float zo = __shfl_xor_sync(0xffffffffu, z, o);
+                const float mn = fmaxf(m, mo);
+                z = (m == -INFINITY ? 0.f : z * fast_exp2(m - mn)) +
+                    (mo == -INFINITY ? 0.f : zo * fast_exp2(mo - mn));
+                m = mn;
+            }
+            if (lane == 0) {
+                sm[h] = m;
+                sz[h] = 1.f / z;
+            }
         }
-        sm[h] = m;
-        sz[h] = 1.f / l;
     }
     __syncthreads();
-    // scores for prefill rows (decode rows have zero deviation, engine.py:145-147)
     const float invH = 1.f / (float)H;
     float *scr = scores_out ? scores_out + (int64_t)r * max_ctx : nullptr;
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
         float w = 0.f;
-        for (int h = 0; h < H; ++h)
-            w += fast_exp2(logits[((int64_t)r * H + h) * max_ctx + i] - sm[h]) * sz[h];
-        const float sc = i < n_pre ? w * invH * dv_l1[s + i] : 0.f;
-        if (scr) scr[i] = sc;
+        if (i < n_pre)
+            for (int h = 0; h < H; ++h)
+                w += fast_exp2(logits[((int64_t)r * H + h) * max_ctx + i] - sm[h]) * sz[h];
+        const float v = i < n_pre ? w * invH * dv_l1[s + i] : 0.f;
+        sc[i] = v;
+        if (scr) scr[i] = v;
     }
-    // recompute-free argmax rounds: keys are recomputed from logits each round
+    __syncthreads();
     int picked = 0;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     for (int round = 0; round < n_extra; ++round) {
         uint64_t best = ~0ull;
         for (int i = threadIdx.x; i < n_pre && i < n; i += blockDim.x) {
             if (!eligible[s + i]) continue;
-            float w = 0.f;
-            for (int h = 0; h < H; ++h)
-                w += fast_exp2(logits[((int64_t)r * H + h) * max_ctx + i] - sm[h]) * sz[h];
-            const float sc = fmaxf(w * invH * dv_l1[s + i], 0.f);
-            const uint64_t key = ((uint64_t)(~__float_as_uint(sc)) << 32) | (uint32_t)i;
+            const uint64_t key = ((uint64_t)(~__float_as_uint(fmaxf(sc[i], 0.f))) << 32) | (uint32_t)i;
             best = key < best ? key : best;
         }
 #pragma unroll
@@ -755,11 +787,11 @@ __global__ void __launch_bounds__(1024) decode_select_kernel(
             const uint64_t x = __shfl_xor_sync(0xffffffffu, best, o);
             best = x < best ? x : best;
         }
-        if (lane == 0) red[wid] = best;
+        if (lane == 0) redk[wid] = best;
         __syncthreads();
         if (threadIdx.x == 0) {
             uint64_t b = ~0ull;
-            for (int k = 0; k < (int)(blockDim.x >> 5); ++k) b = red[k] < b ? red[k] : b;
+            for (int k = 0; k < (int)(blockDim.x >> 5); ++k) b = redk[k] < b ? redk[k] : b;
             s_pick[round] = b == ~0ull ? -1 : (int32_t)(b & 0xffffffffu);
             if (b != ~0ull) eligible[s + (b & 0xffffffffu)] = 0;
         }
@@ -782,68 +814,140 @@ __global__ void __launch_bounds__(1024) decode_select_kernel(
 }
 
 // ---------------------------------------------------------------- decode attention
-// grid (row, kv head, split).  lane owns D/32 dims; each warp walks keys,
-// online softmax per query head of the group; partials combined afterwards.
+// Few-row attention for decode steps (engine.py:104-109 _token_rows): grid
+// (row, kv head, split), 4 warps; every warp walks 32-key tiles.  Logits: lane
+// i owns key i of the tile and computes its dot products with the HQ query
+// heads of the group (q in shared memory, fp32).  A tile's softmax statistics
+// take two warp reductions per head; P.V then broadcasts each key's weight
+// and the lane accumulates its 4 output dims from the V row (coalesced 8-byte
+// loads).  All loops over heads/dims are compile-time (HQ, D = 128), so the
+// per-head state stays in registers.
 constexpr int kMaxGroup = 8;
+
+template <int HQ>
 __global__ void __launch_bounds__(128) decode_attn_partial_kernel(
     const __nv_bfloat16 *__restrict__ q, const int32_t *__restrict__ row_req,
     const int32_t *__restrict__ row_pos, int32_t H, const int32_t *__restrict__ kv_len,
     int32_t causal, int32_t layer, ArenaC A, const int32_t *__restrict__ block_table,
     int32_t max_pages, float scale_log2, int32_t n_splits, float *__restrict__ ws) {
+    constexpr int D = 128;
     const int row = blockIdx.x, g = blockIdx.y, split = blockIdx.z;
-    const int D = A.D, G = A.G, hq = H / G, per = D / 32;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    __shared__ __align__(16) float sq[HQ][D];
+    for (int i = threadIdx.x; i < HQ * D; i += blockDim.x)
+        sq[i / D][i % D] = bf2f(q[((int64_t)row * H + g * HQ + i / D) * D + i % D]);
+    __syncthreads();
     const int r = row_req[row];
     const int kend = causal ? row_pos[row] + 1 : kv_len[r];
-    const int span = (kend + n_splits - 1) / n_splits;
+    const int span = (((kend + n_splits - 1) / n_splits) + 31) & ~31;
     const int kb = split * span, ke = min(kend, kb + span);
-    float qv[kMaxGroup][4], acc[kMaxGroup][4], m[kMaxGroup], l[kMaxGroup];
-    for (int hh = 0; hh < hq; ++hh) {
-        for (int e = 0; e < per; ++e) {
-            qv[hh][e] = bf2f(q[((int64_t)row * H + g * hq + hh) * D + lane * per + e]);
-            acc[hh][e] = 0.f;
-        }
+    float m[HQ], l[HQ], acc[HQ][4];
+#pragma unroll
+    for (int hh = 0; hh < HQ; ++hh) {
         m[hh] = -INFINITY;
         l[hh] = 0.f;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[hh][e] = 0.f;
     }
-    for (int k = kb + wid; k < ke; k += 4) {
-        const int64_t page = block_table[(int64_t)r * max_pages + k / A.P];
-        const __nv_bfloat16 *kr = A.row(page, layer, 0, k % A.P) + g * D + lane * per;
-        const __nv_bfloat16 *vr = A.row(page, layer, 1, k % A.P) + g * D + lane * per;
-        float kf[4], vf[4];
-        for (int e = 0; e < per; ++e) { kf[e] = bf2f(kr[e]); vf[e] = bf2f(vr[e]); }
-        for (int hh = 0; hh < hq; ++hh) {
-            float p = 0.f;
-            for (int e = 0; e < per; ++e) p += kf[e] * qv[hh][e];
-            p = warp_sum(p) * scale_log2;
-            const float mn = fmaxf(m[hh], p);
-            const float c = fast_exp2(m[hh] - mn), e2 = fast_exp2(p - mn);
-            l[hh] = l[hh] * c + e2;
-            for (int e = 0; e < per; ++e) acc[hh][e] = acc[hh][e] * c + e2 * vf[e];
-            m[hh] = mn;
+    const int64_t row_elems = (int64_t)A.G * D;
+    for (int t0 = kb + wid * 32; t0 < ke; t0 += 4 * 32) {
+        // a 32-key tile lies in one page (tiles start at multiples of 32):
+        // one page lookup, then every K and V load of the tile in flight
+        const int k = t0 + lane;
+        const bool live = k < ke;
+        const int nkeys = min(32, ke - t0);
+        const int64_t page = block_table[(int64_t)r * max_pages + t0 / A.P];
+        const __nv_bfloat16 *kbase = A.row(page, layer, 0, t0 % A.P) + g * D;
+        const __nv_bfloat16 *vbase = A.row(page, layer, 1, t0 % A.P) + g * D;
+        uint4 kx[D / 8];
+        uint2 vx[32];
+        if (live) {
+            const uint4 *kr = reinterpret_cast<const uint4 *>(kbase + lane * row_elems);
+#pragma unroll
+            for (int c = 0; c < D / 8; ++c) kx[c] = __ldg(kr + c);
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            if (j < nkeys)
+                vx[j] = __ldg(reinterpret_cast<const uint2 *>(vbase + j * row_elems) + lane);
+        // logits of this lane's key for the group's query heads
+        float p[HQ];
+#pragma unroll
+        for (int hh = 0; hh < HQ; ++hh) p[hh] = 0.f;
+        if (live) {
+#pragma unroll
+            for (int c = 0; c < D / 8; ++c) {
+                const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&kx[c]);
+                float kf[8];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float2 f = __bfloat1622float2(h2[u]);
+                    kf[2 * u] = f.x;
+                    kf[2 * u + 1] = f.y;
+                }
+#pragma unroll
+                for (int hh = 0; hh < HQ; ++hh) {
+                    const float4 qa = *reinterpret_cast<const float4 *>(&sq[hh][8 * c]);
+                    const float4 qb = *reinterpret_cast<const float4 *>(&sq[hh][8 * c + 4]);
+                    p[hh] += kf[0] * qa.x + kf[1] * qa.y + kf[2] * qa.z + kf[3] * qa.w +
+                             kf[4] * qb.x + kf[5] * qb.y + kf[6] * qb.z + kf[7] * qb.w;
+                }
+            }
+        }
+#pragma unroll
+        for (int hh = 0; hh < HQ; ++hh) {
+            const float x = live ? p[hh] * scale_log2 : -INFINITY;
+            const float mt = fmaxf(m[hh], warp_max(x));
+            const float c = fast_exp2(m[hh] - mt);
+            p[hh] = live ? fast_exp2(x - mt) : 0.f;
+            l[hh] = l[hh] * c + warp_sum(p[hh]);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) acc[hh][e] *= c;
+            m[hh] = mt;
+        }
+        // P.V: weights broadcast key by key, lane accumulates dims 4*lane..+4
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            if (j >= nkeys) break;
+            const __nv_bfloat162 *v2 = reinterpret_cast<const __nv_bfloat162 *>(&vx[j]);
+            const float2 va = __bfloat1622float2(v2[0]), vb = __bfloat1622float2(v2[1]);
+#pragma unroll
+            for (int hh = 0; hh < HQ; ++hh) {
+                const float w = __shfl_sync(0xffffffffu, p[hh], j);
+                acc[hh][0] += w * va.x;
+                acc[hh][1] += w * va.y;
+                acc[hh][2] += w * vb.x;
+                acc[hh][3] += w * vb.y;
+            }
         }
     }
     // combine the 4 warps through shared memory
-    __shared__ float sm_m[4][kMaxGroup], sm_l[4][kMaxGroup];
-    __shared__ float sm_acc[4][kMaxGroup][128];
-    if (lane == 0)
-        for (int hh = 0; hh < hq; ++hh) { sm_m[wid][hh] = m[hh]; sm_l[wid][hh] = l[hh]; }
-    for (int hh = 0; hh < hq; ++hh)
-        for (int e = 0; e < per; ++e) sm_acc[wid][hh][lane * per + e] = acc[hh][e];
+    __shared__ float sm_m[4][HQ], sm_l[4][HQ];
+    __shared__ __align__(16) float sm_acc[4][HQ][D];
+    if (lane == 0) {
+#pragma unroll
+        for (int hh = 0; hh < HQ; ++hh) { sm_m[wid][hh] = m[hh]; sm_l[wid][hh] = l[hh]; }
+    }
+#pragma unroll
+    for (int hh = 0; hh < HQ; ++hh)
+        *reinterpret_cast<float4 *>(&sm_acc[wid][hh][4 * lane]) =
+            make_float4(acc[hh][0], acc[hh][1], acc[hh][2], acc[hh][3]);
     __syncthreads();
     // ws layout per (row, head, split): [m, l, acc[D]]
-    for (int idx = threadIdx.x; idx < hq * D; idx += blockDim.x) {
+    for (int idx = threadIdx.x; idx < HQ * D; idx += blockDim.x) {
         const int hh = idx / D, d = idx % D;
         float M = -INFINITY;
+#pragma unroll
         for (int w = 0; w < 4; ++w) M = fmaxf(M, sm_m[w][hh]);
         float L = 0.f, S = 0.f;
+#pragma unroll
         for (int w = 0; w < 4; ++w) {
             if (sm_m[w][hh] == -INFINITY) continue;
             const float c = fast_exp2(sm_m[w][hh] - M);
             L += sm_l[w][hh] * c;
             S += sm_acc[w][hh][d] * c;
         }
-        float *o = ws + (((int64_t)row * H + g * hq + hh) * n_splits + split) * (D + 2);
+        float *o = ws + (((int64_t)row * H + g * HQ + hh) * n_splits + split) * (D + 2);
         if (d == 0) { o[0] = M; o[1] = L; }
         o[2 + d] = S;
     }
@@ -871,7 +975,7 @@ __global__ void decode_attn_combine_kernel(const float *__restrict__ ws, int32_t
 static inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
 static int decode_splits(int64_t n_rows, int G, int max_kv) {
-    int64_t want = (2 * kNumSMs + n_rows * G - 1) / (n_rows * G);
+    int64_t want = (8 * kNumSMs + n_rows * G - 1) / (n_rows * G);
     int64_t cap = (max_kv + 127) / 128;
     if (want > cap) want = cap;
     if (want < 1) want = 1;
@@ -921,9 +1025,9 @@ kvs_status kvs_dhd_select(const void *v_true, const float *alpha, const int32_t 
 }
 
 size_t kvs_dhd_decode_select_workspace(int32_t n_req, int32_t num_heads, int32_t max_ctx) {
-    const int64_t chunks = (max_ctx + kDecChunk - 1) / kDecChunk;
+    const size_t tiles = ((size_t)max_ctx + 31) / 32;
     return align256(sizeof(float) * (size_t)n_req * num_heads * max_ctx) +
-           align256(sizeof(float2) * (size_t)n_req * chunks * num_heads);
+           align256(sizeof(float2) * (size_t)n_req * tiles * num_heads);
 }
 
 kvs_status kvs_dhd_decode_select(const void *q_t, int32_t num_heads, const int32_t *ctx_len,
@@ -935,8 +1039,8 @@ kvs_status kvs_dhd_decode_select(const void *q_t, int32_t num_heads, const int32
     KVS_REQUIRE(arena && batch, KVS_EPARAM, "null arena/batch");
     KVS_REQUIRE(num_heads <= 64 && num_heads % arena->kv_heads == 0, KVS_ESHAPE,
                 "num_heads must be <= 64 and a multiple of kv_heads");
-    KVS_REQUIRE(arena->head_dim % 32 == 0 && arena->head_dim <= 256, KVS_ESHAPE,
-                "head_dim must be a multiple of 32 (<= 256)");
+    KVS_REQUIRE(arena->head_dim == 128, KVS_ESHAPE, "head_dim must be 128 (padded heads)");
+    KVS_REQUIRE(num_heads / arena->kv_heads <= 8, KVS_ESHAPE, "num_heads / kv_heads must be <= 8");
     KVS_REQUIRE(n_extra >= 0 && n_extra <= 64, KVS_EPARAM, "n_extra must be in [0, 64]");
     KVS_REQUIRE(ws_bytes >= kvs_dhd_decode_select_workspace(batch->n_req, num_heads, max_ctx),
                 KVS_EPARAM, "workspace too small");
@@ -950,13 +1054,32 @@ kvs_status kvs_dhd_decode_select(const void *q_t, int32_t num_heads, const int32
     float2 *part = (float2 *)((char *)ws + align256(sizeof(float) * (size_t)batch->n_req *
                                                      num_heads * max_ctx));
     const float scale_log2 = softmax_scale * 1.4426950408889634f;
-    const size_t smem = sizeof(float) * num_heads * arena->head_dim;
-    decode_logits_kernel<<<dim3(chunks, batch->n_req), 256, smem, s>>>(
-        (const __nv_bfloat16 *)q_t, num_heads, ctx_len, max_ctx, layer, arena_c(arena),
-        batch->block_table, batch->max_pages, scale_log2, logits, part);
-    decode_select_kernel<<<batch->n_req, 1024, 0, s>>>(num_heads, ctx_len, max_ctx, chunks, logits,
-                                                       part, dv_l1, eligible, batch->req_off,
-                                                       n_extra, chosen, n_chosen, scores);
+    const size_t smem = sizeof(float) * num_heads * 128;
+    const int hq = num_heads / arena->kv_heads;
+    const dim3 grid(chunks, batch->n_req);
+#define KVS_DECODE_LOGITS(HQ)                                                                  \
+    decode_logits_kernel<HQ><<<grid, 256, smem, s>>>((const __nv_bfloat16 *)q_t, num_heads,    \
+                                                     ctx_len, max_ctx, layer, arena_c(arena),  \
+                                                     batch->block_table, batch->max_pages,     \
+                                                     scale_log2, logits, part)
+    switch (hq) {
+        case 1: KVS_DECODE_LOGITS(1); break;
+        case 2: KVS_DECODE_LOGITS(2); break;
+        case 3: KVS_DECODE_LOGITS(3); break;
+        case 4: KVS_DECODE_LOGITS(4); break;
+        case 5: KVS_DECODE_LOGITS(5); break;
+        case 6: KVS_DECODE_LOGITS(6); break;
+        case 7: KVS_DECODE_LOGITS(7); break;
+        default: KVS_DECODE_LOGITS(8); break;
+    }
+#undef KVS_DECODE_LOGITS
+    const size_t sel_smem = sizeof(float) * (size_t)max_ctx;
+    KVS_REQUIRE(sel_smem <= 200 * 1024, KVS_ESHAPE, "decode context longer than 51200 tokens");
+    cudaFuncSetAttribute(decode_select_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sel_smem);
+    decode_select_kernel<<<batch->n_req, 1024, sel_smem, s>>>(
+        num_heads, ctx_len, max_ctx, logits, part, dv_l1, eligible, batch->req_off, n_extra,
+        chosen, n_chosen, scores);
     KVS_CHECK_LAUNCH("kvs_dhd_decode_select");
     return KVS_OK;
 }
@@ -976,7 +1099,7 @@ kvs_status kvs_decode_attention(const void *q, const int32_t *row_req, const int
     const int G = arena->kv_heads, D = arena->head_dim;
     KVS_REQUIRE(num_heads % G == 0 && num_heads / G <= kMaxGroup, KVS_ESHAPE,
                 "num_heads / kv_heads must be <= 8");
-    KVS_REQUIRE(D % 32 == 0 && D <= 128, KVS_ESHAPE, "decode attention needs head_dim <= 128, %% 32");
+    KVS_REQUIRE(D == 128, KVS_ESHAPE, "decode attention needs head_dim == 128 (padded heads)");
     if (n_rows <= 0) return KVS_OK;
     int max_kv = 0;
     for (int64_t k = 0; k < (int64_t)batch->max_pages; ++k) max_kv += arena->page_size;
@@ -985,9 +1108,23 @@ kvs_status kvs_decode_attention(const void *q, const int32_t *row_req, const int
                 KVS_EPARAM, "workspace too small");
     cudaStream_t s = (cudaStream_t)stream;
     const float scale_log2 = softmax_scale * 1.4426950408889634f;
-    decode_attn_partial_kernel<<<dim3((unsigned)n_rows, G, splits), 128, 0, s>>>(
-        (const __nv_bfloat16 *)q, row_req, row_pos, num_heads, kv_len, causal, layer,
-        arena_c(arena), batch->block_table, batch->max_pages, scale_log2, splits, (float *)ws);
+    const dim3 grid((unsigned)n_rows, G, splits);
+    const int hq = num_heads / G;
+#define KVS_DECODE_ATTN(HQ)                                                                    \
+    decode_attn_partial_kernel<HQ><<<grid, 128, 0, s>>>(                                      \
+        (const __nv_bfloat16 *)q, row_req, row_pos, num_heads, kv_len, causal, layer,          \
+        arena_c(arena), batch->block_table, batch->max_pages, scale_log2, splits, (float *)ws)
+    switch (hq) {
+        case 1: KVS_DECODE_ATTN(1); break;
+        case 2: KVS_DECODE_ATTN(2); break;
+        case 3: KVS_DECODE_ATTN(3); break;
+        case 4: KVS_DECODE_ATTN(4); break;
+        case 5: KVS_DECODE_ATTN(5); break;
+        case 6: KVS_DECODE_ATTN(6); break;
+        case 7: KVS_DECODE_ATTN(7); break;
+        default: KVS_DECODE_ATTN(8); break;
+    }
+#undef KVS_DECODE_ATTN
     decode_attn_combine_kernel<<<dim3((unsigned)n_rows, num_heads), 128, 0, s>>>(
         (const float *)ws, num_heads, D, splits, (__nv_bfloat16 *)out);
     KVS_CHECK_LAUNCH("kvs_decode_attention");

@@ -616,10 +616,11 @@ class Engine:
         nch = torch.zeros(R, dtype=torch.int32, device=dev)
         ws = self._ws["dsel"].get(N.ws_bytes("kvs_dhd_decode_select_workspace", R, cfg.num_heads,
                                              max_ctx), dev)
-        N.call("kvs_dhd_decode_select", q_t.data_ptr(), cfg.num_heads, ctx.data_ptr(), max_ctx,
-               st.dv_l1.data_ptr(), st.eligible.data_ptr(), self.probe_layer, self.arena.c,
-               st.batch_c, n_extra, self.scale, chosen.data_ptr(), nch.data_ptr(), None,
-               ws.data_ptr(), ws.numel(), N.stream_ptr())
+        self._timed("dhd_decode", N.call, "kvs_dhd_decode_select", q_t.data_ptr(), cfg.num_heads,
+                    ctx.data_ptr(), max_ctx, st.dv_l1.data_ptr(), st.eligible.data_ptr(),
+                    self.probe_layer, self.arena.c, st.batch_c, n_extra, self.scale,
+                    chosen.data_ptr(), nch.data_ptr(), None, ws.data_ptr(), ws.numel(),
+                    N.stream_ptr())
         ch, nc = chosen.cpu().numpy(), nch.cpu().numpy()
         return [[int(x) for x in ch[r, :nc[r]]] for r in range(R)]
 
