@@ -201,6 +201,7 @@ class Engine:
         self.scratch = _Scratch(self.device)
         self._xb_of = None
         self.layer0_fast = True     # prefill_batch: probe layer 0 doubles as the prefill's
+        self._side = torch.cuda.Stream(self.device) if torch.cuda.is_available() else None
 
     # ------------------------------------------------------------------ helpers
     def reset_timer_events(self, reserve: int = 0):
@@ -452,6 +453,9 @@ class Engine:
         n = rows.n_rows
         alpha = torch.empty(n, dtype=torch.float32, device=dev)
         ws = self._ws["alpha"].get(N.ws_bytes("kvs_dhd_alpha_workspace", n, H, G), dev)
+        if getattr(st, "_gathered", None) is not None:
+            torch.cuda.current_stream().wait_event(st._gathered)     # k_pert complete
+            st._gathered = None
         self._timed("dhd_alpha", N.call, "kvs_dhd_alpha", q1.data_ptr(), H, 1, self.probe_layer, self.arena.c, st.batch_c,
                rows.row_pos.data_ptr(), rows.tiles[0].data_ptr(), rows.tiles[1].data_ptr(),
                rows.tiles[2].data_ptr(), rows.n_tiles, None, self.scale, alpha.data_ptr(),
@@ -529,7 +533,15 @@ class Engine:
             # layers >= 1 gathered first; the probe's fresh layer 0 runs in
             # place and doubles as the partial prefill's layer 0; cached layer-0
             # rows return for the reused, unselected positions after selection
-            self.gather(st, (1, L))
+            # G1 (HBM-bound) runs on a side stream under the probe's layer 0
+            # (tensor-bound); D1 reads layer 1's k_pert, so it waits for it
+            main = torch.cuda.current_stream()
+            self._side.wait_stream(main)
+            with torch.cuda.stream(self._side):
+                self.gather(st, (1, L))
+                gathered = torch.cuda.Event()
+                gathered.record()
+            st._gathered = gathered
             self.probe_and_select(st, ratio, layer0_in_place=True)
             keep = torch.where(st.selected.bool(), torch.full_like(st.src_slot, -1), st.src_slot)
             self.gather(st, (0, 1), slot=keep)
