@@ -5,6 +5,9 @@
 // (K and V rows of every layer copied verbatim from the entry); RoPE is an
 // extension: K is kept post-rotation at the owner's positions
 // and re-aligned by the rotation of (dst_pos - cand_pos).
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace kvs {
@@ -191,6 +194,130 @@ __global__ void __launch_bounds__(256) qkv_rope_scatter_kernel(
                 if (vo) vo[v] = lo[u];
             }
         }
+    }
+}
+
+// Scatter v2 (the one launched): persistent CTAs, each walking rows
+// blockIdx.x + k * gridDim.x.  A row's whole [q | k | v] slice (12 KB at
+// Llama width) arrives with one TMA bulk copy into a kScatSlots-deep shared
+// ring; warp 1 fetches the row's metadata (position, K/V destination) and
+// its cos/sin coefficients into the slot kScatSlots-1 rows ahead, so the
+// 256 consumer threads only read shared memory, rotate, and store.
+constexpr int kScatSlots = 4;
+
+struct ScatMeta {
+    int64_t dst;      // element offset of the row's K in the arena, -1: no K/V write
+    int32_t pos;
+    int32_t pad;
+};
+
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes,
+                                         uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__global__ void __launch_bounds__(256) qkv_scatter2_kernel(
+    const __nv_bfloat16 *__restrict__ qkv, int64_t n_rows, int32_t H, Arena A,
+    const int32_t *__restrict__ row_req, const int32_t *__restrict__ row_pos,
+    const uint8_t *__restrict__ write_kv, int32_t layer, const int32_t *__restrict__ block_table,
+    int32_t max_pages, const float *__restrict__ cos_t, const float *__restrict__ sin_t,
+    __nv_bfloat16 *__restrict__ q_out, __nv_bfloat16 *__restrict__ k_out,
+    __nv_bfloat16 *__restrict__ v_out) {
+    extern __shared__ __align__(128) uint8_t s_rows[];          // kScatSlots x row bytes
+    __shared__ __align__(16) float s_cs[kScatSlots][2][64];
+    __shared__ ScatMeta s_meta[kScatSlots];
+    __shared__ __align__(8) uint64_t bars[kScatSlots];
+    const int G = A.G, D = A.D, chunks = D / 16, vph = D / 8;
+    const int64_t width = (int64_t)(H + 2 * G) * D;
+    const uint32_t row_bytes = (uint32_t)(width * 2);
+    const int tid = threadIdx.x;
+    const int64_t n_mine = n_rows > (int64_t)blockIdx.x
+                               ? (n_rows - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
+    const bool rope = cos_t != nullptr;
+    if (tid == 0) {
+        for (int j = 0; j < kScatSlots; ++j) mbar_init(&bars[j], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    auto stage = [&](int64_t k) {                 // row k of this CTA into slot k % kScatSlots
+        if (k >= n_mine) return;
+        const int slot = (int)(k % kScatSlots);
+        const int64_t row = (int64_t)blockIdx.x + k * gridDim.x;
+        if (tid == 0) {
+            mbar_expect_tx(&bars[slot], row_bytes);
+            bulk_g2s(smem_u32(s_rows) + (uint32_t)slot * row_bytes, qkv + row * width, row_bytes,
+                     &bars[slot]);
+        } else if (tid >= 32 && tid < 64) {
+            const int lane = tid - 32;
+            const int32_t pos = row_pos[row];
+            if (lane == 0) {
+                int64_t dst = -1;
+                if (write_kv == nullptr || write_kv[row] != 0) {
+                    const int64_t page = block_table[(int64_t)row_req[row] * max_pages + pos / A.P];
+                    dst = A.row(page, layer, 0, pos % A.P) - A.base;
+                }
+                s_meta[slot] = ScatMeta{dst, pos, 0};
+            }
+            if (rope) {
+                const float2 c = __ldg(reinterpret_cast<const float2 *>(cos_t + (size_t)pos * 64) + lane);
+                const float2 sn = __ldg(reinterpret_cast<const float2 *>(sin_t + (size_t)pos * 64) + lane);
+                reinterpret_cast<float2 *>(s_cs[slot][0])[lane] = c;
+                reinterpret_cast<float2 *>(s_cs[slot][1])[lane] = sn;
+            }
+        }
+    };
+    for (int j = 0; j < kScatSlots - 1; ++j) stage(j);
+    __syncthreads();
+    const int item0 = q_out != nullptr ? 0 : H * chunks;
+    const int n_rope = (H + G) * chunks, n_items = n_rope + G * vph, vbase = (H + G) * vph;
+    for (int64_t k = 0; k < n_mine; ++k) {
+        const int slot = (int)(k % kScatSlots);
+        stage(k + kScatSlots - 1);                 // refills the slot freed last iteration
+        mbar_wait(&bars[slot], (uint32_t)((k / kScatSlots) & 1));
+        const int64_t row = (int64_t)blockIdx.x + k * gridDim.x;
+        const uint4 *src = reinterpret_cast<const uint4 *>(s_rows + (size_t)slot * row_bytes);
+        const ScatMeta m = s_meta[slot];
+        uint4 *dk = m.dst >= 0 ? reinterpret_cast<uint4 *>(A.base + m.dst) : nullptr;
+        uint4 *dv = m.dst >= 0 ? reinterpret_cast<uint4 *>(A.base + m.dst + (int64_t)A.P * G * D)
+                               : nullptr;
+        uint4 *qo = q_out ? reinterpret_cast<uint4 *>(q_out + row * (int64_t)H * D) : nullptr;
+        uint4 *ko = k_out ? reinterpret_cast<uint4 *>(k_out + row * (int64_t)G * D) : nullptr;
+        uint4 *vo = v_out ? reinterpret_cast<uint4 *>(v_out + row * (int64_t)G * D) : nullptr;
+        const float *cs = s_cs[slot][0], *sn = s_cs[slot][1];
+        for (int it = item0 + tid; it < n_items; it += blockDim.x) {
+            if (it < n_rope) {
+                const int h = it / chunks, c = it % chunks;
+                const int vlo = h * vph + c, vhi = vlo + chunks;
+                uint4 a = src[vlo], b = src[vhi];
+                if (rope) {
+                    const float4 c0 = *reinterpret_cast<const float4 *>(cs + 8 * c);
+                    const float4 c1 = *reinterpret_cast<const float4 *>(cs + 8 * c + 4);
+                    const float4 s0 = *reinterpret_cast<const float4 *>(sn + 8 * c);
+                    const float4 s1 = *reinterpret_cast<const float4 *>(sn + 8 * c + 4);
+                    uint4 lo_o, hi_o;
+                    rope8_reg(a, b, lo_o, hi_o, c0, c1, s0, s1);
+                    a = lo_o;
+                    b = hi_o;
+                }
+                if (h < H) {
+                    qo[vlo] = a;
+                    qo[vhi] = b;
+                } else {
+                    const int kl = vlo - H * vph, kh = vhi - H * vph;
+                    if (dk) { dk[kl] = a; dk[kh] = b; }
+                    if (ko) { ko[kl] = a; ko[kh] = b; }
+                }
+            } else {
+                const int v = it - n_rope;
+                const uint4 x = src[vbase + v];
+                if (dv) dv[v] = x;
+                if (vo) vo[v] = x;
+            }
+        }
+        __syncthreads();                           // slot consumed: the next stage() may refill it
     }
 }
 
@@ -391,11 +518,26 @@ kvs_status kvs_qkv_rope_scatter(const void *qkv, int64_t n_rows, int32_t num_hea
     KVS_REQUIRE(num_heads % arena->kv_heads == 0, KVS_ESHAPE, "num_heads % kv_heads != 0");
     if (n_rows <= 0) return KVS_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    qkv_rope_scatter_kernel<<<(unsigned)n_rows, 256, 0, s>>>(
-        (const __nv_bfloat16 *)qkv, num_heads, make_arena(arena), row_req, row_pos, write_kv, layer,
-        batch->block_table, batch->max_pages, rope ? rope->cos : nullptr,
-        rope ? rope->sin : nullptr, (__nv_bfloat16 *)q_out, (__nv_bfloat16 *)k_out,
-        (__nv_bfloat16 *)v_out);
+    const size_t row_bytes = (size_t)(num_heads + 2 * arena->kv_heads) * arena->head_dim * 2;
+    const size_t smem = kScatSlots * row_bytes;
+    if (arena->head_dim == 128 && smem <= 200 * 1024 && getenv("KVS_SCATTER_V1") == nullptr) {
+        cudaFuncSetAttribute(qkv_scatter2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        int per_sm = 0;
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qkv_scatter2_kernel, 256, smem);
+        const int64_t grid = std::min<int64_t>(n_rows, (int64_t)kNumSMs * std::max(per_sm, 1));
+        qkv_scatter2_kernel<<<(unsigned)grid, 256, smem, s>>>(
+            (const __nv_bfloat16 *)qkv, n_rows, num_heads, make_arena(arena), row_req, row_pos,
+            write_kv, layer, batch->block_table, batch->max_pages, rope ? rope->cos : nullptr,
+            rope ? rope->sin : nullptr, (__nv_bfloat16 *)q_out, (__nv_bfloat16 *)k_out,
+            (__nv_bfloat16 *)v_out);
+    } else {
+        qkv_rope_scatter_kernel<<<(unsigned)n_rows, 256, 0, s>>>(
+            (const __nv_bfloat16 *)qkv, num_heads, make_arena(arena), row_req, row_pos, write_kv,
+            layer, batch->block_table, batch->max_pages, rope ? rope->cos : nullptr,
+            rope ? rope->sin : nullptr, (__nv_bfloat16 *)q_out, (__nv_bfloat16 *)k_out,
+            (__nv_bfloat16 *)v_out);
+    }
     KVS_CHECK_LAUNCH("kvs_qkv_rope_scatter");
     return KVS_OK;
 }
