@@ -29,6 +29,7 @@ _LAZY = {
     "PrefillResult": "session", "GenerationResult": "session", "model_forward": "session",
     "model_forward_with_reuse": "session", "prefill_with_selection": "session",
     "run_generation": "session",
+    "TraceRecord": "serving", "generate_trace": "serving", "run_serving": "serving",
 }
 
 

@@ -110,3 +110,42 @@ def oracle_mode_cases():
 
 if __name__ == "__main__" and "--oracle-mode" in sys.argv:
     oracle_mode_cases()
+
+
+def serving_cases():
+    """golden_serving.json: reference run_simulation (simulate.py:140-215) on
+    generated traces - per request TTFT, completion, hit rate - for the
+    cache-aware and FCFS schedulers and the adaptive / fixed matchers."""
+    import json as _json
+    from kvlab.model import ModelConfig
+    from kvlab.simulate import MatcherKind, SchedulerKind, SimConfig, run_simulation
+    from kvlab.trace import generate_trace
+    out = []
+    for sched in (SchedulerKind.CACHE_AWARE, SchedulerKind.FCFS):
+        for matcher in (MatcherKind.ADAPTIVE, MatcherKind.FIXED):
+            for overlap, gap in ((0.8, 20.0), (0.5, 60.0)):
+                trace = generate_trace(num_requests=10, seed=3, vocab_size=512, overlap=overlap,
+                                       arrival_gap_ms=gap, decode_steps=4)
+                cfg = SimConfig(model=ModelConfig(num_layers=2, num_heads=2, d_model=16,
+                                                  vocab_size=512, seed=1),
+                                batch_size=3, scheduler=sched, matcher=matcher, window_size=4,
+                                chunk_size=8)
+                rep = run_simulation(trace, cfg)
+                out.append({
+                    "scheduler": sched.value, "matcher": matcher.value, "overlap": overlap,
+                    "gap": gap,
+                    "trace": [{"id": r.id, "arrival_ms": r.arrival_ms, "tokens": r.tokens,
+                               "decode_steps": r.decode_steps} for r in trace],
+                    "requests": [{"id": m.id, "ttft_ms": m.ttft_ms,
+                                  "completion_ms": m.completion_ms, "hit_rate": m.hit_rate}
+                                 for m in rep.requests],
+                    "aggregate": {k: rep.aggregate[k] for k in ("mean_ttft_ms", "p50_ttft_ms",
+                                                                "makespan_ms")},
+                })
+    with open(os.path.join(HERE, "golden_serving.json"), "w") as fh:
+        _json.dump(out, fh)
+    print("serving golden:", len(out))
+
+
+if __name__ == "__main__" and "--serving" in sys.argv:
+    serving_cases()

@@ -1,0 +1,67 @@
+"""F2 serving loop (reference simulate.py:140-215) over the GPU engine.
+
+With the reference's LatencyModel the loop must reproduce run_simulation's
+logical clock exactly - per-request TTFT, completion and admission-time hit
+rates from the device lookups, for both schedulers and both matchers
+(golden_serving.json, produced by the reference itself).  With measured
+latency the batches' device times replace f(mean hit)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+CASES = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden_serving.json")))
+
+
+def _engine():
+    import paper_2503_16525_b200 as K
+    from paper_2503_16525_b200.engine import Engine
+    from paper_2503_16525_b200.pool import CachePool
+    cfg = K.ModelConfig(num_layers=2, num_heads=2, d_model=16, vocab_size=512, seed=1)
+    model = K.init_model(cfg)
+    pool = CachePool(cfg, K.HashParams(window_size=4), arena_pages=256)
+    return K, Engine(model, pool)
+
+
+@pytest.mark.parametrize("idx", range(len(CASES)))
+def test_logical_clock_matches_reference(idx):
+    from paper_2503_16525_b200.serving import TraceRecord, run_serving
+    c = CASES[idx]
+    K, eng = _engine()
+    trace = [TraceRecord(r["id"], r["arrival_ms"], r["tokens"], r["decode_steps"])
+             for r in c["trace"]]
+    rep = run_serving(trace, eng, batch_size=3, scheduler=c["scheduler"], matcher=c["matcher"],
+                      chunk_size=8, latency=K.LatencyModel())
+    got = {m.id: m for m in rep.requests}
+    for w in c["requests"]:
+        m = got[w["id"]]
+        assert m.hit_rate == w["hit_rate"]
+        assert m.ttft_ms == w["ttft_ms"]
+        assert m.completion_ms == w["completion_ms"]
+    for k, v in c["aggregate"].items():
+        assert rep.aggregate[k] == pytest.approx(v, rel=1e-12)
+
+
+def test_generate_trace_matches_reference_stream():
+    from paper_2503_16525_b200.serving import generate_trace
+    c = CASES[0]
+    trace = generate_trace(num_requests=10, seed=3, vocab_size=512, overlap=c["overlap"],
+                           arrival_gap_ms=c["gap"], decode_steps=4)
+    assert [r.tokens for r in trace] == [r["tokens"] for r in c["trace"]]
+    assert [r.arrival_ms for r in trace] == [r["arrival_ms"] for r in c["trace"]]
+
+
+def test_measured_latency_run():
+    from paper_2503_16525_b200.serving import generate_trace, run_serving
+    K, eng = _engine()
+    trace = generate_trace(num_requests=12, seed=5, vocab_size=512, overlap=0.7,
+                           arrival_gap_ms=0.5, decode_steps=2)
+    rep = run_serving(trace, eng, batch_size=4)
+    assert len(rep.requests) == 12
+    assert all(m.ttft_ms >= 0 for m in rep.requests)
+    assert all(b[1] == b[2] and b[2] > 0 for b in rep.batches)      # charged == measured
+    assert len(eng.pool.entries) == 12                              # every request written back
+    assert rep.aggregate["throughput_tokens_per_s"] > 0
