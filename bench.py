@@ -309,7 +309,24 @@ def run_gpu(args, rank, world, device):
     res["h2d_bytes"] = args.batch * args.seq * 8
     res["d2h_bytes"] = args.batch * cfg.d_model * 4
     res["decode"] = decode_leg(args, eng, batches[args.warmup], cfg)
+    res["full_recompute_ms"] = full_recompute_leg(args, eng, batches, dev_tokens)
     return res
+
+
+def full_recompute_leg(args, eng, batches, dev_tokens):
+    """The same scheduled batches with no reuse at all (simulate.py FR mode,
+    mode="full": every position through every layer) on the same GPU - the
+    speed-up baseline of SURVEY 8d.  Device ms per step."""
+    import torch
+    eng.release(eng.prefill_batch(batches[0], mode="full", tokens_dev=dev_tokens[0]))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for i in range(args.warmup, args.warmup + args.steps):
+        eng.release(eng.prefill_batch(batches[i], mode="full", tokens_dev=dev_tokens[i]))
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / args.steps
 
 
 def decode_leg(args, eng, batch, cfg, n_tokens: int = 8):
@@ -459,6 +476,10 @@ def main():
         "roofline": roof, "kernels": extra, "gpu_launches": res["launches"] * args.steps,
         "clocks": res["clocks"],
     }
+    if "full_recompute_ms" in res:
+        extra["full_recompute"] = {"ms_per_step": res["full_recompute_ms"],
+                                   "tok_s": args.batch * args.seq * world / (res["full_recompute_ms"] / 1000.0),
+                                   "dhd_speedup": res["full_recompute_ms"] / ms_per_step}
     if "decode" in res:
         dec = res["decode"]
         dec["dhd_decode_select"]["peak"] = hbm
