@@ -46,12 +46,17 @@ def parse():
     ap.add_argument("--hit", type=float, default=0.5)
     ap.add_argument("--ratio", type=float, default=0.2)
     ap.add_argument("--sources", type=int, default=16)
-    ap.add_argument("--layers", type=int, default=32)
+    ap.add_argument("--layers", type=int, default=None, help="default: the shape's own depth")
+    ap.add_argument("--shape", default="llama", choices=["llama", "qwen", "yi"],
+                    help="model shape (BASELINE configs[1] = llama; qwen / yi = configs[2], [3])")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu legs)")
     ap.add_argument("--mode", default="selective", choices=["selective", "full", "naive"])
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo stages the remote-row exchange through the host (1-GPU test)")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.layers is None:
+        args.layers = {"llama": 32, "qwen": 28, "yi": 48}[args.shape]
+    return args
 
 
 # ---------------------------------------------------------------------------- clocks
@@ -148,8 +153,10 @@ def build_engine(args, device, rank=0, world=1):
     from paper_2503_16525_b200.pool import CachePool, KVArena
     from paper_2503_16525_b200.workload import source_requests
 
-    shape = dict(K.LLAMA31_8B)
-    shape["num_layers"] = args.layers
+    shape = dict({"llama": K.LLAMA31_8B, "qwen": K.QWEN25_7B,
+                  "yi": K.YI15_9B}[getattr(args, "shape", "llama")])
+    if getattr(args, "layers", None):
+        shape["num_layers"] = args.layers
     cfg = K.ModelConfig(**shape, seed=0, max_positions=max(8192, args.seq + 64))
     model = K.ToyModel(cfg, device=device, init="device")
     src_pages = args.sources * ((args.seq + 63) // 64)
@@ -398,9 +405,14 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    cfg_doc = {"workload": WORKLOAD, "requests_per_gpu_step": args.batch, "seq_len": args.seq,
+    workload = WORKLOAD if (args.shape, args.seq, args.hit) == ("llama", 4096, 0.5) else (
+        f"{args.shape}-shape DHD prefill, {args.seq}-token requests, {args.hit:.0%} chunk hit, "
+        f"r={args.ratio}")
+    cfg_doc = {"workload": workload, "requests_per_gpu_step": args.batch, "seq_len": args.seq,
                "hit_rate": args.hit, "recompute_ratio": args.ratio, "pool_sources": args.sources,
-               "layers": args.layers, "model_shape": "llama3.1-8b attention stack (no FFN)",
+               "layers": args.layers,
+               "model_shape": {"llama": "llama3.1-8b", "qwen": "qwen2.5-7b",
+                               "yi": "yi1.5-9b"}[args.shape] + " attention stack (no FFN)",
                "parallelism": f"dp{args.gpus} (requests partitioned, per-GPU pool)",
                "l2": "inputs larger than L2 (2.7 GB weights + 4 GiB KV streamed per step)"}
     if args.impl == "reference":
