@@ -587,6 +587,10 @@ constexpr int RING3 = 5;
 #define KVS_POLY_EVERY 0
 #endif
 constexpr int kPolyEvery = KVS_POLY_EVERY;   // 1 in kPolyEvery exp2 pairs emulated (0: none)
+#ifndef KVS_PINGPONG
+#define KVS_PINGPONG 1
+#endif
+constexpr bool kPingPong = KVS_PINGPONG != 0;    // alternate the two heads' exp phases
 
 struct Smem3 {
     uint64_t q_full;
@@ -728,70 +732,106 @@ __global__ void __launch_bounds__(kThreads2, 1)
             tmem_ld_wait();
             if (i == 0) TRACE(21 + 10 * t, kb);
             const int kbase = kb * BN;
-            float mx[8];
+            if (kbase + BN > kend) {                      // boundary block: position mask
 #pragma unroll
-            for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
-            if (kbase + BN <= kend) {
+                for (int c = 0; c < BN; ++c) s[c] = (kbase + c < kend) ? s[c] : -INFINITY;
+            }
+            float ls[8];
+            // exponentials against mu, P (bf16) written over S; optionally the
+            // block's row max is tracked in the same pass
+            auto exp_pass = [&](float mu, bool track, float &bmax) {
+                float mx[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    ls[j] = 0.f;
+                    mx[j] = -INFINITY;
+                }
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf) {
+                    uint32_t pk[32];
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) {
+                        const float s0 = s[hf * 64 + 2 * q], s1 = s[hf * 64 + 2 * q + 1];
+                        if (track) mx[q & 7] = fmaxf(mx[q & 7], fmaxf(s0, s1));
+                        const float x0 = fmaf(s0, p.scale_log2, -mu);
+                        const float x1 = fmaf(s1, p.scale_log2, -mu);
+                        // every kPolyEvery-th pair on the FMA pipe, the rest on MUFU
+                        const bool poly = kPolyEvery > 0 &&
+                                          q % (kPolyEvery > 0 ? kPolyEvery : 1) == kPolyEvery - 1;
+                        const float e0 = poly ? exp2_poly(x0) : fast_exp2(x0);
+                        const float e1 = poly ? exp2_poly(x1) : fast_exp2(x1);
+                        ls[(2 * q) & 7] += e0;
+                        ls[(2 * q + 1) & 7] += e1;
+                        pk[q] = pack_bf16x2(e0, e1);
+                    }
+                    tmem_st32(tS + hf * 32, reinterpret_cast<const float *>(pk));
+                }
+                if (track)
+                    bmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+            };
+            auto row_max = [&]() {
+                float mx[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
 #pragma unroll
                 for (int c = 0; c < BN; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
+                return fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                             fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+            };
+            // lazy rescale: raise the running max m only when the block's max
+            // exceeds it by > 2^8, rescaling O (warp-collective tcgen05 ops)
+            auto rescale = [&](float mloc) {
+                const bool grow = mloc > m + kRescaleThreshold || (m == -INFINITY && mloc > -INFINITY);
+                const bool touch_o = grow && kb >= 1 && m != -INFINITY;
+                float factor = 1.f;
+                if (grow) {
+                    factor = (m == -INFINITY) ? 0.f : fast_exp2(m - mloc);
+                    l *= factor;
+                    m = mloc;
+                }
+                if (__any_sync(0xffffffffu, touch_o)) {
+                    // PV_t(kb-1) retired before QK_t(kb) (in-order), so O is quiescent
+                    const float f = touch_o ? factor : 1.f;
+                    float o[32];
+#pragma unroll
+                    for (int c = 0; c < HD / 32; ++c) {
+                        tmem_ld32(tO + c * 32, o);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) o[e] *= f;
+                        tmem_st32(tO + c * 32, o);
+                    }
+                }
+            };
+            // ping-pong: the two heads' exponential phases alternate on the
+            // shared MUFU pipe (16 lanes/clk/SM)
+            if (kPingPong && (t == 1 || kb > 0))
+                asm volatile("bar.sync %0, 256;" ::"r"(1 + t) : "memory");
+            if (i == 0) TRACE(24 + 10 * t, kb);           // exp phase starts
+            float bmax = -INFINITY;
+            if (__all_sync(0xffffffffu, m != -INFINITY)) {
+                // speculative pass against the running max (the common case:
+                // no row's max grows by > 2^8), max tracked alongside; rows
+                // that do grow make the warp redo the block with the new max
+                exp_pass(m, true, bmax);
+                if (__any_sync(0xffffffffu, bmax * p.scale_log2 > m + kRescaleThreshold)) {
+                    rescale(bmax * p.scale_log2);
+                    exp_pass(m, false, bmax);
+                }
             } else {
-#pragma unroll
-                for (int c = 0; c < BN; ++c) {
-                    s[c] = (kbase + c < kend) ? s[c] : -INFINITY;
-                    mx[c & 7] = fmaxf(mx[c & 7], s[c]);
-                }
+                rescale(row_max() * p.scale_log2);
+                exp_pass((m == -INFINITY) ? 0.f : m, false, bmax);
             }
-            const float mloc = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                     fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) *
-                               p.scale_log2;
-            const bool grow = mloc > m + kRescaleThreshold || (m == -INFINITY && mloc > -INFINITY);
-            const bool touch_o = grow && kb >= 1 && m != -INFINITY;
-            float factor = 1.f;
-            if (grow) {
-                factor = (m == -INFINITY) ? 0.f : fast_exp2(m - mloc);
-                l *= factor;
-                m = mloc;
-            }
-            if (__any_sync(0xffffffffu, touch_o)) {     // warp-collective tcgen05.ld/st
-                // PV_t(kb-1) retired before QK_t(kb) (in-order), so O is quiescent
-                const float f = touch_o ? factor : 1.f;
-                float o[32];
-#pragma unroll
-                for (int c = 0; c < HD / 32; ++c) {
-                    tmem_ld32(tO + c * 32, o);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) o[e] *= f;
-                    tmem_st32(tO + c * 32, o);
-                }
-            }
-            const float mu = (m == -INFINITY) ? 0.f : m;
-            float ls[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) ls[j] = 0.f;
-#pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                uint32_t pk[32];
-#pragma unroll
-                for (int q = 0; q < 32; ++q) {
-                    const float x0 = fmaf(s[hf * 64 + 2 * q], p.scale_log2, -mu);
-                    const float x1 = fmaf(s[hf * 64 + 2 * q + 1], p.scale_log2, -mu);
-                    // every kPolyEvery-th pair on the FMA pipe, the rest on MUFU
-                    const bool poly = kPolyEvery > 0 && q % (kPolyEvery > 0 ? kPolyEvery : 1) == kPolyEvery - 1;
-                    const float e0 = poly ? exp2_poly(x0) : fast_exp2(x0);
-                    const float e1 = poly ? exp2_poly(x1) : fast_exp2(x1);
-                    ls[(2 * q) & 7] += e0;
-                    ls[(2 * q + 1) & 7] += e1;
-                    pk[q] = pack_bf16x2(e0, e1);
-                }
-                tmem_st32(tS + hf * 32, reinterpret_cast<const float *>(pk));
-            }
+            if (i == 0) TRACE(25 + 10 * t, kb);           // exp phase + P stores issued
+            if (kPingPong) asm volatile("bar.arrive %0, 256;" ::"r"(2 - t) : "memory");
             l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
             tmem_st_wait();
             if (i == 0) TRACE(22 + 10 * t, kb);
             tc_fence_before();
             mbar_arrive(&sh.p_full[t]);
         }
+        if (kPingPong && t == 0 && n_kb >= 1) asm volatile("bar.sync 1, 256;" ::: "memory");
         const int64_t grow = (int64_t)row0 + i;
         if (n_kb >= 1) mbar_wait(&sh.pv_done[t], (uint32_t)(n_kb - 1) & 1u);
         tc_fence_after();
@@ -822,6 +862,242 @@ __global__ void __launch_bounds__(kThreads2, 1)
     tc_fence_before();
     __syncthreads();
     if (warp == 9) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
+// ------------------------------------------------------------------ A1, one head, S double-buffered
+// One query head per CTA; TMEM holds S0 | S1 | O (128 fp32 columns each).
+// The softmax writes P (bf16) over the S buffer it read and O += P.V runs
+// with A from tensor memory.  The MMA warp issues QK(kb+1) into the other S
+// buffer right after PV(kb-1), so the next block's scores are computed while
+// the softmax of this block runs and the softmax warps work back to back;
+// in-order tcgen05 execution keeps QK(kb+2) behind PV(kb), which reads P(kb)
+// from the same buffer.  Single softmax warpgroup: each warp owns its SMSP's
+// MUFU.  K/V ring of 6 tiles (K(kb), V(kb), ...), 1 CTA per SM.
+constexpr int RING6 = 6;
+constexpr int kThreads6 = 192;
+
+struct Smem6 {
+    uint64_t q_full;
+    uint64_t ring_full[RING6], ring_empty[RING6];
+    uint64_t s_full[2], p_full[2], pv_done[2];
+    uint32_t tmem_base;
+};
+
+__global__ void __launch_bounds__(kThreads6, 1)
+    fwd6_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
+                Params p) {
+    extern __shared__ uint8_t dsmem[];
+    __shared__ Smem6 sh;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int tile = blockIdx.y, h = blockIdx.x;
+    const int g = h / (p.num_heads / p.kv_heads);
+    const int req = p.tile_req[tile], row0 = p.tile_row0[tile], nrows = p.tile_rows[tile];
+    const int kmax = p.causal ? p.row_pos[row0 + nrows - 1] + 1 : p.kv_len[req];
+    const int n_kb = (kmax + BN - 1) / BN;
+    const int pages_needed = (kmax + p.page_size - 1) / p.page_size;
+
+    const uint32_t base = align1024(smem_u32(dsmem));
+    const uint32_t sQ = base;                          // 1 tile
+    const uint32_t sR = sQ + TILE_BYTES;               // RING6 tiles
+    uint8_t *gbase = dsmem + (base - smem_u32(dsmem));
+
+    if (threadIdx.x == 0) {
+        mbar_init(&sh.q_full, 1);
+        for (int i = 0; i < RING6; ++i) {
+            mbar_init(&sh.ring_full[i], 1);
+            mbar_init(&sh.ring_empty[i], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&sh.s_full[i], 1);
+            mbar_init(&sh.p_full[i], 128);
+            mbar_init(&sh.pv_done[i], 1);
+        }
+        fence_barrier_init();
+    }
+    if (warp == 5) tmem_alloc(&sh.tmem_base, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sh.tmem_base;
+
+    if (warp == 4) {
+        if (lane == 0) {
+            tma_prefetch(&map_q);
+            tma_prefetch(&map_kv);
+            mbar_expect_tx(&sh.q_full, TILE_BYTES);
+            for (int hf = 0; hf < 2; ++hf)
+                tma_load_3d(gbase + (sQ - base) + hf * HALF_BYTES, &map_q, &sh.q_full, hf * 64, h,
+                            row0);
+            const int32_t *bt = p.block_table + (int64_t)req * p.max_pages;
+            for (int it = 0; it < 2 * n_kb; ++it) {
+                const int kb = it >> 1, kv = it & 1, slot = it % RING6;
+                if (it >= RING6) mbar_wait(&sh.ring_empty[slot], (uint32_t)((it / RING6) - 1) & 1u);
+                mbar_expect_tx(&sh.ring_full[slot], TILE_BYTES);
+                for (int q = 0; q < 2; ++q) {
+                    const int pi = 2 * kb + q;
+                    const int pg = bt[pi < pages_needed ? pi : 2 * kb];
+                    for (int hf = 0; hf < 2; ++hf)
+                        tma_load_4d(gbase + (sR - base) + slot * TILE_BYTES + hf * HALF_BYTES +
+                                        q * (HALF_BYTES / 2),
+                                    &map_kv, &sh.ring_full[slot], hf * 64, g, 0,
+                                    (pg * p.num_layers + p.layer) * 2 + kv);
+                }
+            }
+        }
+    } else if (warp == 5) {
+        if (lane == 0) {
+            const uint32_t idesc_qk = umma_idesc_bf16(BM, BN, false);
+            const uint32_t idesc_pv = umma_idesc_bf16(BM, HD, true);
+            mbar_wait(&sh.q_full, 0);
+            auto issue_qk = [&](int kb) {
+                const int it = 2 * kb, slot = it % RING6, b = kb & 1;
+                mbar_wait(&sh.ring_full[slot], (uint32_t)(it / RING6) & 1u);
+                tc_fence_after();
+#pragma unroll
+                for (int k = 0; k < HD / 16; ++k) {
+                    const uint64_t da =
+                        umma_desc_sw128(sQ + (k >> 2) * HALF_BYTES + (k & 3) * 32, 16, 1024);
+                    const uint64_t db = umma_desc_sw128(
+                        sR + slot * TILE_BYTES + (k >> 2) * HALF_BYTES + (k & 3) * 32, 16, 1024);
+                    umma_bf16(tmem + 128 * b, da, db, idesc_qk, k > 0 ? 1u : 0u);
+                }
+                umma_commit(&sh.s_full[b]);
+                umma_commit(&sh.ring_empty[slot]);
+            };
+            auto issue_pv = [&](int kb) {
+                const int it = 2 * kb + 1, slot = it % RING6, b = kb & 1;
+                mbar_wait(&sh.p_full[b], (uint32_t)(kb >> 1) & 1u);
+                mbar_wait(&sh.ring_full[slot], (uint32_t)(it / RING6) & 1u);
+                tc_fence_after();
+#pragma unroll
+                for (int k = 0; k < BN / 16; ++k) {
+                    const uint64_t db = umma_desc_sw128(sR + slot * TILE_BYTES + k * 2048,
+                                                        HALF_BYTES, 1024);
+                    umma_bf16_ts(tmem + 256, tmem + 128 * b + 8 * k, db, idesc_pv,
+                                 (kb > 0 || k > 0) ? 1u : 0u);
+                }
+                umma_commit(&sh.pv_done[b]);
+                umma_commit(&sh.ring_empty[slot]);
+            };
+            // QK(0), QK(1), PV(0), QK(2), PV(1), ...: QK(kb+1) runs under softmax(kb)
+            if (n_kb >= 1) issue_qk(0);
+            for (int kb = 0; kb < n_kb; ++kb) {
+                if (kb + 1 < n_kb) issue_qk(kb + 1);
+                issue_pv(kb);
+            }
+        }
+        __syncwarp();
+    } else {
+        const int i = threadIdx.x;               // row within tile == TMEM lane
+        const bool valid = i < nrows;
+        const int kend = !valid ? 0 : (p.causal ? p.row_pos[row0 + i] + 1 : kmax);
+        const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+        const uint32_t tO = tmem + 256 + lane_off;
+        float m = -INFINITY, l = 0.f;
+        float s[BN];
+        for (int kb = 0; kb < n_kb; ++kb) {
+            const int b = kb & 1;
+            const uint32_t tS = tmem + 128 * b + lane_off;
+            mbar_wait(&sh.s_full[b], (uint32_t)(kb >> 1) & 1u);
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS + c * 32, s + c * 32);
+            tmem_ld_wait();
+            const int kbase = kb * BN;
+            float mx[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
+            if (kbase + BN <= kend) {
+#pragma unroll
+                for (int c = 0; c < BN; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
+            } else {
+#pragma unroll
+                for (int c = 0; c < BN; ++c) {
+                    s[c] = (kbase + c < kend) ? s[c] : -INFINITY;
+                    mx[c & 7] = fmaxf(mx[c & 7], s[c]);
+                }
+            }
+            const float mloc = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                     fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) *
+                               p.scale_log2;
+            const bool grow = mloc > m + kRescaleThreshold || (m == -INFINITY && mloc > -INFINITY);
+            const bool touch_o = grow && kb >= 1 && m != -INFINITY;
+            float factor = 1.f;
+            if (grow) {
+                factor = (m == -INFINITY) ? 0.f : fast_exp2(m - mloc);
+                l *= factor;
+                m = mloc;
+            }
+            if (__any_sync(0xffffffffu, touch_o)) {     // warp-collective tcgen05.ld/st
+                // PV(kb-1) may still run: O is touched only after it retired
+                mbar_wait(&sh.pv_done[(kb - 1) & 1], (uint32_t)((kb - 1) >> 1) & 1u);
+                tc_fence_after();
+                const float f = touch_o ? factor : 1.f;
+                float o[32];
+#pragma unroll
+                for (int c = 0; c < HD / 32; ++c) {
+                    tmem_ld32(tO + c * 32, o);
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) o[e] *= f;
+                    tmem_st32(tO + c * 32, o);
+                }
+                tmem_st_wait();
+            }
+            const float mu = (m == -INFINITY) ? 0.f : m;
+            float ls[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) ls[j] = 0.f;
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                uint32_t pk[32];
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                    const float e0 = fast_exp2(fmaf(s[hf * 64 + 2 * q], p.scale_log2, -mu));
+                    const float e1 = fast_exp2(fmaf(s[hf * 64 + 2 * q + 1], p.scale_log2, -mu));
+                    ls[(2 * q) & 7] += e0;
+                    ls[(2 * q + 1) & 7] += e1;
+                    pk[q] = pack_bf16x2(e0, e1);
+                }
+                tmem_st32(tS + hf * 32, reinterpret_cast<const float *>(pk));
+            }
+            l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&sh.p_full[b]);
+        }
+        const int64_t grow = (int64_t)row0 + i;
+        if (n_kb >= 1) mbar_wait(&sh.pv_done[(n_kb - 1) & 1], (uint32_t)((n_kb - 1) >> 1) & 1u);
+        tc_fence_after();
+        const float inv = l > 0.f ? 1.f / l : 0.f;
+        float o[32];
+#pragma unroll
+        for (int c = 0; c < HD / 32; ++c) {
+            tmem_ld32(tO + c * 32, o);
+            tmem_ld_wait();
+            if (valid) {
+                uint4 *dst = reinterpret_cast<uint4 *>(p.out + (grow * p.num_heads + h) * HD + c * 32);
+#pragma unroll
+                for (int v = 0; v < 4; ++v) {
+                    uint4 w;
+                    w.x = pack_bf16x2(o[8 * v + 0] * inv, o[8 * v + 1] * inv);
+                    w.y = pack_bf16x2(o[8 * v + 2] * inv, o[8 * v + 3] * inv);
+                    w.z = pack_bf16x2(o[8 * v + 4] * inv, o[8 * v + 5] * inv);
+                    w.w = pack_bf16x2(o[8 * v + 6] * inv, o[8 * v + 7] * inv);
+                    dst[v] = w;
+                }
+            }
+        }
+        if (valid && p.lse != nullptr)
+            p.lse[grow * p.num_heads + h] =
+                (l > 0.f) ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
         tc_fence_after();
         tmem_dealloc(tmem, 512);
     }
@@ -1299,7 +1575,12 @@ kvs_status kvs_attention_fwd(const void *q, const int32_t *row_pos, int64_t n_ro
     cudaStream_t s = (cudaStream_t)stream;
     const int group = num_heads / arena->kv_heads;
     const char *variant = getenv("KVS_ATTN");
-    if (out != nullptr && group % 2 == 0 && variant != nullptr && variant[0] == '4') {
+    if (out != nullptr && variant != nullptr && variant[0] == '6') {
+        const size_t smem = 1024 + attn::TILE_BYTES * (1 + attn::RING6);
+        cudaFuncSetAttribute(attn::fwd6_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        attn::fwd6_kernel<<<dim3(num_heads, n_tiles), attn::kThreads6, smem, s>>>(mq, mkv, p);
+    } else if (out != nullptr && group % 2 == 0 && variant != nullptr && variant[0] == '4') {
         const size_t smem = 1024 + 2 * attn::TILE_BYTES + attn::RING4 * attn::TILE4;
         cudaFuncSetAttribute(attn::fwd4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);

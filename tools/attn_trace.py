@@ -76,3 +76,8 @@ print(f"softmax b: S ready -> S loaded {avg(d(30, 0, 31, 0)):.0f}, S loaded -> P
 print(f"P stored a -> mma sees p_full a {avg(d(22, 0, 11, 0)):.0f}; p_full a -> QK_a issue {avg(d(11, 0, 13, 0)):.0f}; QK_a issue -> S ready a(kb+1) {avg(d(13, 0, 20, 1)):.0f}")
 print(f"P stored b -> mma sees p_full b {avg(d(32, 0, 12, 0)):.0f}; p_full b -> QK_b issue {avg(d(12, 0, 14, 0)):.0f}; QK_b issue -> S ready b(kb+1) {avg(d(14, 0, 30, 1)):.0f}")
 print(f"softmax a start vs b start offset: {avg(d(20, 0, 30, 0)):.0f}")
+for t, base in (("a", 20), ("b", 30)):
+    print(f"softmax {t}: loaded->max done {avg(d(base + 1, 0, base + 3, 0)):.0f}, "
+          f"max->exp start {avg(d(base + 3, 0, base + 4, 0)):.0f}, "
+          f"exp phase {avg(d(base + 4, 0, base + 5, 0)):.0f}, "
+          f"exp end->P stored(wait st) {avg(d(base + 5, 0, base + 2, 0)):.0f}")
