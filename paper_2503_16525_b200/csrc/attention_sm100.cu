@@ -1575,22 +1575,25 @@ kvs_status kvs_attention_fwd(const void *q, const int32_t *row_pos, int64_t n_ro
     cudaStream_t s = (cudaStream_t)stream;
     const int group = num_heads / arena->kv_heads;
     const char *variant = getenv("KVS_ATTN");
-    if (out != nullptr && variant != nullptr && variant[0] == '6') {
+    // default: head pairs (fwd3) for even GQA groups, single heads with
+    // double-buffered S (fwd6) otherwise; KVS_ATTN=1|2|4|6 pins a variant
+    const char v = variant != nullptr ? variant[0] : (group % 2 == 0 ? '3' : '6');
+    if (out != nullptr && (v == '6' || (v != '1' && group % 2 != 0))) {
         const size_t smem = 1024 + attn::TILE_BYTES * (1 + attn::RING6);
         cudaFuncSetAttribute(attn::fwd6_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         attn::fwd6_kernel<<<dim3(num_heads, n_tiles), attn::kThreads6, smem, s>>>(mq, mkv, p);
-    } else if (out != nullptr && group % 2 == 0 && variant != nullptr && variant[0] == '4') {
+    } else if (out != nullptr && group % 2 == 0 && v == '4') {
         const size_t smem = 1024 + 2 * attn::TILE_BYTES + attn::RING4 * attn::TILE4;
         cudaFuncSetAttribute(attn::fwd4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         attn::fwd4_kernel<<<dim3(num_heads / 2, n_tiles), attn::kThreads2, smem, s>>>(mq, mkv, p);
-    } else if (out != nullptr && group % 2 == 0 && (variant == nullptr || variant[0] == '3')) {
+    } else if (out != nullptr && group % 2 == 0 && v == '3') {
         const size_t smem = 1024 + attn::TILE_BYTES * (2 + attn::RING3);
         cudaFuncSetAttribute(attn::fwd3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         attn::fwd3_kernel<<<dim3(num_heads / 2, n_tiles), attn::kThreads2, smem, s>>>(mq, mkv, p);
-    } else if (out != nullptr && group % 2 == 0 && variant[0] == '2') {
+    } else if (out != nullptr && group % 2 == 0 && v == '2') {
         const size_t smem = 1024 + attn::TILE_BYTES * (2 + attn::RING + 2);
         cudaFuncSetAttribute(attn::fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);

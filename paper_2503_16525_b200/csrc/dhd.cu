@@ -8,6 +8,8 @@
 // D3 follows select_decode_step (selection.py:80-105): unmasked softmax of
 //   q_t . K over the whole current context per query head, mean over heads,
 //   times the prefill dv-L1, top n_extra over the eligible rows.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace kvs {
@@ -275,12 +277,40 @@ __device__ __noinline__ void select_request(const float *__restrict__ score, con
     }
 }
 
-// Register-resident selection for requests of up to kRegKeys positions: each
-// thread holds its keys (i = tid + 256k), 4 radix passes with per-warp
-// histograms (one aggregated atomic per warp instruction for the dominant
-// digit), and the tie band at the threshold is resolved in position order
-// only when it is actually split (rare: scores are continuous).
-constexpr int kKPT = 16;
+// Diagnostic phase timeline (KVS_SEL_TRACE builds only): %globaltimer stamps
+// per CTA, read back with kvs_sel_trace_dump().
+#ifdef KVS_SEL_TRACE
+__device__ unsigned long long g_sel_trace[1024 * 8];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define SEL_TRACE(ph) \
+    do { if (threadIdx.x == 0 && blockIdx.x < 1024) g_sel_trace[blockIdx.x * 8 + (ph)] = gtimer(); } while (0)
+#else
+#define SEL_TRACE(ph) do {} while (0)
+#endif
+
+// Selection of one request's top-B (selection.py:63-77) by one CTA, keys in
+// shared memory (position i at keys[i]).  Key = ~bits(score): ascending key
+// = descending score; bit 31 is set for every reused row and non-reused rows
+// are 0xFFFFFFFF.  Digits below bit 31: the 8 exponent bits, then 8 + 8 + 7
+// mantissa bits.
+//   pass 0  exponent digit, per-warp histograms (scores cluster in a few
+//           exponents, so one aggregated atomic counts most of a warp)
+//   then    the threshold exponent's rows are compacted to l1 (key, pos);
+//           the next digit is counted there with ballots into per-lane
+//           registers (no shared atomics on spread digits); the rows
+//           sharing the resulting 17-bit prefix (within 2^-8 of the B-th
+//           score; typically a handful) are ranked pairwise by (key, pos),
+//           which is the reference's ascending-position tie rule
+//   else    (many near-ties or no room) the remaining digits over all keys
+//           and an ordered tie pass.
+// The code is kept small on purpose: only the last CTAs of the fused launch
+// run it, cold, and instruction fetch dominated an unrolled version.
+constexpr int kPairCap = 256;     // threshold-digit rows ranked pairwise
+constexpr int kKPT = 16;          // register keys per thread
 constexpr int kRegKeys = kKPT * kSelThreads;
 
 template <bool kReg>
@@ -288,71 +318,109 @@ __device__ __noinline__ void select_fast(const float *__restrict__ score,
                                          const int32_t *__restrict__ src_slot, int64_t s, int64_t n,
                                          int32_t B, uint8_t *__restrict__ selected,
                                          uint32_t *whist /* [8][256] */, uint32_t *keys /* n, smem */,
-                                         uint32_t *sh) {
+                                         uint32_t *sh, uint2 *l1 /* smem */, int l1_cap,
+                                         const uint32_t *__restrict__ pkeys /* nullable */) {
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     constexpr int NW = kSelThreads / 32;
     __shared__ uint32_t wsum[NW];
-    // key of position tid + 256k: descending score, non-reused rows largest
+    __shared__ uint2 cand[kPairCap];
+    __shared__ uint32_t s_nc;
+    // keys of positions tid + 256k: registers (kReg, n <= kRegKeys) or smem
     const int nk = kReg ? kKPT : (int)((n + kSelThreads - 1) / kSelThreads);
     uint32_t kr[kReg ? kKPT : 1];
-    auto key_of = [&](float sc, int32_t sl) -> uint32_t {
-        const uint32_t x = ~__float_as_uint(fmaxf(sc, 0.f));
-        return sl < 0 ? 0xFFFFFFFFu : (x < 0xFFFFFFFEu ? x : 0xFFFFFFFEu);
-    };
-    if constexpr (kReg) {
-        int32_t sl[kKPT];
-        float sc[kKPT];
+#pragma unroll(kReg ? 1 : 1)
+    for (int k0 = 0; k0 < nk; k0 += 16) {
+        uint32_t v[16];
 #pragma unroll
-        for (int k = 0; k < kKPT; ++k) {
-            const int64_t i = tid + (int64_t)k * kSelThreads;
-            sl[k] = i < n ? __ldcg(src_slot + s + i) : -1;
-            sc[k] = i < n ? __ldcg(score + s + i) : 0.f;
-        }
-#pragma unroll
-        for (int k = 0; k < kKPT; ++k) kr[k] = key_of(sc[k], sl[k]);
-    } else {
-        for (int k0 = 0; k0 < nk; k0 += 8) {
-            int32_t sl[8];
-            float sc[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const int64_t i = tid + (int64_t)(k0 + u) * kSelThreads;
-                sl[u] = i < n ? __ldcg(src_slot + s + i) : -1;
-                sc[u] = i < n ? __ldcg(score + s + i) : 0.f;
+        for (int u = 0; u < 16; ++u) {
+            const int64_t i = tid + (int64_t)(k0 + u) * kSelThreads;
+            if (pkeys != nullptr) {
+                v[u] = i < n ? __ldcg(pkeys + s + i) : 0xFFFFFFFFu;
+            } else {
+                const int32_t sl = i < n ? __ldcg(src_slot + s + i) : -1;
+                const float sc = i < n ? __ldcg(score + s + i) : 0.f;
+                const uint32_t x = ~__float_as_uint(fmaxf(sc, 0.f));
+                v[u] = sl < 0 ? 0xFFFFFFFFu : (x < 0xFFFFFFFEu ? x : 0xFFFFFFFEu);
             }
+        }
+        if constexpr (kReg) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (k0 + u < nk) keys[tid + (k0 + u) * kSelThreads] = key_of(sc[u], sl[u]);
+            for (int u = 0; u < 16; ++u) kr[u] = v[u];
+        } else {
+#pragma unroll
+            for (int u = 0; u < 16; ++u)
+                if (k0 + u < nk) keys[tid + (k0 + u) * kSelThreads] = v[u];
         }
     }
-#define KEY(k) (kReg ? kr[(k) < kKPT ? (k) : 0] : keys[tid + (k) * kSelThreads])
+    if constexpr (!kReg) __syncthreads();
+    SEL_TRACE(5);
+#define KEY(k) (kReg ? kr[(k) < kKPT ? (k) : 0] : ((k) < nk ? keys[tid + (k) * kSelThreads] : 0xFFFFFFFFu))
     if (B <= 0) {
         for (int64_t i = tid; i < n; i += kSelThreads) selected[s + i] = 0;
         return;
     }
-    uint32_t prefix = 0, mask = 0, need = (uint32_t)B;
+    uint32_t prefix = 0x80000000u, mask = 0x80000000u, need = (uint32_t)B;
     uint32_t *wh = whist + wid * 256;
+    bool compact = false;
+    int n1 = 0;
+#pragma unroll 1
     for (int pass = 0; pass < 4; ++pass) {
-        const int shift = 24 - 8 * pass;
+        const int shift = pass == 0 ? 23 : pass == 1 ? 15 : pass == 2 ? 7 : 0;
+        const uint32_t dmask = pass == 3 ? 0x7fu : 0xffu;
+        if (compact) {
+            // lane L counts digits 8L..8L+7 of the compacted rows from ballots
+            uint32_t cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll 1
+            for (int a0 = wid * 32; a0 < n1; a0 += kSelThreads) {
+                const int a = a0 + lane;
+                const uint32_t d = a < n1 ? (l1[a].x >> shift) & dmask : 0u;
+                const uint32_t inb = __ballot_sync(0xffffffffu, a < n1);
+                uint32_t bb[8];
 #pragma unroll
-        for (int w = 0; w < NW; ++w) whist[w * 256 + tid] = 0;
-        __syncthreads();
-#pragma unroll(kReg ? kKPT : 1)
-        for (int k = 0; k < nk; ++k) {
-            const uint32_t key = KEY(k);
-            const bool in = key != 0xFFFFFFFFu && (key & mask) == prefix;
-            const uint32_t bin = (key >> shift) & 0xff;
-            const uint32_t act = __ballot_sync(0xffffffffu, in);
-            if (act == 0) continue;
-            // scores cluster in a few digits (same exponent): the first active
-            // lane's digit is counted with one atomic, the others individually
-            const int first = __ffs(act) - 1;
-            const uint32_t lead = __shfl_sync(0xffffffffu, bin, first);
-            const uint32_t same = __ballot_sync(0xffffffffu, in && bin == lead);
-            if (lane == first) atomicAdd(&wh[lead], (uint32_t)__popc(same));
-            if (in && bin != lead) atomicAdd(&wh[bin], 1u);
+                for (int q = 0; q < 8; ++q) bb[q] = __ballot_sync(0xffffffffu, (d >> q) & 1u);
+                uint32_t hi = inb;
+#pragma unroll
+                for (int q = 3; q < 8; ++q) hi &= ((lane >> (q - 3)) & 1) ? bb[q] : ~bb[q];
+#pragma unroll
+                for (int q = 0; q < 8; ++q)
+                    cnt[q] += __popc(hi & ((q & 1) ? bb[0] : ~bb[0]) & ((q & 2) ? bb[1] : ~bb[1]) &
+                                     ((q & 4) ? bb[2] : ~bb[2]));
+            }
+#pragma unroll
+            for (int q = 0; q < 8; ++q) wh[lane * 8 + q] = cnt[q];
+        } else {
+#pragma unroll
+            for (int w = 0; w < NW; ++w) whist[w * 256 + tid] = 0;
+            __syncthreads();
+            // four keys per step: independent ballot/shuffle chains overlap
+#pragma unroll(kReg ? kKPT / 4 : 1)
+            for (int k0 = 0; k0 < nk; k0 += 4) {
+                uint32_t bin[4], lead[4], same[4];
+                bool in[4];
+                int first[4];
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const uint32_t key = KEY(k0 + g);
+                    in[g] = key != 0xFFFFFFFFu && (key & mask) == prefix;
+                    bin[g] = (key >> shift) & dmask;
+                }
+#pragma unroll
+                for (int g = 0; g < 4; ++g) first[g] = __ffs(__ballot_sync(0xffffffffu, in[g])) - 1;
+#pragma unroll
+                for (int g = 0; g < 4; ++g) lead[g] = __shfl_sync(0xffffffffu, bin[g], first[g] & 31);
+#pragma unroll
+                for (int g = 0; g < 4; ++g)
+                    same[g] = __ballot_sync(0xffffffffu, in[g] && bin[g] == lead[g]);
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    if (lane == first[g]) atomicAdd(&wh[lead[g]], (uint32_t)__popc(same[g]));
+                    if (in[g] && bin[g] != lead[g]) atomicAdd(&wh[bin[g]], 1u);
+                }
+            }
         }
         __syncthreads();
+        // prefix sum over the warp histograms: the digit holding the need-th
+        // best key extends the prefix
         uint32_t c = 0;
 #pragma unroll
         for (int w = 0; w < NW; ++w) c += whist[w * 256 + tid];
@@ -363,6 +431,7 @@ __device__ __noinline__ void select_fast(const float *__restrict__ score,
             if (lane >= o) incl += y;
         }
         if (lane == 31) wsum[wid] = incl;
+        if (tid == 0) s_nc = 0;
         __syncthreads();
         uint32_t base = 0;
 #pragma unroll
@@ -371,13 +440,78 @@ __device__ __noinline__ void select_fast(const float *__restrict__ score,
         if (c > 0 && excl < need && excl + c >= need) {
             sh[0] = prefix | ((uint32_t)tid << shift);
             sh[1] = need - excl;
+            sh[2] = c;
         }
         __syncthreads();
         prefix = sh[0];
         need = sh[1];
-        mask |= 0xffu << shift;
+        mask |= dmask << shift;
+        const uint32_t cnt_t = sh[2];
+        if (pass == 0) SEL_TRACE(7);
+        if (pass == 0 && cnt_t <= (uint32_t)l1_cap) {
+            // compact the threshold exponent's rows; decide all others now
+#pragma unroll(kReg ? kKPT / 4 : 1)
+            for (int k0 = 0; k0 < nk; k0 += 4) {
+                uint32_t key[4], bal[4];
+                bool in[4];
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    key[g] = KEY(k0 + g);
+                    in[g] = key[g] != 0xFFFFFFFFu && (key[g] & mask) == prefix;
+                    bal[g] = __ballot_sync(0xffffffffu, in[g]);
+                }
+                const uint32_t tot =
+                    __popc(bal[0]) + __popc(bal[1]) + __popc(bal[2]) + __popc(bal[3]);
+                uint32_t at = 0;
+                if (lane == 0 && tot) at = atomicAdd(&s_nc, tot);
+                at = __shfl_sync(0xffffffffu, at, 0);
+                const uint32_t lt = (1u << lane) - 1u;
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    const int64_t i = tid + (int64_t)(k0 + g) * kSelThreads;
+                    if (in[g]) l1[at + __popc(bal[g] & lt)] = make_uint2(key[g], (uint32_t)i);
+                    at += __popc(bal[g]);
+                    if (!in[g] && i < n)
+                        selected[s + i] = (key[g] != 0xFFFFFFFFu && key[g] < prefix) ? 1 : 0;
+                }
+            }
+            __syncthreads();
+            compact = true;
+            n1 = (int)cnt_t;
+        } else if (compact && cnt_t <= (uint32_t)kPairCap) {
+            // rank the rows sharing the prefix pairwise; decide the rest of l1
+#pragma unroll 1
+            for (int a0 = wid * 32; a0 < n1; a0 += kSelThreads) {
+                const int a = a0 + lane;
+                const uint2 e = a < n1 ? l1[a] : make_uint2(0xFFFFFFFFu, 0u);
+                const bool is_c = a < n1 && (e.x & mask) == prefix;
+                const uint32_t bal = __ballot_sync(0xffffffffu, is_c);
+                uint32_t at = 0;
+                if (lane == 0 && bal) at = atomicAdd(&s_nc, (uint32_t)__popc(bal));
+                at = __shfl_sync(0xffffffffu, at, 0) + __popc(bal & ((1u << lane) - 1u));
+                if (is_c) cand[at] = e;
+                else if (a < n1) selected[s + e.y] = (e.x & mask) < prefix ? 1 : 0;
+            }
+            __syncthreads();
+            const int nc = (int)s_nc;
+            for (int a = tid; a < nc; a += kSelThreads) {
+                const uint2 me = cand[a];
+                uint32_t rank = 0;
+#pragma unroll 4
+                for (int b = 0; b < nc; ++b) {
+                    const uint2 o = cand[b];
+                    rank += (o.x < me.x || (o.x == me.x && o.y < me.y)) ? 1u : 0u;
+                }
+                selected[s + me.y] = rank < need ? 1 : 0;
+            }
+            SEL_TRACE(6);
+            return;
+        } else {
+            compact = false;       // many near-ties: finish over all keys
+        }
     }
     const uint32_t thr = prefix;
+    SEL_TRACE(6);
     // ties at the threshold: if every tie fits, no ordering is needed
     uint32_t mine = 0;
 #pragma unroll(kReg ? kKPT : 1)
@@ -433,7 +567,7 @@ constexpr int kStageRows = 16;
 constexpr int kVecPerThread = 8;          // 16 threads x 8 x 16 B = one 2 KB V row
 constexpr int kDepth = 3;
 constexpr size_t kStageBytes = (size_t)kSelThreads * kVecPerThread * 2 * 16;   // 64 KB
-constexpr int kMetaStages = 64;           // metadata chunk: 1024 rows x 24 B
+constexpr int kMetaRows = 1024;           // metadata chunk: 1024 rows x 24 B
 // requests up to kSmemKeys positions select with their keys in the (then idle) ring
 constexpr int kSmemKeys = (int)((kDepth * kStageBytes - 8 * 1024) / 4) / kSelThreads * kSelThreads;
 
@@ -444,71 +578,59 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+
 __global__ void __launch_bounds__(kSelThreads, 1) dhd_select_fused_kernel(
     const __nv_bfloat16 *__restrict__ v_true, const float *__restrict__ alpha,
     const int32_t *__restrict__ src_slot, int32_t layer, ArenaC A,
     const int64_t *__restrict__ req_off, int32_t n_req,
     const int32_t *__restrict__ budget, const int32_t *__restrict__ block_table,
     int32_t max_pages, float *__restrict__ dv_l1, float *__restrict__ score,
-    uint8_t *__restrict__ selected, uint32_t *__restrict__ counters) {
+    uint8_t *__restrict__ selected, uint32_t *__restrict__ counters,
+    uint32_t *__restrict__ keyws) {
     // counters[0] = CTAs that published their rows, counters[1] = selectors
-    // done (the last one re-zeroes both)
+    // done (the last one re-zeroes both); keyws[t] = the selection key of
+    // row t (descending score, 0xFFFFFFFF for non-reused rows)
     extern __shared__ __align__(16) uint8_t s_ring[];            // kDepth x kStageBytes
-    int32_t *co = reinterpret_cast<int32_t *>(s_ring + kDepth * kStageBytes);   // n_req + 1
+    int64_t *ro = reinterpret_cast<int64_t *>(s_ring + kDepth * kStageBytes);   // n_req + 1
     __shared__ uint32_t sh[4];
     __shared__ int s_ticket;
     const int tid = threadIdx.x;
-    if (tid < 32) {                           // stage prefix over requests
-        int32_t carry = 0;
-        for (int r0 = 0; r0 < n_req; r0 += 32) {
-            const int r = r0 + tid;
-            const int32_t c = r < n_req ? (int32_t)((req_off[r + 1] - req_off[r] + kStageRows - 1) /
-                                                    kStageRows) : 0;
-            int32_t incl = c;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (tid >= o) incl += y;
-            }
-            if (r < n_req) co[r] = carry + incl - c;
-            carry += __shfl_sync(0xffffffffu, incl, 31);
-        }
-        if (tid == 0) co[n_req] = carry;
-    }
+    SEL_TRACE(0);
+    for (int r = tid; r <= n_req; r += kSelThreads) ro[r] = req_off[r];
     __syncthreads();
-    const int total = co[n_req];
+    const int64_t row_lo = ro[0], row_hi = ro[n_req];
     const int nvec = A.G * A.D / 8;           // 16-byte vectors per V row (<= 128)
     const int row = tid / 16, sub = tid % 16;
-    const int my_stages = total > (int)blockIdx.x ? (total - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    // rows are dealt to CTAs one at a time (row t to CTA (t - row_lo) % grid):
+    // reused spans are long, so dealing whole stages left some CTAs with
+    // several times the mean number of live rows
+    const int64_t first = row_lo + (int64_t)blockIdx.x;
+    const int my_rows = first < row_hi ? (int)((row_hi - 1 - first) / gridDim.x) + 1 : 0;
 
-    // Metadata (row index, liveness, page row, alpha) of up to kMetaStages of
-    // this CTA's stages is loaded cooperatively in one round of independent
+    // Metadata (row index, liveness, page row, alpha) of up to kMetaRows of
+    // this CTA's rows is loaded cooperatively in one round of independent
     // loads into shared memory, so the copy pipeline never waits on it.
     struct RowMeta {
         int64_t t;        // flat row (-1: none)
         int64_t prow;     // page * P + row in page; -1 when not reused
         float alpha;
     };
-    RowMeta *meta = reinterpret_cast<RowMeta *>(co + n_req + 1 + ((n_req + 1) & 1));
+    RowMeta *meta = reinterpret_cast<RowMeta *>(ro + n_req + 1);
     __shared__ int s_live;
-    // returns the number of live (reused) rows of stages [k_first, k_first +
-    // k_count) of this CTA, compacted into meta[]; non-reused rows get their
-    // zero dv-L1 / score right here and never enter the copy pipeline
+    // returns the number of live (reused) rows among this CTA's rows
+    // [k_first, k_first + k_count), compacted into meta[]; non-reused rows get
+    // their zero dv-L1 / score right here and never enter the copy pipeline
     auto load_meta = [&](int k_first, int k_count) -> int {
         if (tid == 0) s_live = 0;
         __syncthreads();
-        for (int j = tid; j < k_count * kStageRows; j += kSelThreads) {
-            const int k = k_first + j / kStageRows, rr = j % kStageRows;
-            const int item = (int)blockIdx.x + k * (int)gridDim.x;
+        for (int j = tid; j < k_count; j += kSelThreads) {
+            const int64_t t = first + (int64_t)(k_first + j) * gridDim.x;
             int r = 0, hi = n_req;
             while (hi - r > 1) {
                 const int mid = (r + hi) >> 1;
-                if (co[mid] <= item) r = mid; else hi = mid;
+                if (ro[mid] <= t) r = mid; else hi = mid;
             }
-            const int64_t s0 = req_off[r], n = req_off[r + 1] - s0;
-            const int64_t i = (int64_t)(item - co[r]) * kStageRows + rr;
-            if (i >= n) continue;
-            const int64_t t = s0 + i;
+            const int64_t i = t - ro[r];
             const bool live = __ldg(src_slot + t) >= 0;
             const int64_t page = __ldg(block_table + (int64_t)r * max_pages + i / A.P);
             const float al = __ldg(alpha + t);
@@ -518,6 +640,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) dhd_select_fused_kernel(
             } else {
                 dv_l1[t] = 0.f;
                 score[t] = 0.f;
+                keyws[t] = 0xFFFFFFFFu;
             }
         }
         __syncthreads();
@@ -546,8 +669,9 @@ __global__ void __launch_bounds__(kSelThreads, 1) dhd_select_fused_kernel(
         cp_async_commit();
     };
 
-    for (int c0 = 0; c0 < my_stages; c0 += kMetaStages) {
-        const int n_live = load_meta(c0, min(kMetaStages, my_stages - c0));
+    for (int c0 = 0; c0 < my_rows; c0 += kMetaRows) {
+        const int n_live = load_meta(c0, min(kMetaRows, my_rows - c0));
+        SEL_TRACE(1);
         const int cn = (n_live + kStageRows - 1) / kStageRows;   // stages of live rows
 #pragma unroll
         for (int j = 0; j < kDepth - 1; ++j) issue(j, j, n_live);
@@ -577,8 +701,11 @@ __global__ void __launch_bounds__(kSelThreads, 1) dhd_select_fused_kernel(
                 for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
                 if (e < n_live && sub == 0) {
                     const RowMeta m = meta[e];
+                    const float sc = m.alpha * acc;
                     dv_l1[m.t] = acc;
-                    score[m.t] = m.alpha * acc;
+                    score[m.t] = sc;
+                    const uint32_t x = ~__float_as_uint(fmaxf(sc, 0.f));
+                    keyws[m.t] = x < 0xFFFFFFFEu ? x : 0xFFFFFFFEu;
                 }
             }
         }
@@ -588,6 +715,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) dhd_select_fused_kernel(
     // every CTA publishes its rows once; the last min(n_req, grid) CTAs to get
     // here become selectors, wait until all CTAs have published, and run one
     // request's top-B each (in parallel), so only one selection is exposed
+    SEL_TRACE(2);
     __threadfence();
     __syncthreads();
     if (tid == 0) s_ticket = (int)atomicAdd(&counters[0], 1u);
@@ -601,19 +729,26 @@ __global__ void __launch_bounds__(kSelThreads, 1) dhd_select_fused_kernel(
         __threadfence();
     }
     __syncthreads();
+    SEL_TRACE(3);
     uint32_t *whist = reinterpret_cast<uint32_t *>(s_ring);           // the ring is free now
     uint32_t *keys = whist + kSelThreads / 32 * 256;
     for (int r = sel; r < n_req; r += n_sel) {
         const int64_t s0 = req_off[r], n = req_off[r + 1] - s0;
-        if (n <= kRegKeys)
-            select_fast<true>(score, src_slot, s0, n, budget[r], selected, whist, keys, sh);
-        else if (n <= kSmemKeys)
-            select_fast<false>(score, src_slot, s0, n, budget[r], selected, whist, keys, sh);
+        constexpr int kFree = (int)(kDepth * kStageBytes / 4) - 8 * 256;   // words after whist
+        if (n <= kRegKeys) {
+            select_fast<true>(score, src_slot, s0, n, budget[r], selected, whist, keys, sh,
+                              reinterpret_cast<uint2 *>(keys), kFree / 2, keyws);
+        } else if (n <= kSmemKeys) {
+            const int nk2 = (int)((n + kSelThreads - 1) / kSelThreads * kSelThreads);   // keys[]
+            select_fast<false>(score, src_slot, s0, n, budget[r], selected, whist, keys, sh,
+                               reinterpret_cast<uint2 *>(keys + nk2), (kFree - nk2) / 2, keyws);
+        }
         else
             select_request<false>(score, src_slot, s0, n, budget[r], selected, keys,
                                   keys + kSelSmemKeys, sh);
         __syncthreads();
     }
+    SEL_TRACE(4);
     // the last selector out leaves the counters zeroed for the next launch
     if (tid == 0 && atomicAdd(&counters[1], 1u) + 1 == (uint32_t)n_sel) {
         counters[0] = 0;
@@ -629,16 +764,20 @@ __global__ void __launch_bounds__(kSelThreads) topk_kernel(const float *__restri
                                                            const int32_t *__restrict__ cand,
                                                            const int64_t *__restrict__ req_off,
                                                            const int32_t *__restrict__ budget,
-                                                           uint8_t *__restrict__ selected) {
+                                                           uint8_t *__restrict__ selected,
+                                                           int key_words, int l1_cap) {
     extern __shared__ uint32_t s_topk[];
     __shared__ uint32_t sh[4];
     const int r = blockIdx.x;
     const int64_t s = req_off[r], n = req_off[r + 1] - s;
     uint32_t *whist = s_topk, *keys = s_topk + 8 * 256;
+    uint2 *l1 = reinterpret_cast<uint2 *>(keys + key_words);
     if (n <= kRegKeys)
-        select_fast<true>(score, cand, s, n, budget[r], selected, whist, keys, sh);
+        select_fast<true>(score, cand, s, n, budget[r], selected, whist, keys, sh, l1, l1_cap,
+                          nullptr);
     else
-        select_fast<false>(score, cand, s, n, budget[r], selected, whist, keys, sh);
+        select_fast<false>(score, cand, s, n, budget[r], selected, whist, keys, sh, l1, l1_cap,
+                           nullptr);
 }
 
 // ---------------------------------------------------------------- D3
@@ -987,15 +1126,29 @@ static int decode_splits(int64_t n_rows, int G, int max_kv) {
 
 using namespace kvs;
 
+extern "C" int32_t kvs_sel_trace_dump(uint64_t *host, int32_t n) {
+#ifdef KVS_SEL_TRACE
+    const int m = n < 1024 * 8 ? n : 1024 * 8;
+    cudaMemcpyFromSymbol(host, kvs::g_sel_trace, sizeof(uint64_t) * m);
+    static unsigned long long zero[1024 * 8];
+    cudaMemcpyToSymbol(kvs::g_sel_trace, zero, sizeof(zero));
+    return m;
+#else
+    (void)host;
+    (void)n;
+    return -1;
+#endif
+}
+
 extern "C" {
 
 size_t kvs_dhd_select_workspace(int64_t n_total, int32_t n_req) {
-    (void)n_total;
     (void)n_req;
-    return 256;            // three self-resetting counters
+    // self-resetting counters, then one selection key per row
+    return 256 + align256(sizeof(uint32_t) * (size_t)(n_total > 0 ? n_total : 0));
 }
 
-/* Workspace contract: the first kvs_dhd_select_workspace() bytes must be zero
+/* Workspace contract: the first 256 bytes of the workspace must be zero
  * before the first call on a buffer; the kernel leaves them zero again. */
 kvs_status kvs_dhd_select(const void *v_true, const float *alpha, const int32_t *src_slot,
                           int32_t layer, const kvs_kv_arena *arena, const kvs_batch *batch,
@@ -1011,15 +1164,15 @@ kvs_status kvs_dhd_select(const void *v_true, const float *alpha, const int32_t 
     // counters start zeroed (Workspace.get(zero=True)) and are re-zeroed by the kernel
     KVS_REQUIRE(arena->kv_heads * arena->head_dim <= 16 * kVecPerThread * 8, KVS_ESHAPE,
                 "select: kv_heads * head_dim must be <= 1024");
-    const size_t smem = kDepth * kStageBytes + sizeof(int32_t) * (batch->n_req + 2) +
-                        24 * kMetaStages * kStageRows;
+    const size_t smem = kDepth * kStageBytes + sizeof(int64_t) * (batch->n_req + 1) +
+                        24 * kMetaRows;
     KVS_REQUIRE(smem <= 227 * 1024, KVS_EPARAM, "select: too many requests in one batch");
     cudaFuncSetAttribute(dhd_select_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     dhd_select_fused_kernel<<<kNumSMs, kSelThreads, smem, s>>>(
         (const __nv_bfloat16 *)v_true, alpha, src_slot, layer, arena_c(arena), batch->req_off,
         batch->n_req, budget, batch->block_table, batch->max_pages, dv_l1, score, selected,
-        counters);
+        counters, reinterpret_cast<uint32_t *>((uint8_t *)ws + 256));
     KVS_CHECK_LAUNCH("kvs_dhd_select");
     return KVS_OK;
 }
@@ -1136,10 +1289,17 @@ kvs_status kvs_topk_select(const float *scores, const int32_t *cand, const int64
                            uint8_t *selected, kvs_stream_t stream) {
     KVS_REQUIRE(n_req >= 1 && n_req <= 65535, KVS_EPARAM, "n_req must be in [1, 65535]");
     KVS_REQUIRE(max_len <= kSmemKeys, KVS_ESHAPE, "requests longer than %d positions", kSmemKeys);
-    const int smem = (int)(sizeof(uint32_t) * (8 * 256 + (max_len > kRegKeys ? max_len : 0)));
+    // keys[] holds whole rows of 256 (position tid + 256k)
+    const int key_words = (int)((std::max<int64_t>(max_len, 1) + kSelThreads - 1) / kSelThreads *
+                                kSelThreads);
+    // compacted threshold-exponent rows: up to max_len entries while the
+    // total stays within 200 KB (larger requests fall back to more passes)
+    const int l1_cap = (int)std::min<int64_t>(
+        std::max<int64_t>(max_len, 1), (200 * 1024 / 4 - 8 * 256 - key_words) / 2);
+    const int smem = (int)(sizeof(uint32_t) * (8 * 256 + key_words + 2 * l1_cap));
     cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     topk_kernel<<<n_req, kSelThreads, smem, (cudaStream_t)stream>>>(scores, cand, req_off, budget,
-                                                                    selected);
+                                                                    selected, key_words, l1_cap);
     KVS_CHECK_LAUNCH("kvs_topk_select");
     return KVS_OK;
 }

@@ -25,8 +25,8 @@ _ws = N.Workspace()
 _sws = N.Workspace()
 
 
-def _sel_ws(dev):
-    return _sws.get(N.ws_bytes("kvs_dhd_select_workspace", 1, 1), dev, zero=True)
+def _sel_ws(dev, n: int = 1):
+    return _sws.get(N.ws_bytes("kvs_dhd_select_workspace", n, 1), dev, zero=True)
 
 
 def _dev():

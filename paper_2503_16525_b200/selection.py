@@ -81,8 +81,8 @@ _dws = N.Workspace()
 _sws = N.Workspace()
 
 
-def _sel_ws(dev):
-    return _sws.get(N.ws_bytes("kvs_dhd_select_workspace", 1, 1), dev, zero=True)
+def _sel_ws(dev, n: int = 1):
+    return _sws.get(N.ws_bytes("kvs_dhd_select_workspace", n, 1), dev, zero=True)
 
 
 def select_decode_step(q_t, k, delta_v, eligible, n_extra: int) -> SelectionResult:
@@ -114,8 +114,8 @@ def select_decode_step(q_t, k, delta_v, eligible, n_extra: int) -> SelectionResu
     tmp = torch.empty(n, dtype=torch.float32, device=dev)
     tsel = torch.empty(n, dtype=torch.uint8, device=dev)
     N.call("kvs_dhd_select", zeros_v.data_ptr(), alpha0.data_ptr(), slot.data_ptr(), 0, sc.arena,
-           sc.batch, bud.data_ptr(), dv.data_ptr(), tmp.data_ptr(), tsel.data_ptr(), _sel_ws(dev).data_ptr(),
-           _sel_ws(dev).numel(), N.stream_ptr())
+           sc.batch, bud.data_ptr(), dv.data_ptr(), tmp.data_ptr(), tsel.data_ptr(), _sel_ws(dev, n).data_ptr(),
+           _sel_ws(dev, n).numel(), N.stream_ptr())
     qd = dense_rows(q_t[:, None, :], dev)                 # [1, H, 128]
     elig = np.zeros(n, dtype=np.uint8)
     elig[[e for e in eligible if 0 <= e < n]] = 1

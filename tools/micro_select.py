@@ -37,6 +37,9 @@ def main():
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--profile", action="store_true")
     ap.add_argument("--nosel", action="store_true", help="budget 0: streaming phase only")
+    ap.add_argument("--trace-csv", default=None)
+    ap.add_argument("--trace", action="store_true",
+                    help="library built with -DKVS_SEL_TRACE (KVS_LIB): per-CTA phase timeline")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     shape = dict(K.LLAMA31_8B)
@@ -114,6 +117,30 @@ def main():
         if it >= 3:
             ts.append(e0.elapsed_time(e1))
     t = float(np.median(ts))
+    if a.trace:
+        import ctypes
+        lib = N.load()
+        lib.kvs_sel_trace_dump.restype = ctypes.c_int32
+        buf = np.zeros(1024 * 8, dtype=np.uint64)
+        lib.kvs_sel_trace_dump(buf.ctypes.data, buf.size)        # clear
+        flush.zero_()
+        torch.cuda.synchronize()
+        N.call("kvs_dhd_select", *args)
+        torch.cuda.synchronize()
+        lib.kvs_sel_trace_dump(buf.ctypes.data, buf.size)
+        tr = buf.reshape(1024, 8)[:148].astype(np.int64)
+        t0 = tr[:, 0].min()
+        names = ["start", "meta", "streamed", "sel_start", "sel_end", "keys", "radix", "pass0"]
+        for ph in (1, 2, 3, 5, 7, 6, 4):
+            v = tr[:, ph]
+            v = v[v > 0] - t0
+            if len(v):
+                print(f"  {names[ph]:>9}: min {v.min() / 1e3:6.2f} med {np.median(v) / 1e3:6.2f} "
+                      f"max {v.max() / 1e3:6.2f} us (n={len(v)})")
+        st0 = tr[:, 0] - t0
+        if a.trace_csv:
+            np.savetxt(a.trace_csv, tr - t0, fmt="%d", delimiter=",")
+        print(f"  start spread: max {st0.max() / 1e3:.2f} us")
     print(f"reqs={a.reqs} seq={a.seq} reused={n_hit.sum()} bytes={nbytes / 1e6:.1f} MB  "
           f"median {t * 1e3:.1f} us  min {min(ts) * 1e3:.1f} us  -> {nbytes / t / 1e6:.0f} GB/s")
 
