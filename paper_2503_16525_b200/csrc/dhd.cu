@@ -567,7 +567,11 @@ constexpr int kStageRows = 16;
 constexpr int kVecPerThread = 8;          // 16 threads x 8 x 16 B = one 2 KB V row
 constexpr int kDepth = 3;
 constexpr size_t kStageBytes = (size_t)kSelThreads * kVecPerThread * 2 * 16;   // 64 KB
-constexpr int kMetaRows = 1024;           // metadata chunk: 1024 rows x 24 B
+constexpr int kMetaQ = 1024;              // live-row queue entries (16 B each), power of 2
+#ifndef KVS_CHUNK
+#define KVS_CHUNK 128
+#endif
+constexpr int kChunkRows = KVS_CHUNK;     // rows per grabbed chunk (<= kSelThreads)
 // requests up to kSmemKeys positions select with their keys in the (then idle) ring
 constexpr int kSmemKeys = (int)((kDepth * kStageBytes - 8 * 1024) / 4) / kSelThreads * kSelThreads;
 
@@ -588,7 +592,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) dhd_select_fused_kernel(
     uint8_t *__restrict__ selected, uint32_t *__restrict__ counters,
     uint32_t *__restrict__ keyws) {
     // counters[0] = CTAs that published their rows, counters[1] = selectors
-    // done (the last one re-zeroes both); keyws[t] = the selection key of
+    // done, counters[2] = chunks handed out (the last selector re-zeroes all); keyws[t] = the selection key of
     // row t (descending score, 0xFFFFFFFF for non-reused rows)
     extern __shared__ __align__(16) uint8_t s_ring[];            // kDepth x kStageBytes
     int64_t *ro = reinterpret_cast<int64_t *>(s_ring + kDepth * kStageBytes);   // n_req + 1
@@ -601,61 +605,90 @@ __global__ void __launch_bounds__(kSelThreads, 1) dhd_select_fused_kernel(
     const int64_t row_lo = ro[0], row_hi = ro[n_req];
     const int nvec = A.G * A.D / 8;           // 16-byte vectors per V row (<= 128)
     const int row = tid / 16, sub = tid % 16;
-    // rows are dealt to CTAs one at a time (row t to CTA (t - row_lo) % grid):
-    // reused spans are long, so dealing whole stages left some CTAs with
-    // several times the mean number of live rows
-    const int64_t first = row_lo + (int64_t)blockIdx.x;
-    const int my_rows = first < row_hi ? (int)((row_hi - 1 - first) / gridDim.x) + 1 : 0;
-
-    // Metadata (row index, liveness, page row, alpha) of up to kMetaRows of
-    // this CTA's rows is loaded cooperatively in one round of independent
-    // loads into shared memory, so the copy pipeline never waits on it.
+    // Work is handed out in chunks grabbed from a global counter, so CTAs
+    // on SMs that see less bandwidth simply take fewer chunks.  Chunk c is
+    // rows row_lo + c + NC*j (strided: reused spans are long, so contiguous
+    // chunks would differ wildly in live rows); at most kSelThreads rows,
+    // i.e. one row per thread.
+    const int64_t n_rows = row_hi - row_lo;
+    const int64_t NC = std::max<int64_t>(2 * gridDim.x, (n_rows + kChunkRows - 1) / kChunkRows);
+    // Live rows of the grabbed chunks form one queue (mq, kMetaQ entries,
+    // circular) that the copy ring streams through without draining between
+    // chunks.  Chunk ids: blockIdx.x, then grid + blockIdx.x, then tickets
+    // 2*grid + atomicAdd(counters[2]) fetched one chunk ahead, so neither
+    // the ticket nor the next chunk's metadata loads stall the ring.
     struct RowMeta {
-        int64_t t;        // flat row (-1: none)
-        int64_t prow;     // page * P + row in page; -1 when not reused
+        int32_t t;        // flat row
+        int32_t page;     // arena page of the cached row
+        int32_t r;        // row in page
         float alpha;
     };
-    RowMeta *meta = reinterpret_cast<RowMeta *>(ro + n_req + 1);
-    __shared__ int s_live;
-    // returns the number of live (reused) rows among this CTA's rows
-    // [k_first, k_first + k_count), compacted into meta[]; non-reused rows get
-    // their zero dv-L1 / score right here and never enter the copy pipeline
-    auto load_meta = [&](int k_first, int k_count) -> int {
-        if (tid == 0) s_live = 0;
+    RowMeta *mq = reinterpret_cast<RowMeta *>(ro + n_req + 1);
+    // double-buffered by call parity: back-to-back calls must not reset the
+    // values a slow thread of the previous call has yet to read
+    __shared__ int s_live[2];
+    __shared__ long long s_chunk[2];
+    int par = 0;
+    int64_t cur = blockIdx.x, nxt = (int64_t)gridDim.x + blockIdx.x;   // cur: loads in flight
+    uint32_t ticket = 0;
+    if (tid == 0) ticket = atomicAdd(&counters[2], 1u);
+    bool p_live = false;
+    int32_t p_page = 0, p_r = 0;
+    float p_alpha = 0.f;
+    int64_t p_t = -1;
+    auto issue_meta = [&](int64_t c) {
+        p_t = -1;
+        if (c >= NC || tid >= kChunkRows) return;
+        const int64_t t = row_lo + c + NC * tid;
+        if (t >= row_hi) return;
+        int r = 0, hi = n_req;
+        while (hi - r > 1) {
+            const int mid = (r + hi) >> 1;
+            if (ro[mid] <= t) r = mid; else hi = mid;
+        }
+        const int64_t i = t - ro[r];
+        p_t = t;
+        p_live = __ldg(src_slot + t) >= 0;
+        p_page = __ldg(block_table + (int64_t)r * max_pages + i / A.P);
+        p_alpha = __ldg(alpha + t);
+        p_r = (int32_t)(i % A.P);
+    };
+    // append chunk `cur`'s live rows to the queue, move on to the next chunk
+    // (its loads go out now); returns the new tail
+    auto finish_meta = [&](int tail) -> int {
+        if (tid == 0) {
+            s_live[par] = 0;
+            s_chunk[par] = 2 * (long long)gridDim.x + ticket;
+            ticket = atomicAdd(&counters[2], 1u);
+        }
         __syncthreads();
-        for (int j = tid; j < k_count; j += kSelThreads) {
-            const int64_t t = first + (int64_t)(k_first + j) * gridDim.x;
-            int r = 0, hi = n_req;
-            while (hi - r > 1) {
-                const int mid = (r + hi) >> 1;
-                if (ro[mid] <= t) r = mid; else hi = mid;
-            }
-            const int64_t i = t - ro[r];
-            const bool live = __ldg(src_slot + t) >= 0;
-            const int64_t page = __ldg(block_table + (int64_t)r * max_pages + i / A.P);
-            const float al = __ldg(alpha + t);
-            if (live) {
-                const int at = atomicAdd(&s_live, 1);
-                meta[at] = RowMeta{t, page * A.P + i % A.P, al};
+        if (p_t >= 0) {
+            if (p_live) {
+                const int at = atomicAdd(&s_live[par], 1);
+                mq[(tail + at) & (kMetaQ - 1)] = RowMeta{(int32_t)p_t, p_page, p_r, p_alpha};
             } else {
-                dv_l1[t] = 0.f;
-                score[t] = 0.f;
-                keyws[t] = 0xFFFFFFFFu;
+                dv_l1[p_t] = 0.f;
+                score[p_t] = 0.f;
+                keyws[p_t] = 0xFFFFFFFFu;
             }
         }
         __syncthreads();
-        return s_live;
+        cur = nxt;
+        nxt = s_chunk[par];
+        issue_meta(cur);
+        const int nt = tail + s_live[par];
+        par ^= 1;
+        return nt;
     };
     // ring layout [stage][j][array][thread][16 B]: a warp's accesses to one
     // (j, array) are 512 contiguous bytes (bank-conflict free)
     const uint32_t my_slice = smem_u32(s_ring) + tid * 16;
-    auto issue = [&](int k_local, int slot, int n_live) {
-        const int e = k_local * kStageRows + row;
-        if (e < n_live) {
-            const RowMeta m = meta[e];
-            const uint4 *vc = reinterpret_cast<const uint4 *>(
-                A.row(m.prow / A.P, layer, 1, (int)(m.prow % A.P)));
-            const uint4 *vt = reinterpret_cast<const uint4 *>(v_true + m.t * (int64_t)(A.G * A.D));
+    auto issue = [&](int k, int slot, int tail) {
+        const int e = k * kStageRows + row;
+        if (e < tail) {
+            const RowMeta m = mq[e & (kMetaQ - 1)];
+            const uint4 *vc = reinterpret_cast<const uint4 *>(A.row(m.page, layer, 1, m.r));
+            const uint4 *vt = reinterpret_cast<const uint4 *>(v_true + (int64_t)m.t * (A.G * A.D));
             const uint32_t dst = my_slice + (uint32_t)slot * (uint32_t)kStageBytes;
 #pragma unroll
             for (int j = 0; j < kVecPerThread; ++j) {
@@ -669,53 +702,59 @@ __global__ void __launch_bounds__(kSelThreads, 1) dhd_select_fused_kernel(
         cp_async_commit();
     };
 
-    for (int c0 = 0; c0 < my_rows; c0 += kMetaRows) {
-        const int n_live = load_meta(c0, min(kMetaRows, my_rows - c0));
-        SEL_TRACE(1);
-        const int cn = (n_live + kStageRows - 1) / kStageRows;   // stages of live rows
+    int tail = 0;
+    issue_meta(cur);
+    tail = finish_meta(tail);
+    SEL_TRACE(1);
+    // keep the queue kDepth stages ahead of the stage being reduced
+    auto refill = [&](int k_need) {
+        while (tail < k_need * kStageRows && cur < NC) tail = finish_meta(tail);
+    };
+    refill(kDepth);
 #pragma unroll
-        for (int j = 0; j < kDepth - 1; ++j) issue(j, j, n_live);
-        for (int k0 = 0; k0 < cn; k0 += kDepth) {
+    for (int j = 0; j < kDepth - 1; ++j) issue(j, j, tail);
+    for (int k0 = 0;; k0 += kDepth) {
+        bool done = false;
 #pragma unroll
-            for (int u = 0; u < kDepth; ++u) {      // unrolled: ring slots are static
-                const int k = k0 + u;
-                if (k >= cn) break;
-                // copies for stage k+depth-1 go out before stage k is reduced
-                issue(k + kDepth - 1, (u + kDepth - 1) % kDepth, n_live);
-                cp_async_wait<kDepth - 1>();
-                const int e = k * kStageRows + row;
-                float acc = 0.f;
-                if (e < n_live) {
-                    const uint8_t *src = s_ring + (size_t)u * kStageBytes + (size_t)tid * 16;
+        for (int u = 0; u < kDepth; ++u) {      // unrolled: ring slots are static
+            const int k = k0 + u;
+            if (k * kStageRows >= tail && cur >= NC) { done = true; break; }
+            refill(k + kDepth);
+            // copies for stage k+depth-1 go out before stage k is reduced
+            issue(k + kDepth - 1, (u + kDepth - 1) % kDepth, tail);
+            cp_async_wait<kDepth - 1>();
+            const int e = k * kStageRows + row;
+            float acc = 0.f;
+            if (e < tail) {
+                const uint8_t *src = s_ring + (size_t)u * kStageBytes + (size_t)tid * 16;
 #pragma unroll
-                    for (int j = 0; j < kVecPerThread; ++j)
-                        if (sub + 16 * j < nvec) {
-                            const uint4 a =
-                                *reinterpret_cast<const uint4 *>(src + (2 * j) * (kSelThreads * 16));
-                            const uint4 b = *reinterpret_cast<const uint4 *>(
-                                src + (2 * j + 1) * (kSelThreads * 16));
-                            acc += l1_diff8(a, b);
-                        }
-                }
+                for (int j = 0; j < kVecPerThread; ++j)
+                    if (sub + 16 * j < nvec) {
+                        const uint4 a =
+                            *reinterpret_cast<const uint4 *>(src + (2 * j) * (kSelThreads * 16));
+                        const uint4 b = *reinterpret_cast<const uint4 *>(
+                            src + (2 * j + 1) * (kSelThreads * 16));
+                        acc += l1_diff8(a, b);
+                    }
+            }
 #pragma unroll
-                for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-                if (e < n_live && sub == 0) {
-                    const RowMeta m = meta[e];
-                    const float sc = m.alpha * acc;
-                    dv_l1[m.t] = acc;
-                    score[m.t] = sc;
-                    const uint32_t x = ~__float_as_uint(fmaxf(sc, 0.f));
-                    keyws[m.t] = x < 0xFFFFFFFEu ? x : 0xFFFFFFFEu;
-                }
+            for (int o = 8; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            if (e < tail && sub == 0) {
+                const RowMeta m = mq[e & (kMetaQ - 1)];
+                const float sc = m.alpha * acc;
+                dv_l1[m.t] = acc;
+                score[m.t] = sc;
+                const uint32_t x = ~__float_as_uint(fmaxf(sc, 0.f));
+                keyws[m.t] = x < 0xFFFFFFFEu ? x : 0xFFFFFFFEu;
             }
         }
-        cp_async_wait<0>();
-        __syncthreads();                     // meta[] is rewritten by the next chunk
+        if (done) break;
     }
+    cp_async_wait<0>();
+    SEL_TRACE(2);
     // every CTA publishes its rows once; the last min(n_req, grid) CTAs to get
     // here become selectors, wait until all CTAs have published, and run one
     // request's top-B each (in parallel), so only one selection is exposed
-    SEL_TRACE(2);
     __threadfence();
     __syncthreads();
     if (tid == 0) s_ticket = (int)atomicAdd(&counters[0], 1u);
@@ -753,6 +792,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) dhd_select_fused_kernel(
     if (tid == 0 && atomicAdd(&counters[1], 1u) + 1 == (uint32_t)n_sel) {
         counters[0] = 0;
         counters[1] = 0;
+        counters[2] = 0;
         __threadfence();
     }
 }
@@ -1165,7 +1205,7 @@ kvs_status kvs_dhd_select(const void *v_true, const float *alpha, const int32_t 
     KVS_REQUIRE(arena->kv_heads * arena->head_dim <= 16 * kVecPerThread * 8, KVS_ESHAPE,
                 "select: kv_heads * head_dim must be <= 1024");
     const size_t smem = kDepth * kStageBytes + sizeof(int64_t) * (batch->n_req + 1) +
-                        24 * kMetaRows;
+                        16 * kMetaQ;
     KVS_REQUIRE(smem <= 227 * 1024, KVS_EPARAM, "select: too many requests in one batch");
     cudaFuncSetAttribute(dhd_select_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
