@@ -379,6 +379,70 @@ def decode_leg(args, eng, batch, cfg, n_tokens: int = 8):
                                   "achieved": d3_bytes / (d3_ms / 1000.0) / 1e9, "unit": "GB/s"}}
 
 
+def select_batch_leg(n_req: int, seq: int = 4096, hit: float = 0.5, ratio: float = 0.2,
+                     iters: int = 10):
+    """D2 (kvs_dhd_select) on a larger scheduled batch than the step's, as
+    SURVEY 8d asks ("measure batched over all requests of a scheduled batch"):
+    n_req Llama-shape requests (kv_heads 8, head dim 128) with reused spans of
+    64-1024 tokens covering ~hit of each, a 2-layer arena (D2 reads the probe
+    layer only), L2 flushed before every launch, CUDA events around each
+    launch.  Returns the achieved algorithmic GB/s."""
+    import torch
+    import paper_2503_16525_b200 as K
+    from paper_2503_16525_b200 import _native as N
+    from paper_2503_16525_b200.engine import Engine
+    from paper_2503_16525_b200.pool import CachePool, KVArena
+    dev = torch.device("cuda", torch.cuda.current_device())
+    shape = dict(K.LLAMA31_8B)
+    shape.update(num_layers=2, vocab_size=1000)
+    cfg = K.ModelConfig(**shape, max_positions=seq + 64)
+    arena = KVArena(cfg, n_req * ((seq + 63) // 64) + 4)
+    eng = Engine(K.ToyModel(cfg, init="device"), CachePool(cfg, arena=arena))
+    rng = np.random.default_rng(0)
+    st = eng.new_batch([rng.integers(0, 1000, seq) for _ in range(n_req)])
+    arena.data.normal_()
+    n = n_req * seq
+    src = np.full(n, -1, dtype=np.int32)
+    for r in range(n_req):
+        p = 0
+        while p < seq:
+            span = int(rng.integers(64, 1025))
+            if rng.random() < hit:
+                src[r * seq + p: r * seq + min(seq, p + span)] = 0
+            p += span
+    st.src_slot = torch.from_numpy(src).to(dev)
+    v_true = (torch.randn(n, cfg.kv_heads, 128, device=dev) * 0.5).to(torch.bfloat16)
+    alpha = torch.rand(n, device=dev)
+    n_hit = np.array([(src[r * seq:(r + 1) * seq] >= 0).sum() for r in range(n_req)])
+    bud = np.array([K.SelectionConfig(ratio=ratio).budget(int(h)) for h in n_hit], np.int32)
+    dv = torch.empty(n, device=dev)
+    score = torch.empty(n, device=dev)
+    sel = torch.empty(n, dtype=torch.uint8, device=dev)
+    bud_dev = torch.from_numpy(bud).to(dev)
+    ws = torch.zeros(N.ws_bytes("kvs_dhd_select_workspace", n, n_req), dtype=torch.uint8,
+                     device=dev)
+    args = (v_true.data_ptr(), alpha.data_ptr(), st.src_slot.data_ptr(), 1, eng.arena.c,
+            st.batch_c, bud_dev.data_ptr(), dv.data_ptr(), score.data_ptr(), sel.data_ptr(),
+            ws.data_ptr(), ws.numel(), N.stream_ptr())
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    nbytes = float(n_hit.sum() * (2 * cfg.kv_heads * 128 * 2 + 12) + 4 * bud.sum())
+    ts = []
+    for it in range(iters + 2):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        N.call("kvs_dhd_select", *args)
+        e1.record()
+        torch.cuda.synchronize()
+        if it >= 2:
+            ts.append(e0.elapsed_time(e1))
+    ms = float(np.median(ts))
+    del arena, eng, st, v_true, flush
+    torch.cuda.empty_cache()
+    return {"requests": n_req, "reused_rows": int(n_hit.sum()), "algorithmic_bytes": nbytes,
+            "ms": ms, "achieved": nbytes / (ms / 1000.0) / 1e9, "unit": "GB/s"}
+
+
 def ncu_traffic(kernel: str):
     """DRAM bytes per launch of `kernel` from the committed ncu capture
     (profiles/r1_ncu_traffic.json), or None."""
@@ -475,6 +539,15 @@ def main():
         extra["dhd_alpha"] = {"bound": "tensor", "achieved": tf, "peak": tflops_sus,
                               "unit": "TFLOP/s", "frac": tf / tflops_sus,
                               "ms_per_step": kern["dhd_alpha"]}
+    if "dhd_select" in kern and world == 1 and not args.profile:
+        # the step's batch (8 requests, ~67 MB) is latency-bound; larger
+        # scheduled batches show the streaming rate
+        extra["dhd_select_batched"] = []
+        for nr in (64, 128):
+            b = select_batch_leg(nr)
+            b["peak"] = hbm
+            b["frac"] = b["achieved"] / hbm
+            extra["dhd_select_batched"].append(b)
     if "gather" in kern:
         extra["gather_ms_per_step"] = kern["gather"]
     if "remote_fetch" in kern:
