@@ -611,7 +611,8 @@ __global__ void __launch_bounds__(kSelThreads, 1) dhd_select_fused_kernel(
     // chunks would differ wildly in live rows); at most kSelThreads rows,
     // i.e. one row per thread.
     const int64_t n_rows = row_hi - row_lo;
-    const int64_t NC = std::max<int64_t>(2 * gridDim.x, (n_rows + kChunkRows - 1) / kChunkRows);
+    const int64_t nc_rows = (n_rows + kChunkRows - 1) / kChunkRows;
+    const int64_t NC = nc_rows > 2 * (int64_t)gridDim.x ? nc_rows : 2 * (int64_t)gridDim.x;
     // Live rows of the grabbed chunks form one queue (mq, kMetaQ entries,
     // circular) that the copy ring streams through without draining between
     // chunks.  Chunk ids: blockIdx.x, then grid + blockIdx.x, then tickets
@@ -826,38 +827,62 @@ __global__ void __launch_bounds__(kSelThreads) topk_kernel(const float *__restri
 // partial max / sum-exp.
 constexpr int kDecChunk = 256;    // keys per CTA of the logits pass (8 warps x 32)
 
-// Pass 1: grid (key chunk, request), 8 warps, each a 32-key tile with one
-// key per lane (a tile lies in one page).  For every kv head the lane loads
-// its key's 256-byte slice and forms the HQ query heads' logits with q from
-// shared memory; logits [request][head][key] (log2 domain) are written
-// coalesced (consecutive keys per head).
+// Pass 1: grid (key chunk, request, kv head), 8 warps, each a 32-key tile
+// with one key per lane (a tile lies in one page).  The lane loads its key's
+// 256-byte slice of the CTA's kv head and forms the HQ query heads' logits
+// with q from shared memory; logits [request][head][key] (log2 domain) are
+// written coalesced (consecutive keys per head).
 template <int HQ>
-__global__ void __launch_bounds__(256) decode_logits_kernel(
+__global__ void __launch_bounds__(256, 2) decode_logits_kernel(
     const __nv_bfloat16 *__restrict__ q_t, int32_t H, const int32_t *__restrict__ ctx_len,
     int32_t max_ctx, int32_t layer, ArenaC A, const int32_t *__restrict__ block_table,
     int32_t max_pages, float scale_log2, float *__restrict__ logits,
     float2 *__restrict__ part /* [request][tile][H] (max, sum) */) {
     constexpr int D = 128;
-    extern __shared__ __align__(16) float sq[];  // [H][D] fp32
-    const int r = blockIdx.y;
+    __shared__ __align__(16) float sq[HQ * D];   // the group's query heads, fp32
+    extern __shared__ __align__(16) uint8_t skey[];   // [warp][32 keys][256 B], swizzled
+    // kv head fastest in the grid: the CTAs reading the 8 slices of the same
+    // 2 KB key rows run together (DRAM row locality)
+    const int g = blockIdx.x, r = blockIdx.z;
     const int n = ctx_len[r];
-    for (int i = threadIdx.x; i < H * D; i += blockDim.x)
-        sq[i] = bf2f(q_t[(int64_t)r * H * D + i]);
-    __syncthreads();
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int t0 = blockIdx.x * kDecChunk + wid * 32;
-    if (t0 >= n) return;
+    const int t0 = blockIdx.y * kDecChunk + wid * 32;
     const int k = t0 + lane;
     const bool live = k < n;
-    const int64_t page = block_table[(int64_t)r * max_pages + t0 / A.P];
-    const __nv_bfloat16 *krow = A.row(page, layer, 0, t0 % A.P) + (int64_t)lane * A.G * D;
-    for (int g = 0; g < A.G; ++g) {
-        uint4 kx[D / 8];
-        if (live) {
-            const uint4 *kr = reinterpret_cast<const uint4 *>(krow + g * D);
+    // The tile's 32 key slices (256 B each, 2 KB apart in the page) are
+    // staged with cp.async so that every warp instruction moves two whole
+    // slices (16 lanes x 16 B each) instead of 32 scattered 16-byte pieces;
+    // chunk c of key j lands at slot c ^ (j & 15) (conflict-free reads of a
+    // whole slice per lane below).  The K copies go out before q is staged.
+    const uint32_t sk = smem_u32(skey) + wid * 8192;
+    if (t0 < n) {
+        const int64_t page = block_table[(int64_t)r * max_pages + t0 / A.P];
+        const uint8_t *kbase =
+            reinterpret_cast<const uint8_t *>(A.row(page, layer, 0, t0 % A.P) + g * D);
+        const int c = lane & 15;
 #pragma unroll
-            for (int c = 0; c < D / 8; ++c) kx[c] = __ldg(kr + c);
+        for (int j = 0; j < 16; ++j) {
+            const int kk = 2 * j + (lane >> 4);
+            if (t0 + kk < n)
+                cp_async16(sk + kk * 256 + ((c ^ (kk & 15)) * 16),
+                           kbase + (int64_t)kk * A.G * D * 2 + c * 16);
         }
+        cp_async_commit();
+    }
+    for (int i = threadIdx.x; i < HQ * D; i += blockDim.x)
+        sq[i] = bf2f(q_t[((int64_t)r * H + g * HQ) * D + i]);
+    cp_async_wait<0>();
+    __syncthreads();
+    if (t0 >= n) return;
+    uint4 kx[D / 8];
+#pragma unroll
+    for (int c = 0; c < D / 8; ++c) {
+        const uint32_t addr = sk + lane * 256 + ((c ^ (lane & 15)) * 16);
+        asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                     : "=r"(kx[c].x), "=r"(kx[c].y), "=r"(kx[c].z), "=r"(kx[c].w)
+                     : "r"(addr));
+    }
+    {
         float p[HQ];
 #pragma unroll
         for (int hh = 0; hh < HQ; ++hh) p[hh] = 0.f;
@@ -873,7 +898,7 @@ __global__ void __launch_bounds__(256) decode_logits_kernel(
             }
 #pragma unroll
             for (int hh = 0; hh < HQ; ++hh) {
-                const float *qh = sq + (g * HQ + hh) * D + 8 * c;
+                const float *qh = sq + hh * D + 8 * c;
                 const float4 qa = *reinterpret_cast<const float4 *>(qh);
                 const float4 qb = *reinterpret_cast<const float4 *>(qh + 4);
                 p[hh] += kf[0] * qa.x + kf[1] * qa.y + kf[2] * qa.z + kf[3] * qa.w +
@@ -884,7 +909,7 @@ __global__ void __launch_bounds__(256) decode_logits_kernel(
 #pragma unroll
         for (int hh = 0; hh < HQ; ++hh) {
             const float x = live ? p[hh] * scale_log2 : -INFINITY;
-            if (live) logits[((int64_t)r * H + g * HQ + hh) * max_ctx + k] = x;
+            if (live) logits[((int64_t)r * H + g * HQ + hh) * ((max_ctx + 3) & ~3) + k] = x;
             const float mt = warp_max(x);
             const float z = warp_sum(live ? fast_exp2(x - mt) : 0.f);
             if (lane == 0) part[((int64_t)r * n_tiles + tile) * H + g * HQ + hh] = make_float2(mt, z);
@@ -942,14 +967,37 @@ __global__ void __launch_bounds__(1024) decode_select_kernel(
     __syncthreads();
     const float invH = 1.f / (float)H;
     float *scr = scores_out ? scores_out + (int64_t)r * max_ctx : nullptr;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-        float w = 0.f;
-        if (i < n_pre)
-            for (int h = 0; h < H; ++h)
-                w += fast_exp2(logits[((int64_t)r * H + h) * max_ctx + i] - sm[h]) * sz[h];
-        const float v = i < n_pre ? w * invH * dv_l1[s + i] : 0.f;
-        sc[i] = v;
-        if (scr) scr[i] = v;
+    // four consecutive rows per thread: 16-byte loads of each head's logits
+    // (L2-resident), eight heads in flight
+    const int64_t ld = (max_ctx + 3) & ~3;
+    for (int i0 = 4 * threadIdx.x; i0 < n; i0 += 4 * blockDim.x) {
+        float w[4] = {0.f, 0.f, 0.f, 0.f};
+        if (i0 < n_pre)
+            for (int h0 = 0; h0 < H; h0 += 8) {
+                float4 x[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    x[u] = h0 + u < H ? __ldcg(reinterpret_cast<const float4 *>(
+                                            logits + ((int64_t)r * H + h0 + u) * ld + i0))
+                                      : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (h0 + u < H) {
+                        const float mh = sm[h0 + u], zh = sz[h0 + u];
+                        w[0] += fast_exp2(x[u].x - mh) * zh;
+                        w[1] += fast_exp2(x[u].y - mh) * zh;
+                        w[2] += fast_exp2(x[u].z - mh) * zh;
+                        w[3] += fast_exp2(x[u].w - mh) * zh;
+                    }
+            }
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const int i = i0 + e;
+            if (i >= n) break;
+            const float v = i < n_pre ? w[e] * invH * dv_l1[s + i] : 0.f;
+            sc[i] = v;
+            if (scr) scr[i] = v;
+        }
     }
     __syncthreads();
     int picked = 0;
@@ -1219,7 +1267,7 @@ kvs_status kvs_dhd_select(const void *v_true, const float *alpha, const int32_t 
 
 size_t kvs_dhd_decode_select_workspace(int32_t n_req, int32_t num_heads, int32_t max_ctx) {
     const size_t tiles = ((size_t)max_ctx + 31) / 32;
-    return align256(sizeof(float) * (size_t)n_req * num_heads * max_ctx) +
+    return align256(sizeof(float) * (size_t)n_req * num_heads * (((size_t)max_ctx + 3) & ~(size_t)3)) +
            align256(sizeof(float2) * (size_t)n_req * tiles * num_heads);
 }
 
@@ -1245,13 +1293,14 @@ kvs_status kvs_dhd_decode_select(const void *q_t, int32_t num_heads, const int32
     const int chunks = (max_ctx + kDecChunk - 1) / kDecChunk;
     float *logits = (float *)ws;
     float2 *part = (float2 *)((char *)ws + align256(sizeof(float) * (size_t)batch->n_req *
-                                                     num_heads * max_ctx));
+                                                     num_heads * (((size_t)max_ctx + 3) & ~(size_t)3)));
     const float scale_log2 = softmax_scale * 1.4426950408889634f;
-    const size_t smem = sizeof(float) * num_heads * 128;
     const int hq = num_heads / arena->kv_heads;
-    const dim3 grid(chunks, batch->n_req);
+    const dim3 grid(arena->kv_heads, chunks, batch->n_req);     // one kv head per CTA
 #define KVS_DECODE_LOGITS(HQ)                                                                  \
-    decode_logits_kernel<HQ><<<grid, 256, smem, s>>>((const __nv_bfloat16 *)q_t, num_heads,    \
+    cudaFuncSetAttribute(decode_logits_kernel<HQ>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                         8 * 8192);                                                            \
+    decode_logits_kernel<HQ><<<grid, 256, 8 * 8192, s>>>((const __nv_bfloat16 *)q_t, num_heads,    \
                                                      ctx_len, max_ctx, layer, arena_c(arena),  \
                                                      batch->block_table, batch->max_pages,     \
                                                      scale_log2, logits, part)
