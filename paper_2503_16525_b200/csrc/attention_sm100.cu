@@ -1358,7 +1358,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     __shared__ float s_lse[2][BM];
     __shared__ int32_t s_qn[2];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tile = blockIdx.y, g = blockIdx.x;
+    // key tiles fastest: the CTAs of one kv group sweep a few requests at a
+    // time, so those requests' query tiles are re-read from L2, not DRAM
+    const int tile = blockIdx.x, g = blockIdx.y;
     const int hq = p.num_heads / p.kv_heads;
     const int req = p.tile_req[tile], k0 = p.row_pos[p.tile_row0[tile]];
     const int64_t s0 = p.req_off[req];
@@ -1685,7 +1687,7 @@ kvs_status kvs_dhd_alpha(const void *q, int32_t num_heads, int32_t causal, int32
     const size_t smem = 1024 + attn::TILE_BYTES * (1 + attn::NS);
     cudaFuncSetAttribute(attn::colsum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    attn::colsum_kernel<<<dim3(arena->kv_heads, n_tiles), attn::kThreads, smem, s>>>(mq, mkv, cp);
+    attn::colsum_kernel<<<dim3(n_tiles, arena->kv_heads), attn::kThreads, smem, s>>>(mq, mkv, cp);
     attn::alpha_reduce_kernel<<<kNumSMs * 4, 256, 0, s>>>(part, n_total, arena->kv_heads,
                                                          num_heads, alpha);
     KVS_CHECK_LAUNCH("kvs_dhd_alpha");
