@@ -38,7 +38,7 @@ WORKLOAD = "llama3.1-8b-shape DHD prefill, 4096-token requests, 50% chunk hit, r
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=8, help="requests per scheduled batch per GPU")
@@ -61,7 +61,10 @@ def parse():
 
 # ---------------------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    """nvidia-smi clocks / throttle reasons sampled every 100 ms.  start()
+    returns once the sampler has produced its first line; mark() brackets the
+    timed region, and only samples stamped inside it are reported."""
+    FIELDS = ("timestamp,index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -69,33 +72,55 @@ class ClockSampler:
         self.idx = gpu_index
         self.proc = None
         self.path = f"/tmp/kvs_clocks_{os.getpid()}.csv"
+        self.t0 = self.t1 = None
 
     def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
         except OSError:
             self.proc = None
+            return
+        deadline = time.time() + 10.0
+        while time.time() < deadline:
+            try:
+                if os.path.getsize(self.path) > 0:
+                    break
+            except OSError:
+                pass
+            time.sleep(0.02)
+
+    def mark(self, end: bool = False):
+        if end:
+            self.t1 = time.time()
+        else:
+            self.t0 = time.time()
 
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)                     # let a sample stamped after t1 land
         self.proc.terminate()
         self.proc.wait()
+        import datetime
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in open(self.path):
             f = [x.strip() for x in line.split(",")]
-            if len(f) < 9:
+            if len(f) < 10:
                 continue
             try:
-                sm.append(float(f[1]))
-                smax = float(f[2])
+                ts = datetime.datetime.strptime(f[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                clk, cmax = float(f[2]), float(f[3])
             except ValueError:
                 continue
-            for name, v in zip(names, f[5:9]):
+            if self.t0 is not None and not (self.t0 <= ts <= (self.t1 or ts)):
+                continue
+            sm.append(clk)
+            smax = cmax
+            for name, v in zip(names, f[6:10]):
                 if v.lower() == "active":
                     reasons.add(name)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
@@ -241,6 +266,7 @@ def run_gpu(args, rank, world, device):
     clocks.start()
     barrier()
     torch.cuda.synchronize()
+    clocks.mark()
     launches0 = N.launch_count["kernels"]
     mallocs0 = torch.cuda.memory_stats(device).get("num_device_alloc", 0)
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -258,6 +284,7 @@ def run_gpu(args, rank, world, device):
         eng.release(st)                     # pages are reused in stream order
     end.record()
     torch.cuda.synchronize()
+    clocks.mark(end=True)
     if args.profile:
         torch.cuda.cudart().cudaProfilerStop()
     barrier()
