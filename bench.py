@@ -186,7 +186,7 @@ def build_engine(args, device, rank=0, world=1):
     model = K.ToyModel(cfg, device=device, init="device")
     src_pages = args.sources * ((args.seq + 63) // 64)
     step_pages = 2 * args.batch * ((args.seq + 63) // 64)
-    arena = KVArena(cfg, src_pages + step_pages + 64, device)
+    arena = KVArena(cfg, src_pages + step_pages + 64 + getattr(args, "extra_pages", 0), device)
     pool = CachePool(cfg, K.HashParams(window_size=8), arena=arena, device=device)
     eng = Engine(model, pool)
     sources = source_requests(args.sources, args.seq, cfg.vocab_size, seed=0)
