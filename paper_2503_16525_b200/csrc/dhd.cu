@@ -309,6 +309,14 @@ __device__ __forceinline__ unsigned long long gtimer() {
 //           and an ordered tie pass.
 // The code is kept small on purpose: only the last CTAs of the fused launch
 // run it, cold, and instruction fetch dominated an unrolled version.
+// The fused launch's selectors run the shared-memory-key (rolled-loop) path
+// even for requests that fit the register path: only 1-8 CTAs run it, once per
+// step, with its code evicted by the step's other kernels, and inside a real
+// step the unrolled register variant's cold instruction fetch cost twice its
+// arithmetic (16 vs 8 us; tools/select_trace_step.py).
+#ifndef KVS_SEL_REG
+#define KVS_SEL_REG 0
+#endif
 constexpr int kPairCap = 256;     // threshold-digit rows ranked pairwise
 constexpr int kKPT = 16;          // register keys per thread
 constexpr int kRegKeys = kKPT * kSelThreads;
@@ -775,7 +783,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) dhd_select_fused_kernel(
     for (int r = sel; r < n_req; r += n_sel) {
         const int64_t s0 = req_off[r], n = req_off[r + 1] - s0;
         constexpr int kFree = (int)(kDepth * kStageBytes / 4) - 8 * 256;   // words after whist
-        if (n <= kRegKeys) {
+        if (KVS_SEL_REG && n <= kRegKeys) {
             select_fast<true>(score, src_slot, s0, n, budget[r], selected, whist, keys, sh,
                               reinterpret_cast<uint2 *>(keys), kFree / 2, keyws);
         } else if (n <= kSmemKeys) {
