@@ -200,10 +200,21 @@ __global__ void __launch_bounds__(256) qkv_rope_scatter_kernel(
 // Scatter v2 (the one launched): persistent CTAs, each walking rows
 // blockIdx.x + k * gridDim.x.  A row's whole [q | k | v] slice (12 KB at
 // Llama width) arrives with one TMA bulk copy into a kScatSlots-deep shared
-// ring; warp 1 fetches the row's metadata (position, K/V destination) and
+// ring (2 slots x 128 threads: many small CTAs per SM beat deeper rings,
+// 81 vs 104 us per session layer at 19.7k rows); warp 1 fetches the row's metadata (position, K/V destination) and
 // its cos/sin coefficients into the slot kScatSlots-1 rows ahead, so the
 // 256 consumer threads only read shared memory, rotate, and store.
-constexpr int kScatSlots = 4;
+#ifndef KVS_SCAT_SLOTS
+#define KVS_SCAT_SLOTS 2
+#endif
+constexpr int kScatSlots = KVS_SCAT_SLOTS;
+// a row's metadata is staged one iteration ahead and published by that
+// iteration's closing barrier, so the ring needs at least two slots
+static_assert(kScatSlots >= 2, "qkv_scatter2 needs at least two ring slots");
+#ifndef KVS_SCAT_THREADS
+#define KVS_SCAT_THREADS 128
+#endif
+constexpr int kScatThreads = KVS_SCAT_THREADS;
 
 struct ScatMeta {
     int64_t dst;      // element offset of the row's K in the arena, -1: no K/V write
@@ -219,7 +230,7 @@ __device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t
         : "memory");
 }
 
-__global__ void __launch_bounds__(256) qkv_scatter2_kernel(
+__global__ void __launch_bounds__(kScatThreads) qkv_scatter2_kernel(
     const __nv_bfloat16 *__restrict__ qkv, int64_t n_rows, int32_t H, Arena A,
     const int32_t *__restrict__ row_req, const int32_t *__restrict__ row_pos,
     const uint8_t *__restrict__ write_kv, int32_t layer, const int32_t *__restrict__ block_table,
@@ -524,9 +535,10 @@ kvs_status kvs_qkv_rope_scatter(const void *qkv, int64_t n_rows, int32_t num_hea
         cudaFuncSetAttribute(qkv_scatter2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         int per_sm = 0;
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qkv_scatter2_kernel, 256, smem);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, qkv_scatter2_kernel, kScatThreads,
+                                                      smem);
         const int64_t grid = std::min<int64_t>(n_rows, (int64_t)kNumSMs * std::max(per_sm, 1));
-        qkv_scatter2_kernel<<<(unsigned)grid, 256, smem, s>>>(
+        qkv_scatter2_kernel<<<(unsigned)grid, kScatThreads, smem, s>>>(
             (const __nv_bfloat16 *)qkv, n_rows, num_heads, make_arena(arena), row_req, row_pos,
             write_kv, layer, batch->block_table, batch->max_pages, rope ? rope->cos : nullptr,
             rope ? rope->sin : nullptr, (__nv_bfloat16 *)q_out, (__nv_bfloat16 *)k_out,
