@@ -27,6 +27,8 @@ else is libkvshare.so.  The residual stream is fp32, GEMM operands bf16.
 """
 from __future__ import annotations
 
+import os
+
 import math
 from dataclasses import dataclass, field
 
@@ -113,7 +115,14 @@ class RowSet:
             est = last.astype(np.float64)
             if kv_len is not None:
                 est = est / np.maximum(cnt[req], 1) * np.asarray(kv_len, np.float64)[req]
-            order = np.argsort(-est, kind="stable")
+            if os.environ.get("KVS_TILE_ORDER", "req") == "lpt":
+                order = np.argsort(-est, kind="stable")
+            else:
+                # request-major, longest first within a request: the CTAs in
+                # flight share one or two requests' K/V, which then stay in L2
+                # (global LPT interleaved all requests and re-read K/V from
+                # DRAM about 3x)
+                order = np.lexsort((-est, req))
             t = np.stack([req[order], row0[order], rows[order]]).astype(np.int32)
         else:
             t = np.zeros((3, 1), dtype=np.int32)
