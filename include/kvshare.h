@@ -268,7 +268,11 @@ kvs_status kvs_dhd_alpha(const void *q, int32_t num_heads, int32_t causal, int32
  * then per request keep budget[r] reused positions by (score desc, pos asc)
  * (selection.py:63-66); selected[t] = 1 for kept positions.  Non-reused
  * positions get score 0 and selected 0.  budget is host-computed with the
- * reference's IEEE-double ceil (selection.py:51-52).                       */
+ * reference's IEEE-double ceil (selection.py:51-52).  One launch for the
+ * whole batch.  Workspace: kvs_dhd_select_workspace(n_total, n_req) bytes
+ * (self-resetting counters, then one 32-bit selection key per position);
+ * its first 256 bytes must be zero before the first call on a buffer and
+ * are left zero by every call.                                              */
 size_t kvs_dhd_select_workspace(int64_t n_total, int32_t n_req);
 kvs_status kvs_dhd_select(const void *v_true, const float *alpha, const int32_t *src_slot,
                           int32_t layer, const kvs_kv_arena *arena, const kvs_batch *batch,
