@@ -324,261 +324,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-// ------------------------------------------------------------------ A1, head pairs
+constexpr int kThreads2 = 384;   // fwd3: WG0, WG1 softmax; WG2 = TMA warp, MMA warp, 2 idle
+
+// ------------------------------------------------------------------ A1, head pairs, P in TMEM
 // CTA = 128 query rows x TWO query heads of the same GQA group: both heads
 // read the same K/V tiles (one TMA stream, identical masks).  Warps 0-3 run
 // head a's softmax, warps 4-7 head b's, warp 8 = TMA, warp 9 = MMA.  TMEM:
-// S_a | S_b | O_a | O_b (128 columns each).  Shared memory: Q_a, Q_b, a
-// 3-slot ring carrying K(0), V(0), K(1), V(1), ... and P_a, P_b.
-constexpr int kThreads2 = 384;   // WG0, WG1 softmax; WG2 = TMA warp, MMA warp, 2 idle
-constexpr int RING = 3;
-
-struct Smem2 {
-    uint64_t q_full;
-    uint64_t ring_full[RING], ring_empty[RING];
-    uint64_t s_full[2], s_empty[2], p_full[2], pv_done[2];
-    uint32_t tmem_base;
-};
-
-__global__ void __launch_bounds__(kThreads2, 1)
-    fwd2_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
-                Params p) {
-    extern __shared__ uint8_t dsmem[];
-    __shared__ Smem2 sh;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tile = blockIdx.y, h0 = 2 * blockIdx.x;
-    const int g = h0 / (p.num_heads / p.kv_heads);
-    const int req = p.tile_req[tile], row0 = p.tile_row0[tile], nrows = p.tile_rows[tile];
-    const int kmax = p.causal ? p.row_pos[row0 + nrows - 1] + 1 : p.kv_len[req];
-    const int n_kb = (kmax + BN - 1) / BN;
-    const int pages_needed = (kmax + p.page_size - 1) / p.page_size;
-
-    const uint32_t base = align1024(smem_u32(dsmem));
-    const uint32_t sQ = base;                          // 2 tiles
-    const uint32_t sR = sQ + 2 * TILE_BYTES;           // RING tiles
-    const uint32_t sP = sR + RING * TILE_BYTES;        // 2 tiles
-    uint8_t *gbase = dsmem + (base - smem_u32(dsmem));
-
-    if (threadIdx.x == 0) {
-        mbar_init(&sh.q_full, 1);
-        for (int i = 0; i < RING; ++i) {
-            mbar_init(&sh.ring_full[i], 1);
-            mbar_init(&sh.ring_empty[i], 1);
-        }
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&sh.s_full[i], 1);
-            mbar_init(&sh.s_empty[i], 128);
-            mbar_init(&sh.p_full[i], 128);
-            mbar_init(&sh.pv_done[i], 1);
-        }
-        fence_barrier_init();
-    }
-    if (warp == 9) tmem_alloc(&sh.tmem_base, 512);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = sh.tmem_base;
-    if (warp >= 8) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
-    if (warp == 8) {
-        if (lane == 0) {
-            tma_prefetch(&map_q);
-            tma_prefetch(&map_kv);
-            mbar_expect_tx(&sh.q_full, 2 * TILE_BYTES);
-            for (int t = 0; t < 2; ++t)
-                for (int hf = 0; hf < 2; ++hf)
-                    tma_load_3d(gbase + (sQ - base) + t * TILE_BYTES + hf * HALF_BYTES, &map_q,
-                                &sh.q_full, hf * 64, h0 + t, row0);
-            const int32_t *bt = p.block_table + (int64_t)req * p.max_pages;
-            for (int it = 0; it < 2 * n_kb; ++it) {
-                const int kb = it >> 1, kv = it & 1, slot = it % RING;
-                if (it >= RING) mbar_wait(&sh.ring_empty[slot], (uint32_t)((it / RING) - 1) & 1u);
-                mbar_expect_tx(&sh.ring_full[slot], TILE_BYTES);
-                for (int q = 0; q < 2; ++q) {
-                    const int pi = 2 * kb + q;
-                    const int pg = bt[pi < pages_needed ? pi : 2 * kb];
-                    for (int hf = 0; hf < 2; ++hf)
-                        tma_load_4d(gbase + (sR - base) + slot * TILE_BYTES + hf * HALF_BYTES +
-                                        q * (HALF_BYTES / 2),
-                                    &map_kv, &sh.ring_full[slot], hf * 64, g, 0,
-                                    (pg * p.num_layers + p.layer) * 2 + kv);
-                }
-            }
-        }
-    } else if (warp == 9) {
-        if (lane == 0) {
-            const uint32_t idesc_qk = umma_idesc_bf16(BM, BN, false);
-            const uint32_t idesc_pv = umma_idesc_bf16(BM, HD, true);
-            mbar_wait(&sh.q_full, 0);
-            auto issue_pv = [&](int j) {
-                const int it = 2 * j + 1, slot = it % RING;  // V(j)
-                mbar_wait(&sh.ring_full[slot], (uint32_t)(it / RING) & 1u);
-                for (int t = 0; t < 2; ++t) {
-                    mbar_wait(&sh.p_full[t], (uint32_t)j & 1u);
-                    tc_fence_after();
-#pragma unroll
-                    for (int k = 0; k < BN / 16; ++k) {
-                        const uint64_t da = umma_desc_sw128(
-                            sP + t * TILE_BYTES + (k >> 2) * HALF_BYTES + (k & 3) * 32, 16, 1024);
-                        const uint64_t db = umma_desc_sw128(sR + slot * TILE_BYTES + k * 2048,
-                                                            HALF_BYTES, 1024);
-                        umma_bf16(tmem + 256 + 128 * t, da, db, idesc_pv, (j > 0 || k > 0) ? 1u : 0u);
-                    }
-                    umma_commit(&sh.pv_done[t]);
-                }
-                umma_commit(&sh.ring_empty[slot]);
-            };
-            for (int kb = 0; kb < n_kb; ++kb) {
-                const int it = 2 * kb, slot = it % RING;
-                mbar_wait(&sh.ring_full[slot], (uint32_t)(it / RING) & 1u);
-                for (int t = 0; t < 2; ++t) {
-                    if (kb >= 1) mbar_wait(&sh.s_empty[t], (uint32_t)(kb - 1) & 1u);
-                    tc_fence_after();
-#pragma unroll
-                    for (int k = 0; k < HD / 16; ++k) {
-                        const uint64_t da = umma_desc_sw128(
-                            sQ + t * TILE_BYTES + (k >> 2) * HALF_BYTES + (k & 3) * 32, 16, 1024);
-                        const uint64_t db = umma_desc_sw128(
-                            sR + slot * TILE_BYTES + (k >> 2) * HALF_BYTES + (k & 3) * 32, 16, 1024);
-                        umma_bf16(tmem + 128 * t, da, db, idesc_qk, k > 0 ? 1u : 0u);
-                    }
-                    umma_commit(&sh.s_full[t]);
-                }
-                umma_commit(&sh.ring_empty[slot]);
-                if (kb >= 1) issue_pv(kb - 1);
-            }
-            if (n_kb >= 1) issue_pv(n_kb - 1);
-        }
-        __syncwarp();
-    }
-    } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
-        // ------------------------------------------------------------ softmax, 2 warpgroups
-        const int t = warp >> 2;                 // head of this warpgroup
-        const int i = threadIdx.x & 127;         // row within tile == TMEM lane
-        const bool valid = i < nrows;
-        const int kend = !valid ? 0 : (p.causal ? p.row_pos[row0 + i] + 1 : kmax);
-        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-        const uint32_t tS = tmem + 128 * t, tO = tmem + 256 + 128 * t;
-        uint8_t *pP = gbase + (sP - base) + t * TILE_BYTES;
-        float m = -INFINITY, l = 0.f;
-        float s[BN];
-        for (int kb = 0; kb < n_kb; ++kb) {
-            mbar_wait(&sh.s_full[t], (uint32_t)kb & 1u);
-            tc_fence_after();
-#pragma unroll
-            for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS + lane_off + c * 32, s + c * 32);
-            tmem_ld_wait();
-            tc_fence_before();
-            mbar_arrive(&sh.s_empty[t]);
-            const int kbase = kb * BN;
-            float mx[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
-            if (kbase + BN <= kend) {
-#pragma unroll
-                for (int c = 0; c < BN; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
-            } else {
-#pragma unroll
-                for (int c = 0; c < BN; ++c) {
-                    s[c] = (kbase + c < kend) ? s[c] : -INFINITY;
-                    mx[c & 7] = fmaxf(mx[c & 7], s[c]);
-                }
-            }
-            const float mloc = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                     fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) *
-                               p.scale_log2;
-            // P buffer (and O, if rescaling) are free once the previous P.V retired
-            if (kb >= 1) mbar_wait(&sh.pv_done[t], (uint32_t)(kb - 1) & 1u);
-            const bool grow = mloc > m + kRescaleThreshold || (m == -INFINITY && mloc > -INFINITY);
-            const bool touch_o = grow && kb >= 1 && m != -INFINITY;
-            float factor = 1.f;
-            if (grow) {
-                factor = (m == -INFINITY) ? 0.f : fast_exp2(m - mloc);
-                l *= factor;
-                m = mloc;
-            }
-            if (__any_sync(0xffffffffu, touch_o)) {     // warp-collective tcgen05.ld/st
-                tc_fence_after();
-                const float f = touch_o ? factor : 1.f;
-                float o[32];
-#pragma unroll
-                for (int c = 0; c < HD / 32; ++c) {
-                    tmem_ld32(tO + lane_off + c * 32, o);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) o[e] *= f;
-                    tmem_st32(tO + lane_off + c * 32, o);
-                }
-                tmem_st_wait();
-                tc_fence_before();
-            }
-            const float mu = (m == -INFINITY) ? 0.f : m;
-            float ls[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) ls[j] = 0.f;
-            uint8_t *prow = pP + i * 128;
-#pragma unroll
-            for (int hf = 0; hf < 2; ++hf)
-#pragma unroll
-                for (int c = 0; c < 8; ++c) {
-                    float e[8];
-#pragma unroll
-                    for (int q = 0; q < 8; ++q) {
-                        e[q] = fast_exp2(fmaf(s[hf * 64 + c * 8 + q], p.scale_log2, -mu));
-                        ls[q] += e[q];
-                    }
-                    uint4 v;
-                    v.x = pack_bf16x2(e[0], e[1]);
-                    v.y = pack_bf16x2(e[2], e[3]);
-                    v.z = pack_bf16x2(e[4], e[5]);
-                    v.w = pack_bf16x2(e[6], e[7]);
-                    *reinterpret_cast<uint4 *>(prow + hf * HALF_BYTES + ((c ^ (i & 7)) << 4)) = v;
-                }
-            l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
-            fence_proxy_async_smem();
-            mbar_arrive(&sh.p_full[t]);
-        }
-        const int64_t grow = (int64_t)row0 + i;
-        if (n_kb >= 1) mbar_wait(&sh.pv_done[t], (uint32_t)(n_kb - 1) & 1u);
-        tc_fence_after();
-        const float inv = l > 0.f ? 1.f / l : 0.f;
-        float o[32];
-#pragma unroll
-        for (int c = 0; c < HD / 32; ++c) {
-            tmem_ld32(tO + lane_off + c * 32, o);
-            tmem_ld_wait();
-            if (valid) {
-                uint4 *dst = reinterpret_cast<uint4 *>(p.out + (grow * p.num_heads + h0 + t) * HD +
-                                                       c * 32);
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    uint4 w;
-                    w.x = pack_bf16x2(o[8 * v + 0] * inv, o[8 * v + 1] * inv);
-                    w.y = pack_bf16x2(o[8 * v + 2] * inv, o[8 * v + 3] * inv);
-                    w.z = pack_bf16x2(o[8 * v + 4] * inv, o[8 * v + 5] * inv);
-                    w.w = pack_bf16x2(o[8 * v + 6] * inv, o[8 * v + 7] * inv);
-                    dst[v] = w;
-                }
-            }
-        }
-        if (valid && p.lse != nullptr)
-            p.lse[grow * p.num_heads + h0 + t] =
-                (l > 0.f) ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 9) {
-        tc_fence_after();
-        tmem_dealloc(tmem, 512);
-    }
-}
-
-// ------------------------------------------------------------------ A1, head pairs, P in TMEM
-// As fwd2 (two query heads of one GQA group share every K/V tile), with the
-// FA4 arrangement: the softmax writes P (bf16, two per column) back over its
-// own S columns and O += P.V runs with A from tensor memory, so no P goes
-// through shared memory and the K/V ring gets 5 slots.  The MMA warp issues
+// S_a | S_b | O_a | O_b (128 columns each).  FA4 arrangement: the softmax
+// writes P (bf16, two per column) back over its own S columns and O += P.V
+// runs with A from tensor memory, so no P goes through shared memory and the
+// K/V ring gets 5 slots.  The MMA warp issues
 // PV_a(kb), QK_a(kb+1), PV_b(kb), QK_b(kb+1): in-order tcgen05 execution
 // makes QK_t(kb+1) overwrite S/P only after PV_t(kb) has read P, and each
 // head's softmax overlaps the other head's two MMAs.
@@ -1103,238 +858,6 @@ __global__ void __launch_bounds__(kThreads6, 1)
     }
 }
 
-// ------------------------------------------------------------------ A1, head pairs, 64-key blocks
-// fwd3 with BN = 64 and TWO S/P buffers per head: TMEM per head t is
-// S_t[0] | S_t[1] (64 fp32 columns each; P bf16 overwrites 32 of them) | O_t
-// (128).  The MMA warp issues QK_a(kb+1), QK_b(kb+1) before PV_a(kb), PV_b(kb),
-// so a head's next scores are computed while its softmax still runs and the
-// softmax warpgroups work back to back.  In-order tcgen05 execution protects
-// P(kb-1) (same buffer as S(kb+1)) until PV(kb-1) has read it.  K/V tiles are
-// one 64-row page each; 10-slot ring.
-constexpr int BN4 = 64;
-constexpr int TILE4 = BN4 * 256;        // [64 rows x 128 bf16] = 16 KB (two 8 KB halves)
-constexpr int HALF4 = BN4 * 128;
-constexpr int RING4 = 10;
-
-struct Smem4 {
-    uint64_t q_full;
-    uint64_t ring_full[RING4], ring_empty[RING4];
-    uint64_t s_full[2][2], p_full[2][2], pv_done[2];
-    uint32_t tmem_base;
-};
-
-__global__ void __launch_bounds__(kThreads2, 1)
-    fwd4_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
-                Params p) {
-    extern __shared__ uint8_t dsmem[];
-    __shared__ Smem4 sh;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tile = blockIdx.y, h0 = 2 * blockIdx.x;
-    const int g = h0 / (p.num_heads / p.kv_heads);
-    const int req = p.tile_req[tile], row0 = p.tile_row0[tile], nrows = p.tile_rows[tile];
-    const int kmax = p.causal ? p.row_pos[row0 + nrows - 1] + 1 : p.kv_len[req];
-    const int n_kb = (kmax + BN4 - 1) / BN4;          // == pages touched (page_size 64)
-
-    const uint32_t base = align1024(smem_u32(dsmem));
-    const uint32_t sQ = base;                          // 2 x 32 KB
-    const uint32_t sR = sQ + 2 * TILE_BYTES;           // RING4 x 16 KB
-    uint8_t *gbase = dsmem + (base - smem_u32(dsmem));
-
-    if (threadIdx.x == 0) {
-        mbar_init(&sh.q_full, 1);
-        for (int i = 0; i < RING4; ++i) {
-            mbar_init(&sh.ring_full[i], 1);
-            mbar_init(&sh.ring_empty[i], 1);
-        }
-        for (int t = 0; t < 2; ++t) {
-            for (int b = 0; b < 2; ++b) {
-                mbar_init(&sh.s_full[t][b], 1);
-                mbar_init(&sh.p_full[t][b], 128);
-            }
-            mbar_init(&sh.pv_done[t], 1);
-        }
-        fence_barrier_init();
-    }
-    if (warp == 9) tmem_alloc(&sh.tmem_base, 512);
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    const uint32_t tmem = sh.tmem_base;
-    // TMEM columns: head t at 256*t: S buffers at +0 / +64, O at +128
-    if (warp >= 8) {
-        asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
-        if (warp == 8 && lane == 0) {
-            tma_prefetch(&map_q);
-            tma_prefetch(&map_kv);
-            mbar_expect_tx(&sh.q_full, 2 * TILE_BYTES);
-            for (int t = 0; t < 2; ++t)
-                for (int hf = 0; hf < 2; ++hf)
-                    tma_load_3d(gbase + (sQ - base) + t * TILE_BYTES + hf * HALF_BYTES, &map_q,
-                                &sh.q_full, hf * 64, h0 + t, row0);
-            const int32_t *bt = p.block_table + (int64_t)req * p.max_pages;
-            for (int it = 0; it < 2 * n_kb; ++it) {
-                const int kb = it >> 1, kv = it & 1, slot = it % RING4;
-                if (it >= RING4) mbar_wait(&sh.ring_empty[slot], (uint32_t)((it / RING4) - 1) & 1u);
-                mbar_expect_tx(&sh.ring_full[slot], TILE4);
-                const int pg = bt[kb];
-                for (int hf = 0; hf < 2; ++hf)
-                    tma_load_4d(gbase + (sR - base) + slot * TILE4 + hf * HALF4, &map_kv,
-                                &sh.ring_full[slot], hf * 64, g, 0,
-                                (pg * p.num_layers + p.layer) * 2 + kv);
-            }
-        } else if (warp == 9 && lane == 0) {
-            const uint32_t idesc_qk = umma_idesc_bf16(BM, BN4, false);
-            const uint32_t idesc_pv = umma_idesc_bf16(BM, HD, true);
-            mbar_wait(&sh.q_full, 0);
-            auto issue_qk = [&](int kb) {
-                const int it = 2 * kb, slot = it % RING4;
-                mbar_wait(&sh.ring_full[slot], (uint32_t)(it / RING4) & 1u);
-                tc_fence_after();
-                for (int t = 0; t < 2; ++t) {
-#pragma unroll
-                    for (int k = 0; k < HD / 16; ++k) {
-                        const uint64_t da = umma_desc_sw128(
-                            sQ + t * TILE_BYTES + (k >> 2) * HALF_BYTES + (k & 3) * 32, 16, 1024);
-                        const uint64_t db = umma_desc_sw128(
-                            sR + slot * TILE4 + (k >> 2) * HALF4 + (k & 3) * 32, 16, 1024);
-                        umma_bf16(tmem + 256 * t + 64 * (kb & 1), da, db, idesc_qk, k > 0 ? 1u : 0u);
-                    }
-                    umma_commit(&sh.s_full[t][kb & 1]);
-                }
-                umma_commit(&sh.ring_empty[slot]);
-            };
-            if (n_kb >= 1) issue_qk(0);
-            for (int kb = 0; kb < n_kb; ++kb) {
-                if (kb + 1 < n_kb) issue_qk(kb + 1);
-                const int it = 2 * kb + 1, slot = it % RING4;
-                mbar_wait(&sh.ring_full[slot], (uint32_t)(it / RING4) & 1u);
-                for (int t = 0; t < 2; ++t) {
-                    mbar_wait(&sh.p_full[t][kb & 1], (uint32_t)(kb >> 1) & 1u);
-                    tc_fence_after();
-#pragma unroll
-                    for (int k = 0; k < BN4 / 16; ++k) {
-                        const uint64_t db =
-                            umma_desc_sw128(sR + slot * TILE4 + k * 2048, HALF4, 1024);
-                        umma_bf16_ts(tmem + 256 * t + 128, tmem + 256 * t + 64 * (kb & 1) + 8 * k,
-                                     db, idesc_pv, (kb > 0 || k > 0) ? 1u : 0u);
-                    }
-                    umma_commit(&sh.pv_done[t]);
-                }
-                umma_commit(&sh.ring_empty[slot]);
-            }
-        }
-        __syncwarp();
-    } else {
-        asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
-        const int t = warp >> 2;
-        const int i = threadIdx.x & 127;
-        const bool valid = i < nrows;
-        const int kend = !valid ? 0 : (p.causal ? p.row_pos[row0 + i] + 1 : kmax);
-        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
-        const uint32_t tH = tmem + 256 * t + lane_off, tO = tH + 128;
-        float m = -INFINITY, l = 0.f;
-        float s[BN4];
-        for (int kb = 0; kb < n_kb; ++kb) {
-            const int b = kb & 1;
-            mbar_wait(&sh.s_full[t][b], (uint32_t)(kb >> 1) & 1u);
-            tc_fence_after();
-            tmem_ld32(tH + 64 * b, s);
-            tmem_ld32(tH + 64 * b + 32, s + 32);
-            tmem_ld_wait();
-            const int kbase = kb * BN4;
-            float mx[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
-            if (kbase + BN4 <= kend) {
-#pragma unroll
-                for (int c = 0; c < BN4; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
-            } else {
-#pragma unroll
-                for (int c = 0; c < BN4; ++c) {
-                    s[c] = (kbase + c < kend) ? s[c] : -INFINITY;
-                    mx[c & 7] = fmaxf(mx[c & 7], s[c]);
-                }
-            }
-            const float mloc = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                     fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) *
-                               p.scale_log2;
-            const bool grow = mloc > m + kRescaleThreshold || (m == -INFINITY && mloc > -INFINITY);
-            const bool touch_o = grow && kb >= 1 && m != -INFINITY;
-            float factor = 1.f;
-            if (grow) {
-                factor = (m == -INFINITY) ? 0.f : fast_exp2(m - mloc);
-                l *= factor;
-                m = mloc;
-            }
-            if (__any_sync(0xffffffffu, touch_o)) {     // warp-collective tcgen05.ld/st
-                // PV(kb-1) may still be queued: O is touched only after it retired
-                mbar_wait(&sh.pv_done[t], (uint32_t)(kb - 1) & 1u);
-                tc_fence_after();
-                const float f = touch_o ? factor : 1.f;
-                float o[32];
-#pragma unroll
-                for (int c = 0; c < HD / 32; ++c) {
-                    tmem_ld32(tO + c * 32, o);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) o[e] *= f;
-                    tmem_st32(tO + c * 32, o);
-                }
-            }
-            const float mu = (m == -INFINITY) ? 0.f : m;
-            float ls[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) ls[j] = 0.f;
-            uint32_t pk[32];
-#pragma unroll
-            for (int q = 0; q < 32; ++q) {
-                const float e0 = fast_exp2(fmaf(s[2 * q], p.scale_log2, -mu));
-                const float e1 = fast_exp2(fmaf(s[2 * q + 1], p.scale_log2, -mu));
-                ls[(2 * q) & 7] += e0;
-                ls[(2 * q + 1) & 7] += e1;
-                pk[q] = pack_bf16x2(e0, e1);
-            }
-            tmem_st32(tH + 64 * b, reinterpret_cast<const float *>(pk));
-            l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
-            tmem_st_wait();
-            tc_fence_before();
-            mbar_arrive(&sh.p_full[t][b]);
-        }
-        const int64_t grow = (int64_t)row0 + i;
-        if (n_kb >= 1) mbar_wait(&sh.pv_done[t], (uint32_t)(n_kb - 1) & 1u);
-        tc_fence_after();
-        const float inv = l > 0.f ? 1.f / l : 0.f;
-        float o[32];
-#pragma unroll
-        for (int c = 0; c < HD / 32; ++c) {
-            tmem_ld32(tO + c * 32, o);
-            tmem_ld_wait();
-            if (valid) {
-                uint4 *dst = reinterpret_cast<uint4 *>(p.out + (grow * p.num_heads + h0 + t) * HD +
-                                                       c * 32);
-#pragma unroll
-                for (int v = 0; v < 4; ++v) {
-                    uint4 w;
-                    w.x = pack_bf16x2(o[8 * v + 0] * inv, o[8 * v + 1] * inv);
-                    w.y = pack_bf16x2(o[8 * v + 2] * inv, o[8 * v + 3] * inv);
-                    w.z = pack_bf16x2(o[8 * v + 4] * inv, o[8 * v + 5] * inv);
-                    w.w = pack_bf16x2(o[8 * v + 6] * inv, o[8 * v + 7] * inv);
-                    dst[v] = w;
-                }
-            }
-        }
-        if (valid && p.lse != nullptr)
-            p.lse[grow * p.num_heads + h0 + t] =
-                (l > 0.f) ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
-    }
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 9) {
-        tc_fence_after();
-        tmem_dealloc(tmem, 512);
-    }
-}
-
 // ------------------------------------------------------------------ D1 pass 2
 // CTA = (key tile kt of request r, kv head g).  Loops over the group's query
 // heads and the query tiles that can see the keys; S^T lands with one key per
@@ -1578,28 +1101,19 @@ kvs_status kvs_attention_fwd(const void *q, const int32_t *row_pos, int64_t n_ro
     const int group = num_heads / arena->kv_heads;
     const char *variant = getenv("KVS_ATTN");
     // default: head pairs (fwd3) for even GQA groups, single heads with
-    // double-buffered S (fwd6) otherwise; KVS_ATTN=1|2|4|6 pins a variant
+    // double-buffered S (fwd6) otherwise; KVS_ATTN=1|3|6 pins a variant
+    // (1: the single-head kernel with P through shared memory)
     const char v = variant != nullptr ? variant[0] : (group % 2 == 0 ? '3' : '6');
     if (out != nullptr && (v == '6' || (v != '1' && group % 2 != 0))) {
         const size_t smem = 1024 + attn::TILE_BYTES * (1 + attn::RING6);
         cudaFuncSetAttribute(attn::fwd6_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         attn::fwd6_kernel<<<dim3(num_heads, n_tiles), attn::kThreads6, smem, s>>>(mq, mkv, p);
-    } else if (out != nullptr && group % 2 == 0 && v == '4') {
-        const size_t smem = 1024 + 2 * attn::TILE_BYTES + attn::RING4 * attn::TILE4;
-        cudaFuncSetAttribute(attn::fwd4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        attn::fwd4_kernel<<<dim3(num_heads / 2, n_tiles), attn::kThreads2, smem, s>>>(mq, mkv, p);
     } else if (out != nullptr && group % 2 == 0 && v == '3') {
         const size_t smem = 1024 + attn::TILE_BYTES * (2 + attn::RING3);
         cudaFuncSetAttribute(attn::fwd3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         attn::fwd3_kernel<<<dim3(num_heads / 2, n_tiles), attn::kThreads2, smem, s>>>(mq, mkv, p);
-    } else if (out != nullptr && group % 2 == 0 && v == '2') {
-        const size_t smem = 1024 + attn::TILE_BYTES * (2 + attn::RING + 2);
-        cudaFuncSetAttribute(attn::fwd2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem);
-        attn::fwd2_kernel<<<dim3(num_heads / 2, n_tiles), attn::kThreads2, smem, s>>>(mq, mkv, p);
     } else if (out != nullptr) {
         const size_t smem = fwd_smem<true>();
         cudaFuncSetAttribute(attn::fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
