@@ -204,6 +204,15 @@ kvs_status kvs_qkv_rope_scatter(const void *qkv, int64_t n_rows, int32_t num_hea
                                 const kvs_kv_arena *arena, const kvs_batch *batch,
                                 const kvs_rope *rope, void *q_out, void *k_out, void *v_out,
                                 kvs_stream_t stream);
+/* Same, reading output row i's q|k|v from qkv[src_row[i]] (head_dim 128):
+ * the partial prefill's first session layer takes its rows of the probe's
+ * all-row projection instead of projecting them again.                     */
+kvs_status kvs_qkv_rope_scatter_rows(const void *qkv, const int32_t *src_row, int64_t n_rows,
+                                     int32_t num_heads, const int32_t *row_req,
+                                     const int32_t *row_pos, const uint8_t *write_kv,
+                                     int32_t layer, const kvs_kv_arena *arena,
+                                     const kvs_batch *batch, const kvs_rope *rope, void *q_out,
+                                     void *k_out, void *v_out, kvs_stream_t stream);
 
 /* Embedding rows: out[r] = table[ids[rows ? rows[r] : r]] (width bf16 each);
  * out_f32 (nullable) receives the same rows widened to fp32 (the residual

@@ -236,7 +236,7 @@ __global__ void __launch_bounds__(kScatThreads) qkv_scatter2_kernel(
     const uint8_t *__restrict__ write_kv, int32_t layer, const int32_t *__restrict__ block_table,
     int32_t max_pages, const float *__restrict__ cos_t, const float *__restrict__ sin_t,
     __nv_bfloat16 *__restrict__ q_out, __nv_bfloat16 *__restrict__ k_out,
-    __nv_bfloat16 *__restrict__ v_out) {
+    __nv_bfloat16 *__restrict__ v_out, const int32_t *__restrict__ src_row) {
     extern __shared__ __align__(128) uint8_t s_rows[];          // kScatSlots x row bytes
     __shared__ __align__(16) float s_cs[kScatSlots][2][64];
     __shared__ ScatMeta s_meta[kScatSlots];
@@ -259,7 +259,8 @@ __global__ void __launch_bounds__(kScatThreads) qkv_scatter2_kernel(
         const int64_t row = (int64_t)blockIdx.x + k * gridDim.x;
         if (tid == 0) {
             mbar_expect_tx(&bars[slot], row_bytes);
-            bulk_g2s(smem_u32(s_rows) + (uint32_t)slot * row_bytes, qkv + row * width, row_bytes,
+            const int64_t src = src_row != nullptr ? (int64_t)src_row[row] : row;
+            bulk_g2s(smem_u32(s_rows) + (uint32_t)slot * row_bytes, qkv + src * width, row_bytes,
                      &bars[slot]);
         } else if (tid >= 32 && tid < 64) {
             const int lane = tid - 32;
@@ -519,7 +520,8 @@ kvs_status kvs_gather_kv(const kvs_kv_arena *arena, const kvs_batch *batch,
     return KVS_OK;
 }
 
-kvs_status kvs_qkv_rope_scatter(const void *qkv, int64_t n_rows, int32_t num_heads,
+static kvs_status qkv_scatter_impl(const void *qkv, const int32_t *src_row, int64_t n_rows,
+                                int32_t num_heads,
                                 const int32_t *row_req, const int32_t *row_pos,
                                 const uint8_t *write_kv, int32_t layer, const kvs_kv_arena *arena,
                                 const kvs_batch *batch, const kvs_rope *rope, void *q_out,
@@ -542,8 +544,10 @@ kvs_status kvs_qkv_rope_scatter(const void *qkv, int64_t n_rows, int32_t num_hea
             (const __nv_bfloat16 *)qkv, n_rows, num_heads, make_arena(arena), row_req, row_pos,
             write_kv, layer, batch->block_table, batch->max_pages, rope ? rope->cos : nullptr,
             rope ? rope->sin : nullptr, (__nv_bfloat16 *)q_out, (__nv_bfloat16 *)k_out,
-            (__nv_bfloat16 *)v_out);
+            (__nv_bfloat16 *)v_out, src_row);
     } else {
+        KVS_REQUIRE(src_row == nullptr, KVS_EPARAM,
+                    "row-indexed scatter needs head_dim 128 (the TMA-ring kernel)");
         qkv_rope_scatter_kernel<<<(unsigned)n_rows, 256, 0, s>>>(
             (const __nv_bfloat16 *)qkv, num_heads, make_arena(arena), row_req, row_pos, write_kv,
             layer, batch->block_table, batch->max_pages, rope ? rope->cos : nullptr,
@@ -552,6 +556,26 @@ kvs_status kvs_qkv_rope_scatter(const void *qkv, int64_t n_rows, int32_t num_hea
     }
     KVS_CHECK_LAUNCH("kvs_qkv_rope_scatter");
     return KVS_OK;
+}
+
+kvs_status kvs_qkv_rope_scatter(const void *qkv, int64_t n_rows, int32_t num_heads,
+                                const int32_t *row_req, const int32_t *row_pos,
+                                const uint8_t *write_kv, int32_t layer, const kvs_kv_arena *arena,
+                                const kvs_batch *batch, const kvs_rope *rope, void *q_out,
+                                void *k_out, void *v_out, kvs_stream_t stream) {
+    return qkv_scatter_impl(qkv, nullptr, n_rows, num_heads, row_req, row_pos, write_kv, layer,
+                            arena, batch, rope, q_out, k_out, v_out, stream);
+}
+
+kvs_status kvs_qkv_rope_scatter_rows(const void *qkv, const int32_t *src_row, int64_t n_rows,
+                                     int32_t num_heads, const int32_t *row_req,
+                                     const int32_t *row_pos, const uint8_t *write_kv,
+                                     int32_t layer, const kvs_kv_arena *arena,
+                                     const kvs_batch *batch, const kvs_rope *rope, void *q_out,
+                                     void *k_out, void *v_out, kvs_stream_t stream) {
+    KVS_REQUIRE(src_row != nullptr, KVS_EPARAM, "null src_row");
+    return qkv_scatter_impl(qkv, src_row, n_rows, num_heads, row_req, row_pos, write_kv, layer,
+                            arena, batch, rope, q_out, k_out, v_out, stream);
 }
 
 kvs_status kvs_embed_rows(const void *table, int64_t width, const int64_t *ids,

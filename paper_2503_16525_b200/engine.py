@@ -300,8 +300,14 @@ class Engine:
                batch_c, self.scale, out.data_ptr(), ws.data_ptr(), ws.numel(), N.stream_ptr())
 
     def _scatter(self, qkv, rows: RowSet, layer, arena_c, batch_c, q_out, write_kv=None,
-                 k_out=None, v_out=None, use_write=True):
+                 k_out=None, v_out=None, use_write=True, src_row=None):
         wk = write_kv if write_kv is not None else (rows.write_kv if use_write else None)
+        if src_row is not None:
+            N.call("kvs_qkv_rope_scatter_rows", qkv.data_ptr(), src_row.data_ptr(), rows.n_rows,
+                   self.cfg.num_heads, rows.row_req.data_ptr(), rows.row_pos.data_ptr(),
+                   N.ptr(wk), layer, arena_c, batch_c, self._rope(), q_out.data_ptr(),
+                   N.ptr(k_out), N.ptr(v_out), N.stream_ptr())
+            return
         N.call("kvs_qkv_rope_scatter", qkv.data_ptr(), rows.n_rows, self.cfg.num_heads,
                rows.row_req.data_ptr(), rows.row_pos.data_ptr(), N.ptr(wk), layer, arena_c,
                batch_c, self._rope(), q_out.data_ptr(), N.ptr(k_out), N.ptr(v_out),
@@ -321,16 +327,22 @@ class Engine:
         return x
 
     def forward_rows(self, x, rows: RowSet, layers, arena_c, batch_c, decode=False,
-                     max_kv=0, write_kv_per_layer=None, capture=None):
-        """Layer loop over a row set: x (fp32 [n, d_model]) updated in place."""
+                     max_kv=0, write_kv_per_layer=None, capture=None, first_qkv=None):
+        """Layer loop over a row set: x (fp32 [n, d_model]) updated in place.
+        first_qkv = (qkv, src_row): the first layer's projection rows already
+        exist (row i is qkv[src_row[i]]) and are not recomputed."""
         cfg, m = self.cfg, self.model
         H, n = cfg.num_heads, rows.n_rows
         q = self.scratch.get("q", (n, H, HEAD_DIM), torch.bfloat16)
         o = self.scratch.get("o", (n, H, HEAD_DIM), torch.bfloat16)
-        for layer in layers:
-            qkv = self._qkv(x, layer)
+        for i, layer in enumerate(layers):
             wk = write_kv_per_layer[layer] if write_kv_per_layer is not None else None
-            self._scatter(qkv, rows, layer, arena_c, batch_c, q, write_kv=wk)
+            if i == 0 and first_qkv is not None:
+                self._scatter(first_qkv[0], rows, layer, arena_c, batch_c, q, write_kv=wk,
+                              src_row=first_qkv[1])
+            else:
+                qkv = self._qkv(x, layer)
+                self._scatter(qkv, rows, layer, arena_c, batch_c, q, write_kv=wk)
             if decode:
                 self._decode_attention(q, rows, layer, arena_c, batch_c, o, max_kv)
             else:
@@ -436,6 +448,11 @@ class Engine:
             torch.zeros(n, dtype=torch.uint8, device=dev)
         self._scatter(qkv, rows, p, self.arena.c, st.batch_c, q1, write_kv=wk, k_out=k_out,
                       v_out=v_true)
+        if p == 1 and layer0_in_place:
+            # rows S of this all-row layer-1 projection are the partial
+            # prefill's layer-1 projection (same x rows): session_forward reuses
+            # them; the buffer stays intact until its layer-2 GEMM
+            st._qkv1 = qkv
         return rows, q1, v_true
 
     def _select(self, st: BatchState, v_true, alpha, budgets):
@@ -515,8 +532,11 @@ class Engine:
             x = self._embed(st.tokens, rows, scratch=capture is None)
             first = 0
         st.session_first = first
+        qkv1 = getattr(st, "_qkv1", None) if x_probe is not None else None
+        st._qkv1 = None
         x = self.forward_rows(x, rows, range(first, self.cfg.num_layers), self.arena.c,
-                              st.batch_c, capture=capture)
+                              st.batch_c, capture=capture,
+                              first_qkv=(qkv1, rows.row_tok) if qkv1 is not None else None)
         last = h2d(rows.row_off[1:] - 1, self.device)
         st.rows = rows
         st.hidden_last = x[last]
