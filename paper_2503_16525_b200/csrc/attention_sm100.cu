@@ -1017,6 +1017,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 __global__ void alpha_reduce_kernel(const float *__restrict__ part, int64_t n, int32_t G, int32_t H,
                                     float *__restrict__ alpha) {
+    // D2 (launched programmatically dependent) may start its prologue now;
+    // it waits for this grid's completion before it reads alpha
+    asm volatile("griddepcontrol.launch_dependents;");
     for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < n;
          t += (int64_t)gridDim.x * blockDim.x) {
         float s = 0.f;

@@ -9,6 +9,7 @@
 //   q_t . K over the whole current context per query head, mean over heads,
 //   times the prefill dv-L1, top n_extra over the eligible rows.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -645,6 +646,7 @@ __global__ void __launch_bounds__(kSelThreads, 1) dhd_select_fused_kernel(
     int32_t p_page = 0, p_r = 0;
     float p_alpha = 0.f;
     int64_t p_t = -1;
+    bool dep_done = false;
     auto issue_meta = [&](int64_t c) {
         p_t = -1;
         if (c >= NC || tid >= kChunkRows) return;
@@ -659,7 +661,13 @@ __global__ void __launch_bounds__(kSelThreads, 1) dhd_select_fused_kernel(
         p_t = t;
         p_live = __ldg(src_slot + t) >= 0;
         p_page = __ldg(block_table + (int64_t)r * max_pages + i / A.P);
-        p_alpha = __ldg(alpha + t);
+        if (!dep_done) {
+            // launched as a programmatic dependent of D1's reduce: everything
+            // above overlaps it; alpha is its output
+            asm volatile("griddepcontrol.wait;" ::: "memory");
+            dep_done = true;
+        }
+        p_alpha = __ldcg(alpha + t);
         p_r = (int32_t)(i % A.P);
     };
     // append chunk `cur`'s live rows to the queue, move on to the next chunk
@@ -713,6 +721,10 @@ __global__ void __launch_bounds__(kSelThreads, 1) dhd_select_fused_kernel(
 
     int tail = 0;
     issue_meta(cur);
+    if (!dep_done) {                 // threads without rows in the first chunk
+        asm volatile("griddepcontrol.wait;" ::: "memory");
+        dep_done = true;
+    }
     tail = finish_meta(tail);
     SEL_TRACE(1);
     // keep the queue kDepth stages ahead of the stage being reduced
@@ -1265,10 +1277,23 @@ kvs_status kvs_dhd_select(const void *v_true, const float *alpha, const int32_t 
     KVS_REQUIRE(smem <= 227 * 1024, KVS_EPARAM, "select: too many requests in one batch");
     cudaFuncSetAttribute(dhd_select_fused_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
-    dhd_select_fused_kernel<<<kNumSMs, kSelThreads, smem, s>>>(
-        (const __nv_bfloat16 *)v_true, alpha, src_slot, layer, arena_c(arena), batch->req_off,
-        batch->n_req, budget, batch->block_table, batch->max_pages, dv_l1, score, selected,
-        counters, reinterpret_cast<uint32_t *>((uint8_t *)ws + 256));
+    // programmatic dependent launch: the prologue (request offsets, the first
+    // chunk's liveness and page loads) overlaps the preceding kernel (D1's
+    // reduce); the kernel waits for it before reading alpha
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(kNumSMs);
+    lc.blockDim = dim3(kSelThreads);
+    lc.dynamicSmemBytes = smem;
+    lc.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    lc.attrs = attr;
+    lc.numAttrs = getenv("KVS_NO_PDL") == nullptr ? 1 : 0;
+    cudaLaunchKernelEx(&lc, dhd_select_fused_kernel, (const __nv_bfloat16 *)v_true, alpha,
+                       src_slot, layer, arena_c(arena), batch->req_off, batch->n_req, budget,
+                       batch->block_table, batch->max_pages, dv_l1, score, selected, counters,
+                       reinterpret_cast<uint32_t *>((uint8_t *)ws + 256));
     KVS_CHECK_LAUNCH("kvs_dhd_select");
     return KVS_OK;
 }
