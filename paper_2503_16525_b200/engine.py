@@ -526,7 +526,7 @@ class Engine:
         after layer 0) the pass starts at layer 1 from rows S of it."""
         if x_probe is not None:
             x = self.scratch.get("x_s", (rows.n_rows, self.cfg.d_model), torch.float32)
-            torch.index_select(x_probe, 0, rows.row_tok.long(), out=x)
+            torch.index_select(x_probe, 0, rows.row_tok, out=x)
             first = 1
         else:
             x = self._embed(st.tokens, rows, scratch=capture is None)
@@ -537,7 +537,10 @@ class Engine:
         x = self.forward_rows(x, rows, range(first, self.cfg.num_layers), self.arena.c,
                               st.batch_c, capture=capture,
                               first_qkv=(qkv1, rows.row_tok) if qkv1 is not None else None)
-        last = h2d(rows.row_off[1:] - 1, self.device)
+        keep = getattr(rows, "_keep", None)
+        # last row of each request: from the device copy of row_off when the
+        # row set was built on the device (no host->device copy here)
+        last = keep[0][1:] - 1 if keep is not None else h2d(rows.row_off[1:] - 1, self.device)
         st.rows = rows
         st.hidden_last = x[last]
         return x
