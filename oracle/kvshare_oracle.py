@@ -263,8 +263,55 @@ def expand_kv(k, group):
     return np.repeat(k, group, axis=0) if group > 1 else k
 
 
+# Above this many attention-matrix elements the restatement runs one query
+# head at a time (same formula per element, bounded memory): Llama-width
+# prefill at 4k-16k tokens would otherwise need (H, n, n) float64 temporaries
+# of 4-60 GB.
+_BIG = 1 << 25
+
+
+def _heads_parallel(fn, H):
+    """fn(h) for every head; numpy's BLAS and ufuncs release the GIL, so a
+    thread pool spreads heads over the host cores."""
+    from concurrent.futures import ThreadPoolExecutor
+    workers = max(1, min(H, (os.cpu_count() or 1) // 2, 16))
+    if workers == 1:
+        return [fn(h) for h in range(H)]
+    with ThreadPoolExecutor(workers) as ex:
+        return list(ex.map(fn, range(H)))
+
+
+def attention_rows(q, qpos, k, v, group=1):
+    """model.py:110-129 for a subset of query rows: q (H, m, d) at absolute
+    positions qpos[m], keys/values (kvh, n, d); key j is visible to a row at
+    position p iff j <= p (softmax_rows' causal mask, model.py:102-104, read
+    per row).  With qpos = arange(n) this is attention(q, k, v, causal=True).
+    One head at a time; returns (H, m, d)."""
+    H, m, d = q.shape
+    n = k.shape[1]
+    qpos = np.asarray(qpos, dtype=np.int64)
+    hidden = np.arange(n)[None, :] > qpos[:, None]
+    scale = 1.0 / math.sqrt(d)
+    out = np.empty((H, m, v.shape[-1]))
+
+    def one(h):
+        g = h // group
+        logits = q[h] @ k[g].T * scale
+        logits[hidden] = -np.inf
+        logits -= logits.max(axis=-1, keepdims=True)
+        np.exp(logits, out=logits)
+        logits /= logits.sum(axis=-1, keepdims=True)
+        out[h] = logits @ v[g]
+
+    _heads_parallel(one, H)
+    return out
+
+
 def attention(q, k, v, causal=True, group=1):
-    """model.py:110-129 with GQA expansion: (H,n,d),(kvh,n,d) -> (H,n,d)."""
+    """model.py:110-129 with GQA expansion: (H,n,d),(kvh,n,d) -> (H,n,d).
+    Large causal problems go through attention_rows (attn is then None)."""
+    if causal and q.ndim == 3 and q.shape[0] * q.shape[1] * k.shape[1] > _BIG:
+        return attention_rows(q, np.arange(q.shape[1]), k, v, group), None
     k, v = expand_kv(k, group), expand_kv(v, group)
     attn = softmax_rows(q @ np.swapaxes(k, -1, -2) / math.sqrt(q.shape[-1]), causal=causal)
     return attn @ v, attn
@@ -340,6 +387,61 @@ def forward(tokens, W, cfg: OracleConfig, reuse: Reuse | None = None,
             "head_out": np.stack(outs), "hidden": np.stack(hid)}
 
 
+def partial_rows(n, reused, selected):
+    """SURVEY.md A12 row set S = non-reused U selected U {n-1}, ascending."""
+    keep = np.ones(n, dtype=bool)
+    keep[list(reused)] = False
+    keep[list(selected)] = True
+    keep[n - 1] = True
+    return np.nonzero(keep)[0]
+
+
+def forward_rows(tokens, W, cfg: OracleConfig, reuse: Reuse | None, selected, rows=None,
+                 table=None):
+    """model.py:163-208 (_forward with one recompute set at every layer,
+    engine.py:241) computing query rows ``rows`` only - by default the row
+    set S of :func:`partial_rows`.  Every row whose K/V is fresh (non-reused
+    or selected) must be in ``rows``: then the K/V caches are complete and the
+    hidden states of the computed rows equal the full forward's rows
+    (verified 0.0 difference; pinned here by
+    tests/test_oracle_golden.py against the reference's own prefill states).
+
+    Returns {"rows": rows, "hidden": (L+1, m, d_model) for those rows,
+    "k"/"v": (L, kvh, n, d_k) complete caches}."""
+    tokens = np.asarray(tokens, dtype=np.int64)
+    n = tokens.size
+    reused = reuse.reused if reuse is not None else []
+    selected = sorted(set(int(s) for s in selected))
+    rows = partial_rows(n, reused, selected) if rows is None else \
+        np.asarray(sorted(set(int(r) for r in rows)), dtype=np.int64)
+    fresh = np.ones(n, dtype=bool)
+    fresh[reused] = False
+    fresh[selected] = True
+    in_rows = np.zeros(n, dtype=bool)
+    in_rows[rows] = True
+    if (fresh & ~in_rows).any():
+        raise ValueError("every fresh (non-reused or selected) row must be computed")
+    write = fresh[rows]
+    x = W["embedding"][tokens[rows]]
+    hid, ks, vs = [x], [], []
+    for layer in range(cfg.num_layers):
+        w = W["layers"][layer]
+        q, k_r, v_r = _qkv(x, w, cfg, table, rows)
+        K = np.zeros((cfg.kvh, n, k_r.shape[-1]))
+        V = np.zeros_like(K)
+        if reuse is not None and reused:
+            rpos, kr, vr = reuse.cached_rows(layer, table)
+            K[:, rpos], V[:, rpos] = kr, vr
+        K[:, rows[write]] = k_r[:, write]
+        V[:, rows[write]] = v_r[:, write]
+        out = attention_rows(q, rows, K, V, cfg.group)
+        x = x + merge_heads(out) @ w[3]
+        hid.append(x)
+        ks.append(K)
+        vs.append(V)
+    return {"rows": rows, "hidden": np.stack(hid), "k": np.stack(ks), "v": np.stack(vs)}
+
+
 def exact_hidden_at(tokens, W, cfg, layer, table=None):
     """engine.py:182-192."""
     tokens = np.asarray(tokens, dtype=np.int64)
@@ -369,6 +471,8 @@ def v_impact_scores(q, k, delta_v, causal=True, group=1):
     """deviation.py:96-115 (+GQA): colsum of causal softmax averaged over query
     heads, times the L1 norm of delta_v summed over (kv) heads."""
     q, k, dv = np.asarray(q, float), np.asarray(k, float), np.asarray(delta_v, float)
+    if causal and q.ndim == 3 and q.shape[0] * q.shape[1] * k.shape[1] > _BIG:
+        return _alpha_per_head(q, k, group) * np.abs(dv).sum(axis=-1).sum(axis=0)
     kk = expand_kv(k, group) if k.ndim == 3 else k
     attn = softmax_rows(q @ np.swapaxes(kk, -1, -2) / math.sqrt(q.shape[-1]), causal=causal)
     alpha = attn.sum(axis=-2)
@@ -379,8 +483,28 @@ def v_impact_scores(q, k, delta_v, causal=True, group=1):
     return alpha * l1
 
 
+def _alpha_per_head(q, k, group):
+    """deviation.py:108-110 (causal column sums of the softmax, mean over
+    query heads) one head at a time, for problems too large for (H, n, n)."""
+    H, n, d = q.shape
+    hidden = np.triu(np.ones((n, n), dtype=bool), k=1)
+    scale = 1.0 / math.sqrt(d)
+
+    def one(h):
+        logits = q[h] @ k[h // group].T * scale
+        logits[hidden] = -np.inf
+        logits -= logits.max(axis=-1, keepdims=True)
+        np.exp(logits, out=logits)
+        logits /= logits.sum(axis=-1, keepdims=True)
+        return logits.sum(axis=0)
+
+    return np.mean(_heads_parallel(one, H), axis=0)
+
+
 def dhd_alpha(q, k, causal=True, group=1):
     """The alpha half of v_impact_scores (deviation.py:108-110)."""
+    if causal and q.ndim == 3 and q.shape[0] * q.shape[1] * k.shape[1] > _BIG:
+        return _alpha_per_head(q, k, group)
     kk = expand_kv(k, group) if k.ndim == 3 else k
     attn = softmax_rows(q @ np.swapaxes(kk, -1, -2) / math.sqrt(q.shape[-1]), causal=causal)
     alpha = attn.sum(axis=-2)
@@ -539,6 +663,17 @@ def prefill_with_selection(tokens, W, cfg, reuse: Reuse, ratio, table=None):
     return states, selected, set(reused) - set(selected), info
 
 
+def _one_row_attention(q, keys, vals, group):
+    """engine.py:104-109: one query row per head over the whole given
+    context (no mask), GQA heads grouped instead of expanded: q (H, d),
+    keys/vals (kvh, n, d) -> (H, d)."""
+    kvh, n, d = keys.shape
+    qg = q.reshape(kvh, group, d)
+    logits = np.einsum("gjd,gnd->gjn", qg, keys) / math.sqrt(d)
+    wts = softmax_rows(logits)
+    return np.einsum("gjn,gnd->gjd", wts, vals).reshape(kvh * group, d)
+
+
 class Session:
     """engine.py:47-171 (ReuseSession) restated over numpy arrays: growing
     per-layer K/V cache (L, kvh, n, d), append / recompute_positions /
@@ -572,11 +707,8 @@ class Session:
             q, k_new, v_new = _qkv(h[None], w, cfg, self.table, np.array([p]))
             self.k[layer, :, p, :] = k_new[:, 0, :]
             self.v[layer, :, p, :] = v_new[:, 0, :]
-            keys = expand_kv(self.k[layer, :, :context, :], cfg.group)
-            vals = expand_kv(self.v[layer, :, :context, :], cfg.group)
-            logits = np.einsum("hd,hnd->hn", q[:, 0, :], keys) / math.sqrt(cfg.d_k)
-            wts = softmax_rows(logits)
-            out = np.einsum("hn,hnd->hd", wts, vals)
+            out = _one_row_attention(q[:, 0, :], self.k[layer, :, :context, :],
+                                     self.v[layer, :, :context, :], cfg.group)
             h = h + out.reshape(-1) @ w[3]
         return h
 
@@ -612,10 +744,8 @@ class Session:
         for layer in range(self.probe_layer):
             w = W["layers"][layer]
             q, k_new, v_new = _qkv(h[None], w, cfg, self.table, np.array([p]))
-            keys = expand_kv(np.concatenate([self.k[layer], k_new], axis=1), cfg.group)
-            vals = expand_kv(np.concatenate([self.v[layer], v_new], axis=1), cfg.group)
-            logits = np.einsum("hd,hnd->hn", q[:, 0, :], keys) / math.sqrt(cfg.d_k)
-            out = np.einsum("hn,hnd->hd", softmax_rows(logits), vals)
+            out = _one_row_attention(q[:, 0, :], np.concatenate([self.k[layer], k_new], axis=1),
+                                     np.concatenate([self.v[layer], v_new], axis=1), cfg.group)
             h = h + out.reshape(-1) @ w[3]
         q, _, _ = _qkv(h[None], W["layers"][self.probe_layer], cfg, self.table, np.array([p]))
         return q[:, 0, :]

@@ -156,6 +156,19 @@ class BatchState:
     tokens_host: list = field(default_factory=list)
     budgets_dev: torch.Tensor | None = None
 
+    def __del__(self):
+        # pages not released, written back or handed on (st.pages = []) return
+        # to the arena when the state goes away (reference sessions own numpy
+        # caches that the GC frees; ours live in the shared arena)
+        arena = getattr(self, "_arena", None)
+        if arena is not None and self.pages:
+            try:
+                for p in self.pages:
+                    arena.release(p)
+            except Exception:                       # interpreter shutdown
+                pass
+            self.pages = []
+
     @property
     def n_hit(self) -> np.ndarray:
         """Host copy of the hit counts (synchronises; not used on the hot path)."""
@@ -266,6 +279,7 @@ class Engine:
         st = BatchState(lens, off, req_off, tokens_dev, pages, block_table, bc, cap)
         st.ctx_len = lens.copy()
         st._keep = (req_off, block_table)
+        st._arena = self.arena
         return st
 
     def release(self, st: BatchState) -> None:

@@ -26,6 +26,7 @@ from .matching import HashParams, window_hashes_device
 from .model import HEAD_DIM, ModelConfig
 
 PAGE_SIZE = 64
+MAX_SEQ = 1 << 21          # R2 packs positions into 21-bit fields (csrc/retriever.cu)
 _MAGIC = b"KVSH"          # pool file format of reference pool.py:8-17
 _VERSION = 1
 
@@ -99,8 +100,24 @@ class KVEntry:
         return (4 + len(self.request_id.encode()) + 4 + 4 * self.n_tokens + 12
                 + 2 * 4 * cfg.num_layers * cfg.kv_heads * self.n_tokens * cfg.d_k)
 
+    @property
+    def live(self) -> bool:
+        """Still in its pool: its slot and pages have not been handed on."""
+        s = self.pool._slots
+        return 0 <= self.slot < len(s) and s[self.slot] is self
+
+    def check_live(self) -> None:
+        """Raise CacheError for an evicted or replaced entry, whose slot and
+        arena pages may already belong to another entry (a stale ReuseMap)."""
+        if not self.live:
+            raise CacheError(f"entry {self.request_id!r} is no longer in the pool "
+                             "(evicted or replaced)")
+
     def export_f32(self) -> tuple[torch.Tensor, torch.Tensor]:
         """Device fp32 K and V in KVSH order [L][n][kv_heads][d_k] (F3 kernel)."""
+        self.check_live()
+        if self.owner >= 0:
+            raise CacheError(f"entry {self.request_id!r} lives on GPU {self.owner}")
         cfg, dev = self.pool.config, self.pool.device
         shape = (cfg.num_layers, self.n_tokens, cfg.kv_heads, cfg.d_k)
         k = torch.empty(shape, dtype=torch.float32, device=dev)
@@ -206,6 +223,8 @@ class CachePool:
             raise CacheError("entry tokens must be a non-empty 1-D sequence")
         if tokens.min() < 0 or tokens.max() >= 2**32:
             raise CacheError("token ids must fit an unsigned 32-bit integer")
+        if tokens.size >= MAX_SEQ:
+            raise ParameterError(f"entries of {MAX_SEQ} tokens or more are not supported")
         return tokens
 
     # ------------------------------------------------------------------ insert
@@ -440,6 +459,8 @@ class CachePool:
         """Batched R2 lookup of a scheduled batch (flat device tokens)."""
         n_req = len(req_off_host) - 1
         n_total = int(req_off_host[-1])
+        if n_req and int(np.diff(req_off_host).max()) >= MAX_SEQ:
+            raise ParameterError(f"requests of {MAX_SEQ} tokens or more are not supported")
         dev = self.device
         src_slot = torch.empty(max(n_total, 1), dtype=torch.int32, device=dev)
         src_cand = torch.empty(max(n_total, 1), dtype=torch.int32, device=dev)

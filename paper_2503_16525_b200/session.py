@@ -13,8 +13,10 @@ Differences from the reference, by construction of the B200 path:
 * After a DHD prefill the session has computed only the rows
   S = non-reused U selected U {n-1} (SURVEY.md A12, exact on those rows);
   ``prefill_states.hidden`` holds NaN on the other rows.  K/V are complete.
-* ORACLE selection mode and the comparison strategies are SURVEY.md F4 and
-  raise ParameterError.
+* ``LayerStates`` fields are materialised as float64 numpy on first access
+  (device snapshots until then).
+* ORACLE selection mode and the comparison strategies run on
+  the device through ``select_baseline``.
 """
 from __future__ import annotations
 
@@ -25,30 +27,29 @@ import numpy as np
 import torch
 
 from .engine import BatchState, Engine, RowSet
-from .errors import InputError, ParameterError
+from .errors import CacheError, InputError, ParameterError
 from .model import HEAD_DIM, ToyModel
 from .pool import CachePool, KVArena, ReuseMap
 from .selection import SelectionConfig, SelectionMode, Strategy
 
-_ENGINES: dict = {}
-
-
 def get_engine(model: ToyModel, pool: CachePool | None = None, need_tokens: int = 0) -> Engine:
-    """One engine per (model, pool); a private growing pool when pool is None."""
+    """One engine per (model, pool), cached on the pool (or, for a private
+    growing pool when pool is None, on the model) - nothing global keeps a
+    model, pool or arena alive after the caller drops them."""
     if pool is not None:
-        key = (id(model), id(pool))
-        eng = _ENGINES.get(key)
-        if eng is None:
-            eng = _ENGINES[key] = Engine(model, pool)
+        engines = pool.__dict__.setdefault("_engines", {})
+        eng = engines.get(id(model))
+        if eng is None or eng.model is not model:
+            eng = engines[id(model)] = Engine(model, pool)
         return eng
-    key = (id(model), None)
-    eng = _ENGINES.get(key)
+    eng = getattr(model, "_private_engine", None)
     pages = KVArena(model.config, 0, model.device).pages_for(need_tokens) + 2
     if eng is None or eng.arena.free_pages < pages:
+        # sessions on the previous arena keep their own engine (and arena)
         total = max(pages * 2, 64, 0 if eng is None else eng.arena.num_pages * 2)
         arena = KVArena(model.config, total, model.device)
-        eng = _ENGINES[key] = Engine(model, CachePool(model.config, arena=arena,
-                                                      device=model.device))
+        eng = Engine(model, CachePool(model.config, arena=arena, device=model.device))
+        model._private_engine = eng
     return eng
 
 
@@ -67,27 +68,91 @@ def _device_hits(reuse: ReuseMap | None, n: int, device):
             if not 0 <= pos < n:
                 raise InputError(f"reuse position {pos} outside request of length {n}")
             if not 0 <= c < entry.n_tokens:
-                from .errors import CacheError
                 raise CacheError(f"cached position {c} outside entry")
+            entry.check_live()
             slot[pos] = entry.slot
             cand[pos] = c
     return torch.from_numpy(slot).to(device), torch.from_numpy(cand).to(device)
 
 
-@dataclass
 class LayerStates:
-    """Per-layer states (model.py:132-151) as numpy float64; attn is None."""
+    """Per-layer states (model.py:132-151); attn is None.
 
-    q: np.ndarray
-    k: np.ndarray
-    v: np.ndarray
-    attn: None
-    head_out: np.ndarray
-    hidden: np.ndarray
+    The fields are float64 numpy arrays of the reference's shapes - q and
+    head_out (L, H, n, d_k), k and v (L, kv_heads, n, d_k), hidden
+    (L+1, n, d_model) - built on first access from device snapshots taken
+    when the pass ran, so a Llama-shape prefill keeps ~1 GB of bf16/fp32 on
+    the GPU instead of ~15 GB of float64 on the host unless a caller reads
+    them.  Rows a partial prefill did not compute read as NaN."""
+
+    attn = None
+
+    def __init__(self, model: ToyModel, n: int, pos: torch.Tensor, capture, x0: torch.Tensor,
+                 kv: torch.Tensor):
+        self._model, self._n, self._pos = model, n, pos
+        self._capture, self._x0, self._kv = capture, x0, kv       # kv: [L, 2, n, G, 128] bf16
+        self._cache: dict = {}
 
     @property
     def n_tokens(self) -> int:
-        return self.hidden.shape[1]
+        return self._n
+
+    def _heads(self, which: int) -> np.ndarray:
+        cfg, m = self._model.config, self._model
+        out = np.full((cfg.num_layers, cfg.num_heads, self._n, cfg.d_k), np.nan)
+        pos = self._pos.cpu().numpy()
+        for item in self._capture:
+            if item[1] != "hidden":
+                out[item[0]][:, pos] = m.unpad_heads(item[which]).float().permute(1, 0, 2) \
+                    .cpu().numpy()
+        return out
+
+    @property
+    def q(self) -> np.ndarray:
+        if "q" not in self._cache:
+            self._cache["q"] = self._heads(1)
+        return self._cache["q"]
+
+    @property
+    def head_out(self) -> np.ndarray:
+        if "head_out" not in self._cache:
+            self._cache["head_out"] = self._heads(2)
+        return self._cache["head_out"]
+
+    @property
+    def hidden(self) -> np.ndarray:
+        if "hidden" not in self._cache:
+            cfg = self._model.config
+            hid = np.full((cfg.num_layers + 1, self._n, cfg.d_model), np.nan)
+            pos = self._pos.cpu().numpy()
+            hid[0][pos] = self._x0.double().cpu().numpy()
+            for item in self._capture:
+                if item[1] == "hidden":
+                    hid[item[0] + 1][pos] = item[2].double().cpu().numpy()
+            self._cache["hidden"] = hid
+        return self._cache["hidden"]
+
+    def _kv_host(self, which: int) -> np.ndarray:
+        x = self._model.unpad_heads(self._kv[:, which])                # L, n, G, d_k
+        return x.float().permute(0, 2, 1, 3).double().cpu().numpy()
+
+    @property
+    def k(self) -> np.ndarray:
+        if "k" not in self._cache:
+            self._cache["k"] = self._kv_host(0)
+        return self._cache["k"]
+
+    @property
+    def v(self) -> np.ndarray:
+        if "v" not in self._cache:
+            self._cache["v"] = self._kv_host(1)
+        return self._cache["v"]
+
+
+def _kv_device(eng: Engine, st: BatchState, r: int, n: int) -> torch.Tensor:
+    """Snapshot of request r's K/V rows [0, n): [L, 2, n, G, 128] bf16."""
+    return torch.stack([torch.stack([eng.arena.rows(st.pages[r], n, layer, kv) for kv in (0, 1)])
+                        for layer in range(eng.cfg.num_layers)])
 
 
 def _kv_numpy(eng: Engine, st: BatchState, r: int, n: int, kv: int) -> np.ndarray:
@@ -99,22 +164,8 @@ def _kv_numpy(eng: Engine, st: BatchState, r: int, n: int, kv: int) -> np.ndarra
 
 
 def _states_from_capture(eng: Engine, st: BatchState, rows: RowSet, capture, x0) -> LayerStates:
-    cfg, m = eng.cfg, eng.model
     n = int(st.lengths[0])
-    pos = rows.row_pos.cpu().numpy()
-    L, H = cfg.num_layers, cfg.num_heads
-    q = np.full((L, H, n, cfg.d_k), np.nan)
-    ho = np.full((L, H, n, cfg.d_k), np.nan)
-    hid = np.full((L + 1, n, cfg.d_model), np.nan)
-    hid[0][pos] = x0.double().cpu().numpy()
-    for item in capture:
-        layer = item[0]
-        if item[1] == "hidden":
-            hid[layer + 1][pos] = item[2].double().cpu().numpy()
-        else:
-            q[layer][:, pos] = m.unpad_heads(item[1]).float().permute(1, 0, 2).cpu().numpy()
-            ho[layer][:, pos] = m.unpad_heads(item[2]).float().permute(1, 0, 2).cpu().numpy()
-    return LayerStates(q, _kv_numpy(eng, st, 0, n, 0), _kv_numpy(eng, st, 0, n, 1), None, ho, hid)
+    return LayerStates(eng.model, n, rows.row_pos, capture, x0, _kv_device(eng, st, 0, n))
 
 
 def _normalize_recompute(recompute, L: int) -> list[set]:
@@ -273,7 +324,7 @@ class ReuseSession:
     def delta_v_probe(self) -> np.ndarray:
         """engine.py:140-148: cache V at the probe layer minus its exact value."""
         eng, st = self.engine, self.state
-        _, _, v_true = eng._probe(_prefill_view(st), write_k=False)
+        _, _, v_true = eng._probe(st, write_k=False)
         cache_v = eng.arena.rows(st.pages[0], self.n_tokens, self.probe_layer, 1)
         delta = torch.zeros_like(cache_v, dtype=torch.float32)
         n = self.n_prefill
@@ -287,11 +338,6 @@ class ReuseSession:
         self._grow(1)
         q = self.engine.probe_query(self.state, np.array([int(token_id)]))
         return self.model.unpad_heads(q[0]).double().cpu().numpy()
-
-
-def _prefill_view(st: BatchState) -> BatchState:
-    """The prefill rows of a (possibly decoded-into) single-request state."""
-    return st
 
 
 @dataclass
@@ -446,8 +492,12 @@ def _oracle_prefill(model, tokens, reuse, config, ref_states, decode_capacity):
 
 @dataclass
 class GenerationResult:
+    """engine.py:288-295; ``chosen`` (positions recomputed per step) is an
+    addition the reference records only through recompute_positions."""
+
     step_deviation: list
     recompute_counts: list
+    chosen: list = field(default_factory=list)
 
     @property
     def cumulative_deviation(self) -> float:
@@ -458,7 +508,7 @@ def run_generation(session: ReuseSession, ref_session: ReuseSession, decode_toke
                    n_extra: int) -> GenerationResult:
     """engine.py:298-328: per token, D3 selection + recompute + append on the
     session, append on the reference session, ||h - h_ref||."""
-    deviations, counts = [], []
+    deviations, counts, chosen_steps = [], [], []
     for tok in decode_tokens:
         tok = int(tok)
         session._grow(1)
@@ -471,4 +521,5 @@ def run_generation(session: ReuseSession, ref_session: ReuseSession, decode_toke
         ref = ref_session.append(tok)
         deviations.append(float(np.linalg.norm(h[0].double().cpu().numpy() - ref.hidden_out)))
         counts.append(len(chosen[0]))
-    return GenerationResult(deviations, counts)
+        chosen_steps.append(list(chosen[0]))
+    return GenerationResult(deviations, counts, chosen_steps)

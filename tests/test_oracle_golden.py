@@ -76,17 +76,60 @@ def test_probe_scores_selection_golden(name):
 
 @pytest.mark.parametrize("name", MODEL_CASES)
 def test_partial_rows_prefill_equals_reference(name):
-    """computing only rows S reproduces the
-    reference rows S - checked here through the oracle's full forward."""
+    """computing only the query rows
+    S = non-reused U selected U {n-1} (O.forward_rows, the restatement the
+    large parity tests use) reproduces the reference's own prefill states on
+    rows S, and its K/V caches are the reference's complete caches."""
     cfg, z = model_case(name)
     W = O.draw_weights(cfg)
     reuse = reuse_of(z)
     n = len(z["target"])
-    sel = set(z["selected"].tolist())
-    reused = set(reuse.reused)
-    S = sorted((set(range(n)) - reused) | sel | {n - 1})
-    np.testing.assert_allclose(z["prefill_hidden"][:, S], z["prefill_hidden"][:, S])
-    assert len(S) <= n
+    sel = z["selected"].tolist()
+    got = O.forward_rows(z["target"], W, cfg, reuse, sel)
+    S = got["rows"]
+    assert S.tolist() == sorted((set(range(n)) - set(reuse.reused)) | set(sel) | {n - 1})
+    assert len(S) < n
+    np.testing.assert_allclose(got["hidden"], z["prefill_hidden"][:, S], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(got["k"], z["prefill_k"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(got["v"], z["prefill_v"], rtol=0, atol=1e-12)
+    with pytest.raises(ValueError):              # a fresh row outside the computed set
+        O.forward_rows(z["target"], W, cfg, reuse, sel, rows=S[1:] if S[0] not in
+                       set(reuse.reused) else S[:-1])
+
+
+@pytest.mark.parametrize("kvh,rope", [(None, None), (2, 10000.0)])
+def test_per_head_restatement_equals_batched(kvh, rope, monkeypatch):
+    """The one-head-at-a-time attention / alpha used above O._BIG equals the
+    batched (H, n, n) restatement, and forward_rows equals forward on rows S
+    with GQA and RoPE."""
+    cfg = O.OracleConfig(3, 4, 64, 300, 3, kvh, rope)
+    W = O.draw_weights(cfg)
+    table = O.rope_table(512, cfg.d_k, rope) if rope else None
+    rng = np.random.default_rng(0)
+    q = rng.normal(size=(4, 97, 16))
+    k = rng.normal(size=(cfg.kvh, 97, 16))
+    v = rng.normal(size=(cfg.kvh, 97, 16))
+    want, _ = O.attention(q, k, v, causal=True, group=cfg.group)
+    want_a = O.dhd_alpha(q, k, group=cfg.group)
+    monkeypatch.setattr(O, "_BIG", 0)
+    got, attn = O.attention(q, k, v, causal=True, group=cfg.group)
+    assert attn is None
+    np.testing.assert_allclose(got, want, rtol=0, atol=1e-13)
+    np.testing.assert_allclose(O.dhd_alpha(q, k, group=cfg.group), want_a, rtol=0, atol=1e-13)
+    toks = rng.integers(0, 300, 60)
+    src = toks[10:40]
+    st = O.forward(src, W, cfg, table=table)
+    se = np.full(60, -1, np.int32)
+    sc = np.full(60, -1, np.int32)
+    se[10:40], sc[10:40] = 0, np.arange(30)
+    reuse = O.Reuse(se, sc, [st["k"]], [st["v"]])
+    sel = [12, 30, 39]
+    full = O.forward(toks, W, cfg, reuse, {l: set(sel) for l in range(3)}, table)
+    part = O.forward_rows(toks, W, cfg, reuse, sel, table=table)
+    S = part["rows"]
+    np.testing.assert_allclose(part["hidden"], full["hidden"][:, S], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(part["k"], full["k"], rtol=0, atol=1e-12)
+    np.testing.assert_allclose(part["v"], full["v"], rtol=0, atol=1e-12)
 
 
 @pytest.mark.parametrize("name", MODEL_CASES)
