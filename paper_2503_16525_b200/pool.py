@@ -284,8 +284,8 @@ class CachePool:
         entry with the same id."""
         cfg = self.config
         tokens = self._validate_tokens(tokens)
-        k = torch.as_tensor(np.asarray(k, float) if not torch.is_tensor(k) else k)
-        v = torch.as_tensor(np.asarray(v, float) if not torch.is_tensor(v) else v)
+        k = k if torch.is_tensor(k) else torch.from_numpy(np.ascontiguousarray(k, dtype=float))
+        v = v if torch.is_tensor(v) else torch.from_numpy(np.ascontiguousarray(v, dtype=float))
         expected = (cfg.num_layers, cfg.kv_heads, tokens.size, cfg.d_k)
         if tuple(k.shape) != expected or tuple(v.shape) != expected:
             raise CacheError(f"K/V shape {tuple(k.shape)} does not match pool config {expected}")
