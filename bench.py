@@ -470,6 +470,58 @@ def select_batch_leg(n_req: int, seq: int = 4096, hit: float = 0.5, ratio: float
             "ms": ms, "achieved": nbytes / (ms / 1000.0) / 1e9, "unit": "GB/s"}
 
 
+def decode_select_batch_leg(n_req: int, ctx: int = 4096, hit: float = 0.5, ratio: float = 0.2,
+                            n_extra: int = 3, iters: int = 10):
+    """D3 (kvs_dhd_decode_select, one fused launch) on a decode batch of
+    n_req Llama-shape requests (32 query / 8 kv heads, head dim 128) with
+    ctx-token contexts, ~hit*(1-ratio) of each request's prefill rows still
+    eligible (reused, not recomputed), L2 flushed before every launch, CUDA
+    events around each launch.  Algorithmic bytes per request-step (SURVEY
+    8d): ctx*kv_heads*d*2 (K at the probe layer) + 4*n_prefill (dv-L1) +
+    n_prefill/8 (eligibility) + 12 (chosen)."""
+    import torch
+    import paper_2503_16525_b200 as K
+    from paper_2503_16525_b200.engine import Engine
+    from paper_2503_16525_b200.pool import CachePool, KVArena
+    dev = torch.device("cuda", torch.cuda.current_device())
+    shape = dict(K.LLAMA31_8B)
+    shape.update(num_layers=2, vocab_size=1000)
+    cfg = K.ModelConfig(**shape, max_positions=ctx + 64)
+    n_pre = ctx - 8                                        # a few decode rows past the prefill
+    arena = KVArena(cfg, n_req * ((ctx + 63) // 64) + 4)
+    eng = Engine(K.ToyModel(cfg, init="device"), CachePool(cfg, arena=arena))
+    st = eng.new_batch([np.zeros(n_pre, dtype=np.int64)] * n_req, decode_capacity=8)
+    arena.data.normal_()
+    st.ctx_len = np.full(n_req, ctx, dtype=np.int64)
+    rng = np.random.default_rng(0)
+    elig = (rng.random(n_req * n_pre) < hit * (1 - ratio)).astype(np.uint8)
+    st.dv_l1 = torch.rand(n_req * n_pre, device=dev)
+    q = (torch.randn(n_req, cfg.num_heads, 128, device=dev) * 0.3).to(torch.bfloat16)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    eng.timers = {}
+    ts = []
+    for it in range(iters + 2):
+        st.eligible = torch.from_numpy(elig).to(dev)       # same eligible set every launch
+        flush.zero_()
+        eng.timers = {}
+        eng.reset_timer_events()
+        # the GPU stays busy while the host enqueues the launch (as inside a
+        # decode step), so the events time the kernel, not the Python call
+        torch.cuda._sleep(100_000)
+        eng.decode_select(st, q, n_extra)
+        torch.cuda.synchronize()
+        if it >= 2:
+            s, e = eng.timers["dhd_decode"][0]
+            ts.append(s.elapsed_time(e))
+    eng.timers = None
+    ms = float(np.median(ts))
+    nbytes = float(n_req * (ctx * cfg.kv_heads * 128 * 2 + 4 * n_pre + n_pre / 8 + 12))
+    del arena, eng, st, flush
+    torch.cuda.empty_cache()
+    return {"requests": n_req, "ctx": ctx, "algorithmic_bytes": nbytes, "ms": ms,
+            "achieved": nbytes / (ms / 1000.0) / 1e9, "unit": "GB/s"}
+
+
 def ncu_traffic(kernel: str):
     """DRAM bytes per launch of `kernel` from the committed ncu capture
     (profiles/r1_ncu_traffic.json), or None."""

@@ -21,7 +21,8 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
          "--expt-relaxed-constexpr", "-diag-suppress", "177",
          "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["capi.cu", "retriever.cu", "gather.cu", "dhd.cu", "attention_sm100.cu", "baselines.cu"]
+SOURCES = ["capi.cu", "retriever.cu", "gather.cu", "dhd.cu", "attention_sm100.cu", "baselines.cu",
+           "decode_dhd.cu"]
 
 
 def _headers_mtime() -> float:

@@ -1030,15 +1030,6 @@ __global__ void alpha_reduce_kernel(const float *__restrict__ part, int64_t n, i
 
 }  // namespace attn
 
-static bool make_kv_map(CUtensorMap *m, const kvs_kv_arena *a) {
-    const uint64_t G = a->kv_heads, D = a->head_dim, P = a->page_size;
-    uint64_t dims[4] = {D, G, P, (uint64_t)a->num_pages * a->num_layers * 2};
-    uint64_t strides[3] = {D * 2, G * D * 2, P * G * D * 2};
-    uint32_t box[4] = {64, 1, (uint32_t)P, 1};
-    return encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, a->base, dims, strides, box,
-                       CU_TENSOR_MAP_SWIZZLE_128B);
-}
-
 static bool make_q_map(CUtensorMap *m, const void *q, int64_t n_rows, int H, int D) {
     uint64_t dims[3] = {(uint64_t)D, (uint64_t)H, (uint64_t)n_rows};
     uint64_t strides[2] = {(uint64_t)D * 2, (uint64_t)H * D * 2};

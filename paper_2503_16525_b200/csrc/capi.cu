@@ -53,6 +53,15 @@ bool encode_tmap(CUtensorMap *map, CUtensorMapDataType dtype, int rank, void *ga
     return true;
 }
 
+bool make_kv_map(CUtensorMap *m, const kvs_kv_arena *a) {
+    const uint64_t G = a->kv_heads, D = a->head_dim, P = a->page_size;
+    uint64_t dims[4] = {D, G, P, (uint64_t)a->num_pages * a->num_layers * 2};
+    uint64_t strides[3] = {D * 2, G * D * 2, P * G * D * 2};
+    uint32_t box[4] = {64, 1, (uint32_t)P, 1};
+    return encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, a->base, dims, strides, box,
+                       CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
 }  // namespace kvs
 
 extern "C" {

@@ -237,4 +237,19 @@ bool encode_tmap(CUtensorMap *map, CUtensorMapDataType dtype, int rank, void *ga
                  const uint64_t *dims, const uint64_t *strides_bytes /* rank-1 */,
                  const uint32_t *box, CUtensorMapSwizzle swz);
 
+// The arena as a 4-D TMA tensor (dims: head_dim, kv head, page row, page x
+// layer x K/V), box = 64 dims x 1 head x one page of rows, SWIZZLE_128B:
+// one load brings half of a kv head's 128 dims for a page's 64 rows.
+bool make_kv_map(CUtensorMap *m, const kvs_kv_arena *a);
+
+// D3 fused decode-stage DHD (decode_dhd.cu), dispatched by kvs_dhd_decode_select.
+size_t d3_fused_workspace(int32_t n_req, int32_t num_heads, int32_t max_ctx);
+bool d3_fused_supported(const kvs_kv_arena *arena, int32_t n_req, int32_t num_heads,
+                        int32_t n_extra);
+kvs_status d3_fused_launch(const void *q_t, int32_t num_heads, const int32_t *ctx_len,
+                           int32_t max_ctx, const float *dv_l1, uint8_t *eligible, int32_t layer,
+                           const kvs_kv_arena *arena, const kvs_batch *batch, int32_t n_extra,
+                           float softmax_scale, int32_t *chosen, int32_t *n_chosen, float *scores,
+                           void *ws, cudaStream_t s);
+
 }  // namespace kvs

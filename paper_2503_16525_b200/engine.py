@@ -668,12 +668,12 @@ class Engine:
     def decode_select(self, st: BatchState, q_t: torch.Tensor, n_extra: int):
         """D3 (selection.py:80-105) for every request; updates eligibility."""
         cfg, dev, R = self.cfg, self.device, len(st.lengths)
-        ctx = torch.from_numpy(st.ctx_len.astype(np.int32)).to(dev)
+        ctx = h2d(st.ctx_len.astype(np.int32), dev)
         max_ctx = int(st.ctx_len.max())
         chosen = torch.empty(R, max(n_extra, 1), dtype=torch.int32, device=dev)
         nch = torch.zeros(R, dtype=torch.int32, device=dev)
         ws = self._ws["dsel"].get(N.ws_bytes("kvs_dhd_decode_select_workspace", R, cfg.num_heads,
-                                             max_ctx), dev)
+                                             max_ctx), dev, zero=True)
         self._timed("dhd_decode", N.call, "kvs_dhd_decode_select", q_t.data_ptr(), cfg.num_heads,
                     ctx.data_ptr(), max_ctx, st.dv_l1.data_ptr(), st.eligible.data_ptr(),
                     self.probe_layer, self.arena.c, st.batch_c, n_extra, self.scale,

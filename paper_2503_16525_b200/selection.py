@@ -124,7 +124,7 @@ def select_decode_step(q_t, k, delta_v, eligible, n_extra: int) -> SelectionResu
     chosen = torch.empty(1, n_extra, dtype=torch.int32, device=dev)
     nch = torch.zeros(1, dtype=torch.int32, device=dev)
     scores = torch.zeros(1, n, dtype=torch.float32, device=dev)
-    ws = _dws.get(N.ws_bytes("kvs_dhd_decode_select_workspace", 1, H, n), dev)
+    ws = _dws.get(N.ws_bytes("kvs_dhd_decode_select_workspace", 1, H, n), dev, zero=True)
     N.call("kvs_dhd_decode_select", qd.data_ptr(), H, ctx.data_ptr(), n, dv.data_ptr(),
            elig_t.data_ptr(), 0, sc.arena, sc.batch, n_extra, 1.0 / math.sqrt(d),
            chosen.data_ptr(), nch.data_ptr(), scores.data_ptr(), ws.data_ptr(), ws.numel(),
