@@ -374,8 +374,9 @@ def decode_leg(args, eng, batch, cfg, n_tokens: int = 8):
     import torch
     rng = np.random.default_rng(5)
     st = eng.prefill_batch(batch, ratio=args.ratio, decode_capacity=n_tokens + 1)
-    toks = rng.integers(0, cfg.vocab_size, (n_tokens, len(batch)))
-    eng.decode_step(st, toks[0], 3)                             # warm-up step
+    toks = torch.from_numpy(rng.integers(0, cfg.vocab_size, (n_tokens, len(batch)))).to(
+        torch.int64).cuda()
+    eng.decode_step_device(st, toks[0], 3)                      # warm-up step
     torch.cuda.synchronize()
     timers = {}
     eng.reset_timer_events(reserve=8 * n_tokens)
@@ -383,8 +384,8 @@ def decode_leg(args, eng, batch, cfg, n_tokens: int = 8):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ctx0 = st.ctx_len.copy()
     e0.record()
-    for t in range(1, n_tokens):
-        eng.decode_step(st, toks[t], 3)
+    for t in range(1, n_tokens):                                # no host round trip per token
+        eng.decode_step_device(st, toks[t], 3)
     e1.record()
     torch.cuda.synchronize()
     eng.timers = None
@@ -648,6 +649,15 @@ def main():
         dec = res["decode"]
         dec["dhd_decode_select"]["peak"] = hbm
         dec["dhd_decode_select"]["frac"] = dec["dhd_decode_select"]["achieved"] / hbm
+        if world == 1 and not args.profile:
+            # D3 on decode batches of the serving configs (measure
+            # batched; the step's own 8 requests are latency-bound)
+            dec["dhd_decode_select_batched"] = []
+            for nr in (64, 128):
+                b = decode_select_batch_leg(nr)
+                b["peak"] = hbm
+                b["frac"] = b["achieved"] / hbm
+                dec["dhd_decode_select_batched"].append(b)
         extra["decode"] = dec
     if "e2e_ms" in res:
         line["e2e"] = {"value": res["tokens"] / (res["e2e_ms"] / 1000.0), "unit": "tok/s",

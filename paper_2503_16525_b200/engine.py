@@ -628,47 +628,44 @@ class Engine:
         zeros = torch.zeros(n, dtype=torch.float32, device=self.device)
         st.dv_l1, _, _ = self._select(st, v_true, zeros, np.zeros(len(st.lengths), np.int32))
 
-    def _decode_rows(self, st: BatchState, chosen: list[list[int]], new_tokens) -> RowSet:
-        req, pos, tok_idx = [], [], []
-        off = [0]
-        for r, ch in enumerate(chosen):
-            for c in ch:
-                req.append(r)
-                pos.append(c)
-            req.append(r)
-            pos.append(int(st.ctx_len[r]))
-            off.append(len(req))
-        dev = self.device
-        rs = RowSet(len(req), torch.arange(len(req), dtype=torch.int32, device=dev),
-                    torch.tensor(req, dtype=torch.int32, device=dev),
-                    torch.tensor(pos, dtype=torch.int32, device=dev), None,
-                    np.array(off, dtype=np.int64))
-        return rs
-
-    def probe_query(self, st: BatchState, new_tokens: np.ndarray) -> torch.Tensor:
+    def probe_query(self, st: BatchState, new_tokens) -> torch.Tensor:
         """query_rows_probe (engine.py:150-171) for every request's next token:
-        layers below the probe over cache + own row, then the probe-layer q."""
+        layers below the probe over cache + own row, then the probe-layer q.
+        new_tokens: host array or device int64 tensor [R]."""
         cfg, dev = self.cfg, self.device
         R = len(st.lengths)
+        pos = self._ctx_dev(st)
         rows = RowSet(R, torch.arange(R, dtype=torch.int32, device=dev),
-                      torch.arange(R, dtype=torch.int32, device=dev),
-                      torch.from_numpy(st.ctx_len.astype(np.int32)).to(dev), None,
+                      torch.arange(R, dtype=torch.int32, device=dev), pos, None,
                       np.arange(R + 1, dtype=np.int64))
-        tok = torch.from_numpy(np.asarray(new_tokens, dtype=np.int64)).to(dev)
+        tok = new_tokens if torch.is_tensor(new_tokens) else \
+            h2d(np.asarray(new_tokens, dtype=np.int64), dev)
         x = self._embed(tok, rows)
         max_kv = int(st.capacity.max())
         x = self.forward_rows(x, rows, range(self.probe_layer), self.arena.c, st.batch_c,
                               decode=True, max_kv=max_kv)
-        qkv = x.to(torch.bfloat16) @ self.model.w_qkv[self.probe_layer]
+        qkv = self._qkv(x, self.probe_layer)
         q = torch.empty(R, cfg.num_heads, HEAD_DIM, dtype=torch.bfloat16, device=dev)
         zero = torch.zeros(R, dtype=torch.uint8, device=dev)
         self._scatter(qkv, rows, self.probe_layer, self.arena.c, st.batch_c, q, write_kv=zero)
         return q
 
-    def decode_select(self, st: BatchState, q_t: torch.Tensor, n_extra: int):
-        """D3 (selection.py:80-105) for every request; updates eligibility."""
+    def _ctx_dev(self, st: BatchState) -> torch.Tensor:
+        """Device copy of the current context lengths (int32), refreshed when
+        the host value changes (pinned H2D, no sync)."""
+        key = getattr(st, "_ctx_key", None)
+        cur = st.ctx_len.tobytes()
+        if key != cur:
+            st._ctx_dev = h2d(st.ctx_len.astype(np.int32), self.device)
+            st._ctx_key = cur
+        return st._ctx_dev
+
+    def decode_select_device(self, st: BatchState, q_t: torch.Tensor, n_extra: int):
+        """D3 (selection.py:80-105) for every request, on the device: returns
+        (chosen [R, n_extra] int32 ascending, -1 padded; n_chosen [R]) and
+        clears the chosen rows from st.eligible.  No host synchronisation."""
         cfg, dev, R = self.cfg, self.device, len(st.lengths)
-        ctx = h2d(st.ctx_len.astype(np.int32), dev)
+        ctx = self._ctx_dev(st)
         max_ctx = int(st.ctx_len.max())
         chosen = torch.empty(R, max(n_extra, 1), dtype=torch.int32, device=dev)
         nch = torch.zeros(R, dtype=torch.int32, device=dev)
@@ -679,40 +676,60 @@ class Engine:
                     self.probe_layer, self.arena.c, st.batch_c, n_extra, self.scale,
                     chosen.data_ptr(), nch.data_ptr(), None, ws.data_ptr(), ws.numel(),
                     N.stream_ptr())
-        ch, nc = chosen.cpu().numpy(), nch.cpu().numpy()
-        return [[int(x) for x in ch[r, :nc[r]]] for r in range(R)]
+        return chosen, nch
 
-    def decode_step(self, st: BatchState, new_tokens, n_extra: int):
-        """One decode token per request (engine.py:312-327): probe query, D3
-        selection, then chosen rows + new token as one layer-batched pass."""
-        R = len(st.lengths)
-        new_tokens = np.asarray(new_tokens, dtype=np.int64).reshape(R)
+    def decode_select(self, st: BatchState, q_t: torch.Tensor, n_extra: int):
+        """decode_select_device with the choices as host lists (synchronises)."""
+        chosen, nch = self.decode_select_device(st, q_t, n_extra)
+        ch, nc = chosen.cpu().numpy(), nch.cpu().numpy()
+        return [[int(x) for x in ch[r, :nc[r]]] for r in range(len(st.lengths))]
+
+    def decode_step_device(self, st: BatchState, new_tokens: torch.Tensor, n_extra: int):
+        """One decode token per request (engine.py:312-327) with no host
+        round trip: probe query, D3, then the chosen rows and the new token as
+        one layer-batched pass.  The pass has a fixed
+        n_extra + 1 row slots per request; slots D3 left empty (-1) keep their
+        K/V untouched and their outputs are discarded.  new_tokens: device
+        int64 [R].  Returns (hidden of the new rows [R, d_model] fp32,
+        chosen [R, n_extra] int32 -1 padded, n_chosen [R] int32)."""
+        R, dev = len(st.lengths), self.device
         if (st.ctx_len + 1 > st.capacity).any():
             raise InputError("decode capacity exhausted")
-        chosen = [[] for _ in range(R)]
-        if n_extra > 0 and st.eligible is not None and bool(st.eligible.any()):
+        E = max(int(n_extra), 0)
+        ctx = self._ctx_dev(st)
+        if E > 0 and st.eligible is not None:
             self.ensure_dv(st)
             q_t = self.probe_query(st, new_tokens)
-            chosen = self.decode_select(st, q_t, n_extra)
-        rows = self._decode_rows(st, chosen, new_tokens)
-        dev = self.device
-        if not st.tokens_host:
-            flat = st.tokens.cpu().numpy()
-            st.tokens_host = [list(flat[st.req_off_host[r]:st.req_off_host[r + 1]])
-                              for r in range(R)]
-        tok_rows = []
-        for r, ch in enumerate(chosen):
-            tok_rows += [int(st.tokens_host[r][c]) for c in ch]
-            tok_rows.append(int(new_tokens[r]))
-        tok = torch.tensor(tok_rows, dtype=torch.int64, device=dev)
+            chosen, nch = self.decode_select_device(st, q_t, E)
+        else:
+            chosen = torch.full((R, max(E, 1)), -1, dtype=torch.int32, device=dev)[:, :E]
+            nch = torch.zeros(R, dtype=torch.int32, device=dev)
+        pos = torch.cat([chosen, ctx[:, None]], dim=1)                    # [R, E + 1]
+        valid = pos >= 0
+        pos_c = pos.clamp(min=0)
+        prev = st.req_off[:-1, None] + pos_c[:, :E].to(torch.int64)       # prefill rows only
+        tok = torch.cat([st.tokens[prev.clamp(max=st.tokens.numel() - 1)],
+                         new_tokens.view(R, 1).to(torch.int64)], dim=1).reshape(-1)
+        n = R * (E + 1)
+        rows = RowSet(n, torch.arange(n, dtype=torch.int32, device=dev),
+                      torch.arange(R, dtype=torch.int32, device=dev).repeat_interleave(E + 1),
+                      pos_c.reshape(-1).to(torch.int32), valid.reshape(-1).to(torch.uint8),
+                      np.arange(0, n + 1, E + 1, dtype=np.int64))
         x = self._embed(tok, rows)
         x = self.forward_rows(x, rows, range(self.cfg.num_layers), self.arena.c, st.batch_c,
                               decode=True, max_kv=int(st.capacity.max()))
-        last = torch.from_numpy(rows.row_off[1:] - 1).to(dev)
-        for r in range(R):
-            st.tokens_host[r].append(int(new_tokens[r]))
         st.ctx_len = st.ctx_len + 1
-        return x[last], chosen
+        st._decoded = getattr(st, "_decoded", []) + [new_tokens]
+        return x.view(R, E + 1, -1)[:, E], chosen, nch
+
+    def decode_step(self, st: BatchState, new_tokens, n_extra: int):
+        """decode_step_device for host tokens, choices returned as host lists
+        (one synchronisation, for the reference-shaped API)."""
+        R = len(st.lengths)
+        tok = h2d(np.asarray(new_tokens, dtype=np.int64).reshape(R), self.device)
+        h, chosen, nch = self.decode_step_device(st, tok, n_extra)
+        ch, nc = chosen.cpu().numpy(), nch.cpu().numpy()
+        return h, [[int(x) for x in ch[r, :nc[r]]] for r in range(R)]
 
     # ------------------------------------------------------------------ write-back
     def write_back(self, st: BatchState, request_ids) -> None:
