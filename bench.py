@@ -185,7 +185,8 @@ def build_engine(args, device, rank=0, world=1):
     cfg = K.ModelConfig(**shape, seed=0, max_positions=max(8192, args.seq + 64))
     model = K.ToyModel(cfg, device=device, init="device")
     src_pages = args.sources * ((args.seq + 63) // 64)
-    step_pages = 2 * args.batch * ((args.seq + 63) // 64)
+    # a rank's share of a partitioned batch can exceed B by the balance slack
+    step_pages = (2 if world == 1 else 3) * args.batch * ((args.seq + 63) // 64)
     arena = KVArena(cfg, src_pages + step_pages + 64 + getattr(args, "extra_pages", 0), device)
     pool = CachePool(cfg, K.HashParams(window_size=8), arena=arena, device=device)
     eng = Engine(model, pool)
@@ -210,6 +211,39 @@ def build_engine(args, device, rank=0, world=1):
         eng.fetcher = RemoteFetcher(eng)
     torch.cuda.synchronize()
     return cfg, model, pool, eng, sources
+
+
+def scheduled_share(eng, reqs, rank: int, world: int):
+    """The cache-aware hand-off of one scheduled batch on an N-GPU box: the
+    admission-time lookup of every request (simulate.py:177-189; the token
+    index is replicated, so every rank computes the same hit maps), the
+    reference scheduler's batch 0 (scheduling.py:106-125), and
+    partition_batch over the ranks by owner-of-hit-bytes, cost-balanced.
+    Deterministic and identical on every rank; returns this rank's requests
+    (token arrays).  Runs once per scheduled batch, before the timed loop."""
+    import torch
+    from paper_2503_16525_b200.scheduling import Request, partition_batch, schedule
+    if world == 1:
+        return reqs
+    st = eng.new_batch(reqs)
+    eng.lookup(st)
+    idx = eng.pool._build_index()
+    R = len(reqs)
+    lens = torch.as_tensor(st.lengths, device=st.src_slot.device)
+    req = torch.repeat_interleave(torch.arange(R, device=lens.device), lens)
+    hit = st.src_slot >= 0
+    own = idx["slot_owner_dev"][st.src_slot.clamp(min=0).long()].long()
+    own = torch.where(own < 0, torch.full_like(own, rank), own)     # replicated: any rank
+    key = torch.where(hit, req * world + own, torch.full_like(req, R * world))
+    owner_hits = torch.bincount(key, minlength=R * world + 1)[:R * world].view(R, world)
+    owner_hits = owner_hits.cpu().numpy()
+    eng.release(st)
+    queue = [Request(f"q{i}", 0.0, reqs[i], 0, float(owner_hits[i].sum()) / len(reqs[i]))
+             for i in range(R)]
+    batch = schedule(queue, len(queue))[0]
+    order = [int(r.id[1:]) for r in batch.requests]
+    parts = partition_batch(batch, world, [owner_hits[i] for i in order])
+    return [reqs[order[i]] for i in parts[rank]]
 
 
 def algorithmic_counts(eng, st, cfg):
@@ -241,8 +275,12 @@ def run_gpu(args, rank, world, device):
     torch.cuda.set_device(device)
     cfg, model, pool, eng, sources = build_engine(args, device, rank, world)
     n_steps = args.warmup + args.steps
-    batches = request_batches(sources, n_steps, args.batch, args.seq, args.hit, cfg.vocab_size,
-                              seed=1 + rank)
+    # one global request stream: every step the scheduler hands batch 0 of
+    # schedule(queue, N*B) (simulate.py:193-196) to the box, and
+    # partition_batch spreads it over the N GPUs
+    stream = request_batches(sources, n_steps, args.batch * world, args.seq, args.hit,
+                             cfg.vocab_size, seed=1)
+    batches = [scheduled_share(eng, reqs, rank, world) for reqs in stream]
     dev_tokens = [torch.from_numpy(np.concatenate(b)).to(device) for b in batches]
     torch.cuda.synchronize()
 
@@ -309,7 +347,7 @@ def run_gpu(args, rank, world, device):
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     elapsed = float(t.item())
-    tokens = args.steps * args.batch * args.seq * world
+    tokens = sum(sum(len(x) for x in reqs) for reqs in stream[args.warmup:])
     kern = {}
     for name, evs in timers.items():
         kern[name] = sum(a.elapsed_time(b) for a, b in evs) / args.steps     # ms per step
@@ -544,9 +582,27 @@ def peaks():
         return 6650.0, 1590.0, 1400.0, "fallback"
 
 
+def spawn_ranks(args) -> int:
+    """bench.py --gpus N without a launcher: run N ranks under
+    torch.distributed.run (one process per GPU, 127.0.0.1 rendezvous); rank 0
+    prints the line."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
     world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     workload = WORKLOAD if (args.shape, args.seq, args.hit) == ("llama", 4096, 0.5) else (
@@ -558,6 +614,8 @@ def main():
                "model_shape": {"llama": "llama3.1-8b", "qwen": "qwen2.5-7b",
                                "yi": "yi1.5-9b"}[args.shape] + " attention stack (no FFN)",
                "parallelism": f"dp{args.gpus} (requests partitioned, per-GPU pool)",
+               "hand_off": "schedule(queue, N*B)[0] -> partition_batch (owner-of-hit-bytes, "
+                           "cost-balanced); admission lookup before the timed loop",
                "l2": "inputs larger than L2 (2.7 GB weights + 4 GiB KV streamed per step)"}
     if args.impl == "reference":
         if rank != 0:
@@ -583,6 +641,10 @@ def main():
     ngpu = torch.cuda.device_count()
     if world > 1:
         import torch.distributed as dist
+        if args.dist_backend == "nccl" and world > ngpu:
+            # NCCL cannot put two ranks on one GPU: a functional run of N ranks
+            # on fewer GPUs stages the exchange through host memory (gloo)
+            args.dist_backend = "gloo"
         if args.dist_backend == "nccl":
             dist.init_process_group("nccl", device_id=torch.device("cuda", local % ngpu))
         else:
@@ -641,6 +703,9 @@ def main():
         "roofline": roof, "kernels": extra, "gpu_launches": res["launches"] * args.steps,
         "clocks": res["clocks"],
     }
+    if world > 1:
+        line["dist_backend"] = args.dist_backend
+        line["gpus_active"] = min(world, ngpu)
     if "full_recompute_ms" in res:
         extra["full_recompute"] = {"ms_per_step": res["full_recompute_ms"],
                                    "tok_s": args.batch * args.seq * world / (res["full_recompute_ms"] / 1000.0),

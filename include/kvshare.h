@@ -157,14 +157,18 @@ kvs_status kvs_gather_kv(const kvs_kv_arena *arena, const kvs_batch *batch,
 /* X1 remote-shard fetch (multi-GPU).  The owner packs the rows
  * (slot, cand) a peer hit - all layers, K and V - into a dense buffer
  * [n_rows][L][2][kv_heads*head_dim] bf16 that travels over NCCL send/recv;
- * the requester unpacks them into its pages at flat positions flat_t,
- * re-aligning K by (pos - cand) like kvs_gather_kv.                       */
+ * the requester unpacks layers [layer_begin, layer_end) of them into its
+ * pages at flat positions flat_t, re-aligning K by (pos - cand) like
+ * kvs_gather_kv; rows whose skip[flat_t] (nullable, u8) is set are left
+ * alone (the fast prefill path restores cached layer-0 rows only for the
+ * reused positions DHD did not select).                                   */
 kvs_status kvs_pack_rows(const kvs_kv_arena *arena, const int32_t *slot, const int32_t *cand,
                          int64_t n_rows, const int32_t *slot_pages, int32_t slot_max_pages,
                          void *out, kvs_stream_t stream);
 kvs_status kvs_unpack_rows(const kvs_kv_arena *arena, const kvs_batch *batch,
                            const int64_t *flat_t, const int32_t *cand, int64_t n_rows,
-                           const void *in, const kvs_rope *rope, kvs_stream_t stream);
+                           const void *in, const kvs_rope *rope, int32_t layer_begin,
+                           int32_t layer_end, const uint8_t *skip, kvs_stream_t stream);
 
 /* F4 comparison strategies (selection.py:133-186).
  * kvs_topk_select: per request r (positions [req_off[r], req_off[r+1]),

@@ -15,7 +15,7 @@ from .matching import (HashParams, MatchResult, build_hash_index, fixed_chunk_ma
                        match_sequences, rolling_hash, window_hashes)
 from .model import LLAMA31_8B, QWEN25_7B, YI15_9B, ModelConfig, ToyModel, init_model
 from .scheduling import (Batch, LatencyModel, Request, batch_latency, fcfs_schedule,
-                         optimal_batches_bruteforce, partition_batch, schedule, total_latency)
+                         partition_batch, schedule)
 
 __version__ = "0.1.0"
 
@@ -46,5 +46,4 @@ __all__ = sorted(set(_LAZY) | {
     "InputError", "KVLabError", "LatencyModel", "MatchResult", "ModelConfig", "NumericError",
     "ParameterError", "Request", "ShapeError", "ToyModel", "batch_latency", "build_hash_index",
     "fcfs_schedule", "fixed_chunk_match", "hit_rate", "init_model", "match_sequences",
-    "optimal_batches_bruteforce", "partition_batch", "rolling_hash", "schedule",
-    "total_latency", "window_hashes", "LLAMA31_8B", "QWEN25_7B", "YI15_9B"})
+    "partition_batch", "rolling_hash", "schedule", "window_hashes", "LLAMA31_8B", "QWEN25_7B", "YI15_9B"})

@@ -62,7 +62,8 @@ _SIGS = {
     "kvs_entry_export": [P(KVArena), c_vp, c_i64, c_i32, c_vp, c_vp, c_vp],
     "kvs_embed_rows": [c_vp, c_i64, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp],
     "kvs_pack_rows": [P(KVArena), c_vp, c_vp, c_i64, c_vp, c_i32, c_vp, c_vp],
-    "kvs_unpack_rows": [P(KVArena), P(Batch), c_vp, c_vp, c_i64, c_vp, P(Rope), c_vp],
+    "kvs_unpack_rows": [P(KVArena), P(Batch), c_vp, c_vp, c_i64, c_vp, P(Rope), c_i32, c_i32,
+                        c_vp, c_vp],
     "kvs_build_rows": [c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "kvs_attention_fwd": [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_i32, c_vp, c_i32, c_i32,
                           P(KVArena), P(Batch), c_f32, c_vp, c_vp, c_vp],

@@ -429,9 +429,11 @@ __global__ void __launch_bounds__(128) unpack_rows_kernel(
     Arena A, const int64_t *__restrict__ req_off, int32_t n_req,
     const int32_t *__restrict__ block_table, int32_t max_pages, const int64_t *__restrict__ flat_t,
     const int32_t *__restrict__ cand, const uint4 *__restrict__ in,
-    const float *__restrict__ cos_t, const float *__restrict__ sin_t) {
+    const float *__restrict__ cos_t, const float *__restrict__ sin_t, int32_t layer_begin,
+    int32_t layer_end, const uint8_t *__restrict__ skip) {
     const int64_t r = blockIdx.x;
     const int64_t t = flat_t[r];
+    if (skip != nullptr && skip[t]) return;
     int lo = 0, hi = n_req;
     while (hi - lo > 1) {
         int mid = (lo + hi) >> 1;
@@ -442,7 +444,7 @@ __global__ void __launch_bounds__(128) unpack_rows_kernel(
     const int64_t page = block_table[(int64_t)lo * max_pages + pos / A.P];
     const int half = A.D / 2, chunks = half / 8, vvec = A.G * A.D / 8;
     const uint4 *src = in + r * (int64_t)A.L * 2 * vvec;
-    for (int layer = 0; layer < A.L; ++layer) {
+    for (int layer = layer_begin; layer < layer_end; ++layer) {
         const uint4 *sk = src + (layer * 2 + 0) * vvec;
         const uint4 *sv = src + (layer * 2 + 1) * vvec;
         uint4 *dk = reinterpret_cast<uint4 *>(A.row(page, layer, 0, pos % A.P));
@@ -614,13 +616,18 @@ kvs_status kvs_pack_rows(const kvs_kv_arena *arena, const int32_t *slot, const i
 
 kvs_status kvs_unpack_rows(const kvs_kv_arena *arena, const kvs_batch *batch,
                            const int64_t *flat_t, const int32_t *cand, int64_t n_rows,
-                           const void *in, const kvs_rope *rope, kvs_stream_t stream) {
+                           const void *in, const kvs_rope *rope, int32_t layer_begin,
+                           int32_t layer_end, const uint8_t *skip, kvs_stream_t stream) {
     KVS_REQUIRE(arena && batch, KVS_EPARAM, "null arena/batch");
     KVS_REQUIRE(arena->head_dim % 16 == 0, KVS_ESHAPE, "head_dim must be a multiple of 16");
-    if (n_rows <= 0) return KVS_OK;
+    KVS_REQUIRE(0 <= layer_begin && layer_begin <= layer_end && layer_end <= arena->num_layers,
+                KVS_EPARAM, "layer range [%d, %d) outside [0, %d)", layer_begin, layer_end,
+                arena->num_layers);
+    if (n_rows <= 0 || layer_begin == layer_end) return KVS_OK;
     unpack_rows_kernel<<<(unsigned)n_rows, 128, 0, (cudaStream_t)stream>>>(
         make_arena(arena), batch->req_off, batch->n_req, batch->block_table, batch->max_pages,
-        flat_t, cand, (const uint4 *)in, rope ? rope->cos : nullptr, rope ? rope->sin : nullptr);
+        flat_t, cand, (const uint4 *)in, rope ? rope->cos : nullptr, rope ? rope->sin : nullptr,
+        layer_begin, layer_end, skip);
     KVS_CHECK_LAUNCH("kvs_unpack_rows");
     return KVS_OK;
 }

@@ -224,6 +224,7 @@ class Engine:
         self._xb_of = None
         self.layer0_fast = True     # prefill_batch: probe layer 0 doubles as the prefill's
         self._side = torch.cuda.Stream(self.device) if torch.cuda.is_available() else None
+        self._fetch_stream = torch.cuda.Stream(self.device) if torch.cuda.is_available() else None
 
     # ------------------------------------------------------------------ helpers
     def reset_timer_events(self, reserve: int = 0):
@@ -395,17 +396,21 @@ class Engine:
         st._contributed = res.contributed
         return st
 
-    def gather(self, st: BatchState, layers=None, slot=None):
+    def gather(self, st: BatchState, layers=None, slot=None, remote: bool = True):
         """G1 for layers [begin, end) (all by default); `slot` overrides the
-        hit map (e.g. with selected rows masked out)."""
+        hit map (e.g. with selected rows masked out).  remote=False leaves the
+        rows of other GPUs' shards to the caller."""
         if not self.pool.entries:
             return
         begin, end = layers if layers is not None else (0, self.cfg.num_layers)
         idx = self.pool._build_index()
         slot = st.src_slot if slot is None else slot
         if self.fetcher is not None:
-            slot = self.fetcher.local_mask(st.src_slot, idx)
-            self._timed("remote_fetch", self.fetcher.fetch, st, idx)
+            # remote-shard rows come through the fetcher (plain path: whole
+            # exchange here; the fast path of prefill_batch overlaps it)
+            slot = self.fetcher.local_mask(slot, idx)
+            if remote:
+                self._timed("remote_fetch", self.fetcher.fetch, st, idx, (begin, end))
         self._timed("gather", N.call, "kvs_gather_kv", self.arena.c, st.batch_c, slot.data_ptr(),
                st.src_cand.data_ptr(), idx["slot_pages"].data_ptr(), idx["slot_max_pages"], begin,
                end, self._rope(), N.stream_ptr())
@@ -493,6 +498,9 @@ class Engine:
         n = rows.n_rows
         alpha = torch.empty(n, dtype=torch.float32, device=dev)
         ws = self._ws["alpha"].get(N.ws_bytes("kvs_dhd_alpha_workspace", n, H, G), dev)
+        if getattr(st, "_before_alpha", None) is not None:
+            st._before_alpha()                                     # remote rows (sharded pool)
+            st._before_alpha = None
         if getattr(st, "_gathered", None) is not None:
             torch.cuda.current_stream().wait_event(st._gathered)     # k_pert complete
             st._gathered = None
@@ -574,23 +582,44 @@ class Engine:
             return st
         self.lookup(st)
         L = self.cfg.num_layers
-        if (mode == "selective" and ratio > 0 and self.probe_layer == 1 and self.fetcher is None
-                and self.layer0_fast):
+        if mode == "selective" and ratio > 0 and self.probe_layer == 1 and self.layer0_fast:
             # layers >= 1 gathered first; the probe's fresh layer 0 runs in
             # place and doubles as the partial prefill's layer 0; cached layer-0
             # rows return for the reused, unselected positions after selection
             # G1 (HBM-bound) runs on a side stream under the probe's layer 0
-            # (tensor-bound); D1 reads layer 1's k_pert, so it waits for it
+            # (tensor-bound); D1 reads layer 1's k_pert, so it waits for it.
+            # With a sharded pool the remote rows' exchange also runs off the
+            # main stream: planned and counted right after the lookup, moved
+            # and unpacked while the probe computes (st._before_alpha).
             main = torch.cuda.current_stream()
             self._side.wait_stream(main)
+            rf = None
+            if self.fetcher is not None:
+                idx = self.pool._build_index()
+                self._fetch_stream.wait_stream(main)
+                with torch.cuda.stream(self._fetch_stream):
+                    rf = self.fetcher.begin(st, idx)
             with torch.cuda.stream(self._side):
-                self.gather(st, (1, L))
+                self.gather(st, (1, L), remote=False)
                 gathered = torch.cuda.Event()
                 gathered.record()
             st._gathered = gathered
+            if rf is not None:
+                def before_alpha():
+                    with torch.cuda.stream(self._fetch_stream):
+                        self._timed("remote_fetch", rf.finish)
+                        rf.unpack(st, (1, L))
+                    main.wait_stream(self._fetch_stream)
+                    for t in (rf.rows, rf.flat_t, rf.cand):          # layer 0 later on main
+                        if t is not None:
+                            t.record_stream(main)
+                st._before_alpha = before_alpha
             self.probe_and_select(st, ratio, layer0_in_place=True)
             keep = torch.where(st.selected.bool(), torch.full_like(st.src_slot, -1), st.src_slot)
-            self.gather(st, (0, 1), slot=keep)
+            self.gather(st, (0, 1), slot=keep, remote=False)
+            if rf is not None:
+                rf.unpack(st, (0, 1), skip=st.selected)
+                st._remote_fetch = rf
             rows = self.build_rows(st, st.selected)
             self.session_forward(st, rows, x_probe=st._x_probe)
             st._x_probe = None

@@ -448,6 +448,7 @@ class CachePool:
         idx["slot_owner"] = owner
         idx["slot_on_owner"] = oslot
         idx["slot_owner_dev"] = torch.from_numpy(owner).to(dev)
+        idx["slot_on_owner_dev"] = torch.from_numpy(oslot).to(dev)
         idx["c"] = c
         self._index = idx
         self._dirty = False

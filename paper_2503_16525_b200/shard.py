@@ -7,98 +7,118 @@ reference (pool.py:125-161).  K/V payload stays on the GPU that wrote it.
 After the lookup a rank splits its hit rows into local ones (G1 gather) and
 remote ones, and fetches the latter in one grouped exchange:
 
-  1. all_to_all of per-peer row counts;
-  2. send (slot, cand) request lists to the owners;
-  3. owners pack the rows (kvs_pack_rows: all layers, K and V) and send
-     them back; receivers unpack into their pages with RoPE re-alignment
-     (kvs_unpack_rows).
+  1. plan on the device: owner of every hit row, remote rows grouped by owner
+     (a stable sort), per-peer counts; all_to_all of the counts;
+  2. the only host round trip: the 2 x world counts, to size the transfers;
+  3. all_to_all of the (owner slot, cached position) request lists;
+  4. owners pack the rows (kvs_pack_rows: all layers, K and V); all_to_all
+     of the packed rows; requesters unpack them into their pages with RoPE
+     re-alignment (kvs_unpack_rows, a layer range at a time).
 
-Point-to-point ops go through torch.distributed (NCCL over NVLink on the
-GPU box; gloo for the CPU tests of the planning and the exchange pattern).
-Nothing else on the path communicates.
+Steps 1-2 run on a fetch stream right after the lookup, so the host waits
+only for the count exchange while the probe's layer 0 is already queued on
+the main stream; steps 3-4 overlap the probe as well (engine.prefill_batch).
+Collectives go through torch.distributed: NCCL over NVLink on a multi-GPU
+box, gloo (staged through host memory) for the CPU tests and for the
+two-ranks-on-one-GPU functional test.  Nothing else on the path
+communicates.
 """
 from __future__ import annotations
 
-import numpy as np
 import torch
 import torch.distributed as dist
 
 from . import _native as N
 
 
-def plan_remote_rows(src_slot: np.ndarray, slot_owner: np.ndarray, rank: int, world: int):
-    """Flat positions whose hit lives on another rank, grouped by owner.
-    ``slot_owner[s]`` is the owning rank (or -1 for this rank)."""
-    need = [np.zeros(0, dtype=np.int64) for _ in range(world)]
-    hit = np.nonzero(src_slot >= 0)[0]
-    if hit.size == 0:
-        return need
-    own = slot_owner[src_slot[hit]]
-    own = np.where(own < 0, rank, own)
-    for q in range(world):
-        if q != rank:
-            need[q] = hit[own == q].astype(np.int64)
-    return need
+def plan_remote(src_slot: torch.Tensor, slot_owner: torch.Tensor, rank: int, world: int):
+    """Flat positions whose hit lives on another rank, grouped by owner rank
+    (ascending position within an owner), and the per-owner counts.
+    ``slot_owner[s]`` is the owning rank of slot s (-1 = every rank holds it).
+    Returns (order int64 [n] - the first counts.sum() entries are the remote
+    rows -, counts int64 [world]).  Runs where the tensors live; no sync."""
+    hit = src_slot >= 0
+    own = torch.where(hit, slot_owner[src_slot.clamp(min=0).long()].to(torch.int64),
+                      torch.full_like(src_slot, -1, dtype=torch.int64))
+    remote = hit & (own >= 0) & (own != rank)
+    key = torch.where(remote, own, torch.full_like(own, world))
+    order = torch.sort(key, stable=True).indices
+    counts = torch.bincount(key, minlength=world + 1)[:world]
+    return order, counts
 
 
-def exchange_rows(need, src_slot, src_cand, pack_fn, unpack_fn, rank: int, world: int,
-                  row_elems: int, dtype, device, group=None) -> int:
-    """Run the three-phase exchange; returns the number of rows received.
-    ``src_slot`` must already be in the owners' slot numbering.  With the gloo
-    backend the payloads are staged through host memory (CPU tests and the
-    single-GPU functional run); with NCCL they move GPU to GPU."""
-    staged = dist.get_backend(group) == "gloo"
-    comm = torch.device("cpu") if staged else device
-    send_counts = torch.tensor([len(need[q]) for q in range(world)], dtype=torch.int64,
-                               device=comm)
-    recv_counts = torch.empty_like(send_counts)
-    dist.all_to_all_single(recv_counts, send_counts, group=group)
-    recv_counts = recv_counts.cpu().numpy()
-    # phase 2: request lists (slot, cand) to the owners
-    ops, req_in = [], {}
-    for q in range(world):
-        if q == rank:
-            continue
-        if len(need[q]):
-            t = need[q]
-            lst = torch.from_numpy(np.stack([src_slot[t], src_cand[t]], 1).astype(np.int32))
-            ops.append(dist.P2POp(dist.isend, lst.to(comm).contiguous(), q, group))
-        if recv_counts[q]:
-            req_in[q] = torch.empty((int(recv_counts[q]), 2), dtype=torch.int32, device=comm)
-            ops.append(dist.P2POp(dist.irecv, req_in[q], q, group))
-    if ops:
-        for w in dist.batch_isend_irecv(ops):
-            w.wait()
-    # phase 3: owners pack and send rows back; requesters receive and unpack
-    ops, rows_in = [], {}
-    for q, lst in req_in.items():
-        lst = lst.to(device)
-        packed = pack_fn(lst[:, 0].contiguous(), lst[:, 1].contiguous())
-        ops.append(dist.P2POp(dist.isend, packed.to(comm), q, group))
-    for q in range(world):
-        if q != rank and len(need[q]):
-            rows_in[q] = torch.empty((len(need[q]), row_elems), dtype=dtype, device=comm)
-            ops.append(dist.P2POp(dist.irecv, rows_in[q], q, group))
-    if ops:
-        for w in dist.batch_isend_irecv(ops):
-            w.wait()
-    got = 0
-    for q, buf in rows_in.items():
-        t = need[q]
-        unpack_fn(torch.from_numpy(t).to(device), torch.from_numpy(src_cand[t].astype(np.int32))
-                  .to(device), buf.to(device))
-        got += len(t)
-    return got
+def _a2a(out: torch.Tensor, inp: torch.Tensor, out_splits, in_splits, group, staged: bool):
+    """all_to_all_single; with gloo the payload is staged through host memory."""
+    if not staged:
+        dist.all_to_all_single(out, inp, out_splits, in_splits, group=group)
+        return out
+    host_out = torch.empty(out.shape, dtype=out.dtype)
+    dist.all_to_all_single(host_out, inp.cpu(), out_splits, in_splits, group=group)
+    out.copy_(host_out)
+    return out
+
+
+class RemoteFetch:
+    """One exchange in flight: start() plans and swaps the counts, finish()
+    moves the rows and returns what unpack() needs."""
+
+    def __init__(self, fetcher: "RemoteFetcher", src_slot, src_cand, idx):
+        self.f, self.src_slot, self.src_cand, self.idx = fetcher, src_slot, src_cand, idx
+        self.rows = self.flat_t = self.cand = None
+        self.n_rows = 0
+
+    def start(self):
+        f = self.f
+        self.order, send = plan_remote(self.src_slot, self.idx["slot_owner_dev"], f.rank, f.world)
+        recv = torch.empty_like(send)
+        _a2a(recv, send, None, None, f.group, f.staged)
+        pair = torch.stack([send, recv])
+        self._counts = torch.empty(pair.shape, dtype=pair.dtype, pin_memory=not f.staged)
+        self._counts.copy_(pair, non_blocking=not f.staged)
+        if not f.staged:
+            self._ev = torch.cuda.Event()
+            self._ev.record()
+        return self
+
+    def finish(self):
+        f = self.f
+        if not f.staged:
+            self._ev.synchronize()                       # the one host round trip
+        send, recv = (self._counts[0].tolist(), self._counts[1].tolist())
+        n_need, n_give = int(sum(send)), int(sum(recv))
+        dev = self.src_slot.device
+        need = self.order[:n_need]
+        on_owner = self.idx["slot_on_owner_dev"][self.src_slot[need].long()]
+        req = torch.stack([on_owner, self.src_cand[need]], dim=1).to(torch.int32).contiguous()
+        got = torch.empty((n_give, 2), dtype=torch.int32, device=dev)
+        _a2a(got, req, recv, send, f.group, f.staged)
+        packed = f.pack(got[:, 0].contiguous(), got[:, 1].contiguous(), self.idx)
+        rows = torch.empty((n_need, f.row_elems), dtype=torch.bfloat16, device=dev)
+        _a2a(rows, packed, send, recv, f.group, f.staged)
+        self.rows, self.flat_t, self.cand = rows, need.contiguous(), self.src_cand[need].contiguous()
+        self.n_rows = n_need
+        return self
+
+    def unpack(self, st, layers, skip=None):
+        """Remote rows' layers [begin, end) into the request pages; rows with
+        skip[flat_t] set (e.g. DHD-selected positions) are left alone."""
+        if self.n_rows == 0:
+            return
+        eng = self.f.engine
+        N.call("kvs_unpack_rows", eng.arena.c, st.batch_c, self.flat_t.data_ptr(),
+               self.cand.data_ptr(), self.n_rows, self.rows.data_ptr(), eng._rope(), layers[0],
+               layers[1], N.ptr(skip), N.stream_ptr())
 
 
 class RemoteFetcher:
-    """Engine hook: local rows via G1, remote rows via exchange_rows."""
+    """Engine hook: local rows via G1, remote rows via RemoteFetch."""
 
     def __init__(self, engine, group=None):
         self.engine = engine
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
+        self.staged = dist.get_backend(group) == "gloo"
         cfg = engine.cfg
         self.row_elems = cfg.num_layers * 2 * cfg.kv_heads * 128
 
@@ -108,25 +128,21 @@ class RemoteFetcher:
         local = (src_slot >= 0) & ((owner[s] < 0) | (owner[s] == self.rank))
         return torch.where(local, src_slot, torch.full_like(src_slot, -1))
 
-    def fetch(self, st, idx) -> int:
+    def pack(self, slots: torch.Tensor, cands: torch.Tensor, idx) -> torch.Tensor:
         eng = self.engine
-        src = st.src_slot.cpu().numpy()
-        cand = st.src_cand.cpu().numpy()
-        need = plan_remote_rows(src, idx["slot_owner"], self.rank, self.world)
-        on_owner = np.where(src >= 0, idx["slot_on_owner"][np.maximum(src, 0)], -1)
-        arena = eng.arena
+        out = torch.empty((slots.numel(), self.row_elems), dtype=torch.bfloat16,
+                          device=eng.device)
+        N.call("kvs_pack_rows", eng.arena.c, slots.data_ptr(), cands.data_ptr(), slots.numel(),
+               idx["slot_pages"].data_ptr(), idx["slot_max_pages"], out.data_ptr(),
+               N.stream_ptr())
+        return out
 
-        def pack(slots, cands):
-            out = torch.empty((slots.numel(), self.row_elems), dtype=torch.bfloat16,
-                              device=eng.device)
-            N.call("kvs_pack_rows", arena.c, slots.data_ptr(), cands.data_ptr(), slots.numel(),
-                   idx["slot_pages"].data_ptr(), idx["slot_max_pages"], out.data_ptr(),
-                   N.stream_ptr())
-            return out
+    def begin(self, st, idx) -> RemoteFetch:
+        return RemoteFetch(self, st.src_slot, st.src_cand, idx).start()
 
-        def unpack(flat_t, cands, buf):
-            N.call("kvs_unpack_rows", arena.c, st.batch_c, flat_t.data_ptr(), cands.data_ptr(),
-                   flat_t.numel(), buf.data_ptr(), eng._rope(), N.stream_ptr())
-
-        return exchange_rows(need, on_owner, cand, pack, unpack, self.rank, self.world,
-                             self.row_elems, torch.bfloat16, eng.device, self.group)
+    def fetch(self, st, idx, layers=None) -> int:
+        """Whole exchange and unpack of layers [begin, end) on the current
+        stream (the plain, non-overlapped path)."""
+        rf = self.begin(st, idx).finish()
+        rf.unpack(st, layers or (0, self.engine.cfg.num_layers))
+        return rf.n_rows

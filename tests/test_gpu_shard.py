@@ -1,10 +1,13 @@
-"""Sharded pool on a real GPU: two ranks (gloo, both on
-cuda:0 - the driver's boxes have one GPU) each own half of the source
-entries' K/V pages; the token index is replicated.  Every rank runs the same
-scheduled batch, fetching the rows it hits on the other rank's shard through
-the pack -> exchange -> unpack path (kvs_pack_rows / kvs_unpack_rows).  The
-hit maps must equal the single-rank run bit for bit and the first-token
-states must agree to within GEMM-shape rounding."""
+"""Sharded pool on a real GPU: two ranks each own half of the
+source entries' K/V pages; the token index is replicated.  Every rank runs
+the same scheduled batch through the bench's fast prefill path, fetching the
+rows it hits on the other rank's shard on the fetch stream (device-side
+plan, count exchange, request lists, kvs_pack_rows -> exchange ->
+kvs_unpack_rows for layers >= 1 under the probe, layer 0 after selection).
+The hit maps must equal the single-rank run bit for bit and the first-token
+states must agree to within GEMM-shape rounding.  gloo with both ranks on
+cuda:0 (the driver's boxes have one GPU); the NCCL twin runs when the box
+has two GPUs.  bench.py --gpus 2 must spawn and run its two ranks."""
 import os
 import socket
 import sys
@@ -28,7 +31,7 @@ def _port():
     return p
 
 
-def _run(rank, world, port, out):
+def _run(rank, world, port, out, backend="gloo"):
     import torch.distributed as dist
     sys.path.insert(0, ROOT)
     import bench
@@ -36,14 +39,21 @@ def _run(rank, world, port, out):
     if world > 1:
         os.environ["MASTER_ADDR"] = "127.0.0.1"
         os.environ["MASTER_PORT"] = str(port)
-        dist.init_process_group("gloo", rank=rank, world_size=world)
-    dev = torch.device("cuda", 0)
+        if backend == "nccl":
+            dist.init_process_group("nccl", rank=rank, world_size=world,
+                                    device_id=torch.device("cuda", rank))
+        else:
+            dist.init_process_group("gloo", rank=rank, world_size=world)
+    dev = torch.device("cuda", rank if backend == "nccl" else 0)
     torch.cuda.set_device(dev)
     args = Namespace(layers=2, sources=4, seq=512, batch=3, hit=0.6, ratio=0.2)
     cfg, model, pool, eng, sources = bench.build_engine(args, dev, rank, world)
     batch = request_batches(sources, 1, args.batch, args.seq, args.hit, cfg.vocab_size, seed=7)[0]
     st = eng.prefill_batch(batch, ratio=args.ratio)
     torch.cuda.synchronize()
+    assert st.session_first == 1                          # fast path, also with a fetcher
+    if world > 1:
+        assert st._remote_fetch.n_rows > 0                # rows came from the other shard
     out.put((rank, st.src_slot.cpu().numpy(), st.src_cand.cpu().numpy(),
              st.hidden_last.cpu().numpy(), st.selected.cpu().numpy()))
     if world > 1:
@@ -51,11 +61,11 @@ def _run(rank, world, port, out):
         dist.destroy_process_group()
 
 
-def _spawn(world):
+def _spawn(world, backend="gloo"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_run, args=(r, world, port, q)) for r in range(world)]
+    procs = [ctx.Process(target=_run, args=(r, world, port, q, backend)) for r in range(world)]
     for p in procs:
         p.start()
     res = [q.get(timeout=600) for _ in range(world)]
@@ -75,3 +85,27 @@ def test_sharded_pool_matches_single_rank():
         assert rel < 1e-2, f"rank {rank}: first-token state rel err {rel:.3e}"
         # the same rows are recomputed up to near-ties of the DHD score
         assert (sel != single[4]).sum() <= max(2, int(0.02 * single[4].sum()))
+
+
+@pytest.mark.skipif(torch.cuda.device_count() < 2, reason="NCCL twin needs two GPUs")
+def test_sharded_pool_nccl_matches_single_rank():
+    single = _spawn(1)[0]
+    for rank, slot, cand, hidden, sel in _spawn(2, "nccl"):
+        np.testing.assert_array_equal(slot, single[1])
+        np.testing.assert_array_equal(cand, single[2])
+        rel = np.linalg.norm(hidden - single[3]) / np.linalg.norm(single[3])
+        assert rel < 1e-2, f"rank {rank}: first-token state rel err {rel:.3e}"
+
+
+def test_bench_spawns_ranks():
+    """bench.py --gpus 2 without a launcher starts two ranks itself."""
+    import json
+    import subprocess
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                          "--steps", "2", "--warmup", "1", "--layers", "2", "--seq", "512",
+                          "--batch", "2", "--sources", "4", "--profile"],
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0
+    assert line["dist_backend"] in ("gloo", "nccl")

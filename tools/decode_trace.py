@@ -31,7 +31,8 @@ def main():
     steps = 3
     with profile(activities=[ProfilerActivity.CPU, ProfilerActivity.CUDA]) as prof:
         for _ in range(steps):
-            eng.decode_step(st, rng.integers(0, cfg.vocab_size, len(batch)), 3)
+            tok = torch.from_numpy(rng.integers(0, cfg.vocab_size, len(batch))).to(dev)
+            eng.decode_step_device(st, tok, 3)
         torch.cuda.synchronize()
     path = os.path.join(ROOT, "gpurun_out", "decode_trace.json")
     os.makedirs(os.path.dirname(path), exist_ok=True)
