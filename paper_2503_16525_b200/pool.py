@@ -203,6 +203,7 @@ class CachePool:
         self._slot_hash: list[torch.Tensor | None] = []
         self._dirty = True
         self._index = None
+        self._tidx = None
         self._ws = N.Workspace()
 
     # ------------------------------------------------------------------ basics
@@ -229,9 +230,8 @@ class CachePool:
 
     # ------------------------------------------------------------------ insert
     def _new_slot(self) -> int:
-        for i, e in enumerate(self._slots):
-            if e is None:
-                return i
+        """Slots are append-only (a freed slot is never handed out again), so
+        the device index only ever appends; _compact() reclaims them."""
         self._slots.append(None)
         self._slot_tokens.append(None)
         self._slot_hash.append(None)
@@ -252,7 +252,12 @@ class CachePool:
         ``owner`` in its slot ``owner_slot`` (sharded pool).
         Lookups see it like any other entry; its rows are fetched from the
         owner by shard.RemoteFetcher.  ``owner_slot`` defaults to this pool's
-        slot, which is the owner's too when every rank inserts in one order."""
+        slot, which is the owner's too when every rank inserts in one order
+        (slot ids are append-only and sharded pools never evict or renumber)."""
+        if self.capacity_bytes is not None:
+            # every rank evicts on its own LRU: victims (and slot ids) would
+            # diverge between the ranks that share this entry's owner slot
+            raise ParameterError("a sharded pool cannot use capacity_bytes")
         entry = self.insert_pages(request_id, tokens, [])
         entry.owner = int(owner)
         entry.owner_slot = entry.slot if owner_slot is None else int(owner_slot)
@@ -277,6 +282,7 @@ class CachePool:
         self._dirty = True
         if self.capacity_bytes is not None:
             self.evict_to_capacity(self.capacity_bytes)
+        self._maybe_renumber()
         return entry
 
     def insert(self, request_id: str, tokens, k, v) -> None:
@@ -390,46 +396,47 @@ class CachePool:
 
     # ------------------------------------------------------------------ index
     def _build_index(self):
+        """The device token index, maintained incrementally:
+
+        * entry tokens, window hashes and window slots live in append-only
+          flat device buffers (capacity doubling); a new entry appends its
+          rows and its windows are merged into the hash-sorted window list
+          (sort of the new windows + a searchsorted merge: O(new log new +
+          total) device work, no re-sort and no host rebuild of the index);
+        * a dropped entry only loses its recency rank (-1): the lookup
+          kernels skip its windows;
+        * when dead windows outnumber live ones the buffers are compacted
+          (live slots keep their ids), and when freed slot ids dominate, live
+          entries are renumbered (single-GPU pools only: a sharded pool's
+          slot ids are shared with the owners).
+        Recency ranks, slot page tables and owners are small per-slot host
+        arrays re-uploaded after any change."""
         if not self._dirty and self._index is not None:
             return self._index
-        live = [i for i, e in enumerate(self._slots) if e is not None]
-        n_slots = len(self._slots)
         dev = self.device
-        tok_off = np.zeros(n_slots + 1, dtype=np.int64)
-        win_off = np.zeros(n_slots + 1, dtype=np.int64)
-        toks, hashes, wslot = [], [], []
-        for s in range(n_slots):
-            t = self._slot_tokens[s]
-            n = 0 if t is None else t.numel()
-            nw = 0 if t is None else self._slot_hash[s].numel()
-            tok_off[s + 1] = tok_off[s] + n
-            win_off[s + 1] = win_off[s] + nw
-            if t is not None:
-                toks.append(t)
-                hashes.append(self._slot_hash[s])
-                wslot.append(torch.full((nw,), s, dtype=torch.int32, device=dev))
-        n_windows = int(win_off[-1])
-        tokens = torch.cat(toks) if toks else torch.zeros(1, dtype=torch.int64, device=dev)
-        win_hash = torch.cat(hashes) if hashes else torch.zeros(1, dtype=torch.int64, device=dev)
-        win_slot = torch.cat(wslot) if wslot else torch.zeros(1, dtype=torch.int32, device=dev)
-        sorted_hash = torch.empty(max(n_windows, 1), dtype=torch.int64, device=dev)
-        sorted_widx = torch.empty(max(n_windows, 1), dtype=torch.int32, device=dev)
-        if n_windows:
-            ws = self._ws.get(N.ws_bytes("kvs_index_sort_workspace", n_windows), dev)
-            N.call("kvs_index_sort", win_hash.data_ptr(), n_windows, sorted_hash.data_ptr(),
-                   sorted_widx.data_ptr(), ws.data_ptr(), ws.numel(), N.stream_ptr())
-        order = sorted(live, key=lambda s: -self._slots[s].insert_seq)
+        n_slots = len(self._slots)
+        live = [i for i, e in enumerate(self._slots) if e is not None]
+        ti = self._tidx
+        if ti is None:
+            ti = self._tidx = _TokenIndexBuffers(dev)
+        # append the slots that are new since the last build
+        for sl in range(ti.n_slots, n_slots):
+            ti.append(self._slot_tokens[sl], self._slot_hash[sl])
+        ti.set_live(self._slots)
+        if ti.dead_windows() > max(ti.live_windows(), 1 << 16):
+            ti.compact(self._slots, self._slot_tokens, self._slot_hash)
+        order = sorted(live, key=lambda sl: -self._slots[sl].insert_seq)
         rank = np.full(max(n_slots, 1), -1, dtype=np.int32)
         r2s = np.zeros(max(n_slots, 1), dtype=np.int32)
-        for r, s in enumerate(order):
-            rank[s] = r
-            r2s[r] = s
-        idx = dict(tokens=tokens, tok_off=torch.from_numpy(tok_off).to(dev),
-                   win_off=torch.from_numpy(win_off).to(dev), win_hash=win_hash,
-                   win_slot=win_slot, sorted_hash=sorted_hash, sorted_widx=sorted_widx,
-                   slot_rank=torch.from_numpy(rank).to(dev), rank2slot=torch.from_numpy(r2s).to(dev))
+        for r, sl in enumerate(order):
+            rank[sl] = r
+            r2s[r] = sl
+        idx = dict(tokens=ti.tokens, tok_off=ti.tok_off_dev(), win_off=ti.win_off_dev(),
+                   win_hash=ti.win_hash, win_slot=ti.win_slot, sorted_hash=ti.sorted_hash,
+                   sorted_widx=ti.sorted_widx, slot_rank=torch.from_numpy(rank).to(dev),
+                   rank2slot=torch.from_numpy(r2s).to(dev))
         p = self.params
-        c = N.TokenIndex(n_slots, n_windows, p.window_size, p.base, p.modulus,
+        c = N.TokenIndex(n_slots, ti.n_sorted, p.window_size, p.base, p.modulus,
                          *(idx[k].data_ptr() for k in ("tokens", "tok_off", "win_off", "win_hash",
                                                         "win_slot", "sorted_hash", "sorted_widx",
                                                         "slot_rank", "rank2slot")))
@@ -437,12 +444,12 @@ class CachePool:
         sp = np.zeros((max(n_slots, 1), max_pages), dtype=np.int32)
         owner = np.full(max(n_slots, 1), -1, dtype=np.int32)
         oslot = np.arange(max(n_slots, 1), dtype=np.int32)
-        for s in live:
-            pg = self._slots[s].pages
-            sp[s, :len(pg)] = pg
-            owner[s] = self._slots[s].owner
-            if self._slots[s].owner >= 0:
-                oslot[s] = self._slots[s].owner_slot
+        for sl in live:
+            pg = self._slots[sl].pages
+            sp[sl, :len(pg)] = pg
+            owner[sl] = self._slots[sl].owner
+            if self._slots[sl].owner >= 0:
+                oslot[sl] = self._slots[sl].owner_slot
         idx["slot_pages"] = torch.from_numpy(sp).to(dev)
         idx["slot_max_pages"] = max_pages
         idx["slot_owner"] = owner
@@ -453,6 +460,20 @@ class CachePool:
         self._index = idx
         self._dirty = False
         return idx
+
+    def _maybe_renumber(self) -> None:
+        """Reclaim freed slot ids once they dominate (single-GPU pools)."""
+        n_live = len(self.entries)
+        if len(self._slots) <= 2 * n_live + 64 or any(e.owner >= 0 for e in self.entries.values()):
+            return
+        live = [e for e in self._slots if e is not None]
+        toks = [self._slot_tokens[e.slot] for e in live]
+        hashes = [self._slot_hash[e.slot] for e in live]
+        self._slots, self._slot_tokens, self._slot_hash = list(live), toks, hashes
+        for i, e in enumerate(live):
+            e.slot = i
+        self._tidx = None                       # rebuilt from the renumbered slots
+        self._dirty = True
 
     # ------------------------------------------------------------------ lookup
     def lookup_device(self, tokens_flat: torch.Tensor, req_off: torch.Tensor,
@@ -546,3 +567,107 @@ class CachePool:
 
     def slot_entry(self, slot: int) -> KVEntry | None:
         return self._slots[slot] if 0 <= slot < len(self._slots) else None
+
+
+class _TokenIndexBuffers:
+    """Append-only device buffers behind CachePool's token index (see
+    CachePool._build_index).  Hashes are < 2^63, so int64 order is the
+    uint64 order the lookup kernels search."""
+
+    def __init__(self, device):
+        self.device = device
+        z64 = lambda: torch.zeros(1, dtype=torch.int64, device=device)   # noqa: E731
+        self.tokens, self.win_hash = z64(), z64()
+        self.win_slot = torch.zeros(1, dtype=torch.int32, device=device)
+        self.sorted_hash, self.sorted_widx = z64(), torch.zeros(1, dtype=torch.int32, device=device)
+        self.n_tok = self.n_win = self.n_sorted = 0
+        self.tok_off, self.win_off = [0], [0]
+        self.live = []                              # per slot: still in the pool
+        self._off_dev = None
+
+    @property
+    def n_slots(self) -> int:
+        return len(self.tok_off) - 1
+
+    @staticmethod
+    def _grow(buf: torch.Tensor, need: int) -> torch.Tensor:
+        if buf.numel() >= need:
+            return buf
+        out = torch.empty(max(need, 2 * buf.numel()), dtype=buf.dtype, device=buf.device)
+        out[:buf.numel()].copy_(buf)
+        return out
+
+    def append(self, tok: torch.Tensor | None, hashes: torch.Tensor | None) -> None:
+        n = 0 if tok is None else tok.numel()
+        m = 0 if hashes is None else hashes.numel()
+        slot = self.n_slots
+        self.tokens = self._grow(self.tokens, self.n_tok + n)
+        self.win_hash = self._grow(self.win_hash, self.n_win + m)
+        self.win_slot = self._grow(self.win_slot, self.n_win + m)
+        if n:
+            self.tokens[self.n_tok:self.n_tok + n].copy_(tok)
+        if m:
+            self.win_hash[self.n_win:self.n_win + m].copy_(hashes)
+            self.win_slot[self.n_win:self.n_win + m].fill_(slot)
+            self._merge(hashes, self.n_win)
+        self.n_tok += n
+        self.n_win += m
+        self.tok_off.append(self.n_tok)
+        self.win_off.append(self.n_win)
+        self.live.append(tok is not None)
+        self._off_dev = None
+
+    def _merge(self, hashes: torch.Tensor, first_widx: int) -> None:
+        """Merge new windows (widx first_widx + k) into the sorted list."""
+        h_new, perm = torch.sort(hashes)
+        w_new = (perm + first_widx).to(torch.int32)
+        N0, M = self.n_sorted, h_new.numel()
+        out_h = torch.empty(N0 + M, dtype=torch.int64, device=self.device)
+        out_w = torch.empty(N0 + M, dtype=torch.int32, device=self.device)
+        if N0:
+            old_h, old_w = self.sorted_hash[:N0], self.sorted_widx[:N0]
+            pos_new = torch.searchsorted(old_h, h_new, right=True) + \
+                torch.arange(M, device=self.device)
+            pos_old = torch.searchsorted(h_new, old_h, right=False) + \
+                torch.arange(N0, device=self.device)
+            out_h[pos_old] = old_h
+            out_w[pos_old] = old_w
+            out_h[pos_new] = h_new
+            out_w[pos_new] = w_new
+        else:
+            out_h.copy_(h_new)
+            out_w.copy_(w_new)
+        self.sorted_hash, self.sorted_widx, self.n_sorted = out_h, out_w, N0 + M
+
+    def set_live(self, slots) -> None:
+        self.live = [slots[i] is not None for i in range(self.n_slots)]
+
+    def live_windows(self) -> int:
+        return sum(self.win_off[i + 1] - self.win_off[i] for i in range(self.n_slots)
+                   if self.live[i])
+
+    def dead_windows(self) -> int:
+        return self.n_sorted - self.live_windows()
+
+    def compact(self, slots, slot_tokens, slot_hash) -> None:
+        """Rebuild the buffers from the live slots only (slot ids kept; a dead
+        slot keeps an empty range)."""
+        fresh = _TokenIndexBuffers(self.device)
+        for i in range(self.n_slots):
+            alive = slots[i] is not None
+            fresh.append(slot_tokens[i] if alive else None, slot_hash[i] if alive else None)
+        fresh.set_live(slots)
+        self.__dict__.update(fresh.__dict__)
+
+    def tok_off_dev(self) -> torch.Tensor:
+        self._offsets()
+        return self._off_dev[0]
+
+    def win_off_dev(self) -> torch.Tensor:
+        self._offsets()
+        return self._off_dev[1]
+
+    def _offsets(self) -> None:
+        if self._off_dev is None:
+            self._off_dev = (torch.tensor(self.tok_off, dtype=torch.int64, device=self.device),
+                             torch.tensor(self.win_off, dtype=torch.int64, device=self.device))

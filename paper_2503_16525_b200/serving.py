@@ -7,7 +7,7 @@ batch: arrivals are admitted whenever the server frees up, each admitted
 request gets its hit rate from a pool lookup (R2 on the device), the
 cache-aware (or FCFS) scheduler forms the next batch, and the batch is
 charged a prefill latency.  Decode runs off the server, one tick per token;
-completed requests write their prefill K/V back to the pool.
+completed requests write their K/V back to the pool.
 
 What changes: the batch actually runs on the GPU (Engine.prefill_batch: G1,
 probe, D1, D2, partial prefill over the scheduled requests together), and
@@ -19,9 +19,12 @@ event loop; the measured run then turns the logical TTFT into real TTFT and
 records (mean hit rate, measured ms) per batch for the paper's concave
 latency premise.  Write-back is zero-copy: the request's
 arena pages become the pool entry (reference copies K/V, simulate.py:207-210).
-Deviation metrics and decode-stage recompute (simulate.py:218-310) are not
-part of this loop; decode ticks cost 1 ms per token as in the reference with
-LatencyModel.per_token_ms = 0.
+After each prefill batch the decode stage runs on the device (decode-stage
+DHD, simulate.py:268-276), so write-back stores the decode-corrected K/V of
+the prefill rows like the reference (simulate.py:298-301).  The per-request
+deviation metrics of _process_request (simulate.py:250-296) are not carried;
+decode ticks cost 1 ms per token on the logical clock as in the reference
+with LatencyModel.per_token_ms = 0.
 """
 from __future__ import annotations
 
@@ -94,24 +97,64 @@ class ServingReport:
     aggregate: dict = field(default_factory=dict)
 
 
-def measure_prefill(engine, token_lists, ratio: float, mode: str = "selective"):
+def measure_prefill(engine, token_lists, ratio: float, mode: str = "selective",
+                    decode_capacity: int = 0):
     """Run one scheduled batch through Engine.prefill_batch; returns (state,
     device milliseconds between CUDA events around it)."""
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
-    st = engine.prefill_batch(token_lists, ratio=ratio, mode=mode)
+    st = engine.prefill_batch(token_lists, ratio=ratio, mode=mode,
+                              decode_capacity=decode_capacity)
     e1.record()
     torch.cuda.synchronize()
     return st, float(e0.elapsed_time(e1))
 
 
+def decode_token_stream(seed: int, request_index: int, steps: int, vocab_size: int) -> list:
+    """simulate.py:134-137: Philox over SeedSequence((seed, request index))."""
+    seq = np.random.SeedSequence(entropy=(seed, request_index))
+    gen = np.random.Generator(np.random.Philox(seq))
+    return gen.integers(0, vocab_size, steps).tolist()
+
+
+def decode_batch(engine, st, streams, n_extra: int) -> None:
+    """The decode stage of a served batch on the device (simulate.py:268-276
+    -> engine.py:298-328): every step, D3 picks up to n_extra still-stale
+    rows per request and recomputes them in the same pass as the new token,
+    so the request's pages end up holding the decode-corrected K/V that the
+    reference writes back (simulate.py:298-301).  A request whose own decode
+    steps are done stops recomputing (its eligibility is cleared); its extra
+    appended rows lie beyond the written-back prefix."""
+    R = len(streams)
+    steps = max((len(s) for s in streams), default=0)
+    if steps == 0:
+        return
+    if st.eligible is None:
+        n_extra = 0
+    toks = np.zeros((steps, R), dtype=np.int64)
+    for r, s in enumerate(streams):
+        toks[:len(s), r] = s
+    dev = engine.device
+    tok_dev = torch.from_numpy(toks).to(dev)
+    for t in range(steps):
+        for r, s in enumerate(streams):
+            if len(s) == t and n_extra > 0:        # request r has no step t: no more recompute
+                a, b = int(st.req_off_host[r]), int(st.req_off_host[r + 1])
+                st.eligible[a:b] = 0
+        engine.decode_step_device(st, tok_dev[t], n_extra)
+
+
 def run_serving(trace, engine, *, batch_size: int = 4, ratio: float = 0.2,
                 scheduler: str = "cache_aware", mode: str = "selective",
                 latency: LatencyModel | None = None, matcher: str = "adaptive",
-                chunk_size: int | None = None) -> ServingReport:
+                chunk_size: int | None = None, n_extra: int = 3,
+                seed: int = 0) -> ServingReport:
     """simulate.py:140-215 over the GPU engine.  ``latency=None`` charges each
     batch its measured device time; a LatencyModel charges f(mean hit) +
-    per-token term exactly like the reference (the batch still runs)."""
+    per-token term exactly like the reference (the batch still runs).  The
+    decode stage runs on the device after each prefill batch (decode-stage
+    DHD with n_extra, decode tokens from the reference's stream for ``seed``)
+    so completed requests write back decode-corrected K/V."""
     if batch_size < 1:
         raise ConfigError(f"batch_size must be >= 1, got {batch_size}")
     if mode not in ("selective", "fr", "naive"):
@@ -126,6 +169,7 @@ def run_serving(trace, engine, *, batch_size: int = 4, ratio: float = 0.2,
     chunk = chunk_size or pool.params.window_size
     pending = sorted(trace, key=lambda r: (r.arrival_ms, r.id))
     records = {r.id: r for r in pending}
+    index = {r.id: i for i, r in enumerate(pending)}     # simulate.py:159 request index
     queue: list = []
     writebacks: list = []            # heap of (completion_ms, seq, id, tokens, pages)
     wb_seq = 0
@@ -157,9 +201,17 @@ def run_serving(trace, engine, *, batch_size: int = 4, ratio: float = 0.2,
         chosen = {r.id for r in batch.requests}
         queue = [r for r in queue if r.id not in chosen]
         toks = [np.asarray(records[r.id].tokens, dtype=np.int64) for r in batch.requests]
+        steps = max(records[r.id].decode_steps for r in batch.requests)
         st, measured = measure_prefill(engine, toks, ratio,
                                        "full" if mode == "fr" else
-                                       ("naive" if mode == "naive" else "selective"))
+                                       ("naive" if mode == "naive" else "selective"),
+                                       decode_capacity=steps if mode != "fr" else 0)
+        if mode != "fr":
+            # FR writes back fresh K/V (simulate.py:232-248); the other modes
+            # write back what decode leaves in the cache
+            streams = [decode_token_stream(seed, index[r.id], records[r.id].decode_steps,
+                                           engine.cfg.vocab_size) for r in batch.requests]
+            decode_batch(engine, st, streams, 0 if mode == "naive" else n_extra)
         charged = batch_latency(batch, latency) if latency is not None else measured
         batches.append((batch.mean_hit_rate, charged, measured))
         prefill_done = now + charged

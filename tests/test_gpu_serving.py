@@ -65,3 +65,40 @@ def test_measured_latency_run():
     assert all(b[1] == b[2] and b[2] > 0 for b in rep.batches)      # charged == measured
     assert len(eng.pool.entries) == 12                              # every request written back
     assert rep.aggregate["throughput_tokens_per_s"] > 0
+
+
+def test_writeback_holds_decode_corrected_kv():
+    """simulate.py:298-301: a completed request writes back the K/V its
+    session holds after the decode stage (rows D3 chose were recomputed in
+    place), not the prefill-time cache.  The served entry equals a replay of
+    the same prefill + decode on a twin engine, and differs from the
+    prefill-only cache exactly on rows the decode stage recomputed."""
+    import torch
+
+    from paper_2503_16525_b200.serving import (TraceRecord, decode_batch, decode_token_stream,
+                                               run_serving)
+    K, eng = _engine()
+    K2, twin = _engine()
+    rng = np.random.default_rng(9)
+    src = rng.integers(0, 512, 96).tolist()
+    req = rng.integers(0, 512, 10).tolist() + src[4:80] + rng.integers(0, 512, 12).tolist()
+    trace = [TraceRecord("a", 0.0, src, 0), TraceRecord("b", 500.0, req, 6)]
+    run_serving(trace, eng, batch_size=1, latency=K.LatencyModel(), n_extra=3, seed=0)
+    run_serving(trace[:1], twin, batch_size=1, latency=K.LatencyModel(), n_extra=3, seed=0)
+    st = twin.prefill_batch([np.asarray(req)], ratio=0.2, decode_capacity=6)
+    n = len(req)
+    before = torch.stack([twin.arena.rows(st.pages[0], n, l, kv) for l in range(2)
+                          for kv in (0, 1)]).clone()
+    elig0 = st.eligible.clone()
+    decode_batch(twin, st, [decode_token_stream(0, 1, 6, 512)], 3)
+    after = torch.stack([twin.arena.rows(st.pages[0], n, l, kv) for l in range(2)
+                         for kv in (0, 1)])
+    entry = eng.pool.entries["b"]
+    served = torch.stack([eng.arena.rows(entry.pages, n, l, kv) for l in range(2)
+                          for kv in (0, 1)])
+    assert torch.equal(served, after)
+    recomputed = (elig0.bool() & ~st.eligible.bool()).nonzero().flatten()
+    assert recomputed.numel() > 0
+    changed = (after != before).flatten(2).any(-1).any(0).nonzero().flatten()
+    assert set(changed.tolist()) <= set(recomputed.tolist())
+    assert len(set(changed.tolist())) > 0
