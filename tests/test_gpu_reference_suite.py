@@ -21,7 +21,7 @@ REF_TESTS = os.path.join(ROOT, "baseline", "_ref", "kvlab_tests")
 def test_reference_matcher_suite_on_gpu_matchcore():
     env = dict(os.environ, PYTHONPATH=os.pathsep.join(
         [os.path.join(ROOT, "tests"), os.path.join(ROOT, "baseline", "_ref"), ROOT]))
-    cmd = [sys.executable, "-m", "pytest", "-q", "-p", "_gpu_matchcore_plugin",
+    cmd = [sys.executable, "-m", "pytest", "-p", "_gpu_matchcore_plugin",
            "-p", "no:cacheprovider", os.path.join(REF_TESTS, "test_matching.py"),
            os.path.join(REF_TESTS, "test_acceptance.py"), "-k",
            "not test_acceptance or criterion_05 or criterion_06"]
@@ -29,4 +29,8 @@ def test_reference_matcher_suite_on_gpu_matchcore():
                          timeout=1200)
     tail = out.stdout[-3000:] + out.stderr[-2000:]
     assert out.returncode == 0, tail
-    assert " passed" in out.stdout and "failed" not in out.stdout, tail
+    import re
+    m = re.search(r"(\d+) passed", out.stdout)
+    assert m and int(m.group(1)) >= 30 and "failed" not in out.stdout, tail
+    assert "GPU drop-in" in out.stdout, tail          # the plugin's report header
+    print(out.stdout.strip().splitlines()[-1])
