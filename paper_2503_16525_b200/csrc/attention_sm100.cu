@@ -104,7 +104,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         fence_barrier_init();
     }
-    if (warp == 5) tmem_alloc(&sh.tmem_base, 512);
+    // LSE-only launches (D1 pass 1) need S double-buffered and no O: 256
+    // columns, so two CTAs share an SM (two softmax warps per SMSP)
+    constexpr uint32_t kTmemCols = kPV ? 512 : 256;
+    if (warp == 5) tmem_alloc(&sh.tmem_base, kTmemCols);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -289,6 +292,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         const int64_t grow = (int64_t)row0 + i;
         if (kPV) {
+            // every pv_done phase is waited on (PV(n_kb-2) was not, above)
+            if (n_kb >= 2) mbar_wait(&sh.pv_done[n_kb & 1], (uint32_t)((n_kb - 2) >> 1) & 1u);
             if (n_kb >= 1) mbar_wait(&sh.pv_done[(n_kb - 1) & 1], (uint32_t)((n_kb - 1) >> 1) & 1u);
             tc_fence_after();
             const float inv = l > 0.f ? 1.f / l : 0.f;
@@ -320,7 +325,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     __syncthreads();
     if (warp == 5) {
         tc_fence_after();
-        tmem_dealloc(tmem, 512);
+        tmem_dealloc(tmem, kTmemCols);
     }
 }
 
@@ -456,7 +461,9 @@ __global__ void __launch_bounds__(kThreads2, 1)
                         umma_bf16_ts(tmem + 256 + 128 * t, tmem + 128 * t + 8 * k, db, idesc_pv,
                                      (kb > 0 || k > 0) ? 1u : 0u);
                     }
-                    umma_commit(&sh.pv_done[t]);
+                    // O is read back once, after the last P.V: one pv_done phase
+                    // per head (a phase nobody waits on is a synccheck error)
+                    if (!more) umma_commit(&sh.pv_done[t]);
                     if (more) {
                         if (t == 0) mbar_wait(&sh.ring_full[kslot], (uint32_t)(itk / RING3) & 1u);
                         TRACE(13 + t, kb);
@@ -588,7 +595,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
         }
         if (kPingPong && t == 0 && n_kb >= 1) asm volatile("bar.sync 1, 256;" ::: "memory");
         const int64_t grow = (int64_t)row0 + i;
-        if (n_kb >= 1) mbar_wait(&sh.pv_done[t], (uint32_t)(n_kb - 1) & 1u);
+        if (n_kb >= 1) mbar_wait(&sh.pv_done[t], 0u);
         tc_fence_after();
         const float inv = l > 0.f ? 1.f / l : 0.f;
         float o[32];
@@ -823,6 +830,9 @@ __global__ void __launch_bounds__(kThreads6, 1)
             tmem_st_wait();
             tc_fence_before();
             mbar_arrive(&sh.p_full[b]);
+            // consume PV(kb-1)'s phase (it ran under this block's softmax, so
+            // the wait is free): every pv_done phase is waited on
+            if (kb >= 1) mbar_wait(&sh.pv_done[(kb - 1) & 1], (uint32_t)((kb - 1) >> 1) & 1u);
         }
         const int64_t grow = (int64_t)row0 + i;
         if (n_kb >= 1) mbar_wait(&sh.pv_done[(n_kb - 1) & 1], (uint32_t)((n_kb - 1) >> 1) & 1u);

@@ -396,11 +396,19 @@ class Engine:
         st._contributed = res.contributed
         return st
 
+    def set_hits(self, st: BatchState, hits) -> None:
+        """Hit maps from CachePool.admit for the batch's requests, in order."""
+        if len(hits) != len(st.lengths) or any(h.length != int(l) for h, l in zip(hits, st.lengths)):
+            raise InputError("admitted hit maps do not match the batch's requests")
+        st.src_slot = torch.cat([h.src_slot for h in hits])
+        st.src_cand = torch.cat([h.src_cand for h in hits])
+        st.n_hit = np.array([h.n_hit for h in hits], dtype=np.int64)
+
     def gather(self, st: BatchState, layers=None, slot=None, remote: bool = True):
         """G1 for layers [begin, end) (all by default); `slot` overrides the
         hit map (e.g. with selected rows masked out).  remote=False leaves the
         rows of other GPUs' shards to the caller."""
-        if not self.pool.entries:
+        if not self.pool.entries and not self.pool._retired:
             return
         begin, end = layers if layers is not None else (0, self.cfg.num_layers)
         idx = self.pool._build_index()
@@ -568,19 +576,27 @@ class Engine:
         return x
 
     def prefill_batch(self, token_lists, ratio: float = 0.2, mode: str = "selective",
-                      decode_capacity: int = 0, tokens_dev=None) -> BatchState:
-        """One scheduled batch through the hot path (modes: selective / naive / full)."""
+                      decode_capacity: int = 0, tokens_dev=None, hits=None) -> BatchState:
+        """One scheduled batch through the hot path (modes: selective / naive / full).
+        hits: the requests' admission-time hit maps (CachePool.admit results,
+        simulate.py:180-186, 264-266) instead of a lookup at batch time."""
         if not 0.0 <= ratio <= 1.0:
             raise ParameterError(f"ratio must lie in [0, 1], got {ratio}")
         st = self.new_batch(token_lists, decode_capacity, tokens_dev)
-        if mode == "full" or not self.pool.entries:
+        if hits is not None and mode != "full":
+            self.set_hits(st, hits)
+            if not int(st.n_hit.sum()):
+                hits = None
+                mode = "full"
+        if mode == "full" or (hits is None and not self.pool.entries):
             st.n_hit_dev = torch.zeros(len(st.lengths), dtype=torch.int32, device=self.device)
             rows = self.build_rows(st, None)
             rows.write_kv.fill_(1)
             self.session_forward(st, rows)
             st.selected = None
             return st
-        self.lookup(st)
+        if hits is None:
+            self.lookup(st)
         L = self.cfg.num_layers
         if mode == "selective" and ratio > 0 and self.probe_layer == 1 and self.layer0_fast:
             # layers >= 1 gathered first; the probe's fresh layer 0 runs in
@@ -636,6 +652,22 @@ class Engine:
         sel = st.selected.bool() if st.selected is not None else torch.zeros_like(reused)
         st.eligible = (reused & ~sel).to(torch.uint8)
         return st
+
+    def forward_all_rows(self, st: BatchState, write_kv: torch.Tensor, capture=None):
+        """Every row of every request through every layer (model.py:163-208):
+        K/V are written for rows with write_kv set (uint8, flat over the
+        batch) and kept as gathered elsewhere - model_forward (all ones),
+        model_forward_with_reuse / a PRACTICAL session's prefill (not reused
+        or recomputed).  capture receives (layer, q, o) and (layer, "hidden",
+        x) like forward_rows."""
+        rows = self._rows_all(st)
+        x = self._embed(st.tokens, rows)
+        L = self.cfg.num_layers
+        x = self.forward_rows(x, rows, range(L), self.arena.c, st.batch_c,
+                              write_kv_per_layer=[write_kv] * L, capture=capture)
+        st.rows = rows
+        st.hidden_last = x[h2d(st.req_off_host[1:] - 1, self.device)]
+        return x
 
     def refresh_lru(self, st: BatchState):
         c = st._contributed.cpu().numpy()

@@ -21,7 +21,7 @@ import numpy as np
 import torch
 
 from . import _native as N
-from .errors import CacheError, FormatError, ParameterError
+from .errors import CacheError, FormatError, InputError, ParameterError
 from .matching import HashParams, window_hashes_device
 from .model import HEAD_DIM, ModelConfig
 
@@ -170,6 +170,28 @@ class ReuseMap:
 
 
 @dataclass
+class AdmittedHits:
+    """A request's admission-time device hit map (CachePool.admit); its
+    source slots stay pinned in the pool until release()."""
+
+    pool: "CachePool" = field(repr=False)
+    length: int
+    n_hit: int
+    src_slot: torch.Tensor         # int32 [length], -1 = miss
+    src_cand: torch.Tensor         # int32 [length]
+    slots: list
+
+    @property
+    def hit_rate(self) -> float:
+        return self.n_hit / self.length if self.length else 0.0
+
+    def release(self) -> None:
+        if self.slots is not None:
+            self.pool.unpin(self.slots)
+            self.slots = None
+
+
+@dataclass
 class BatchLookup:
     """Device hit maps of a batched lookup (flat over the batch)."""
 
@@ -205,6 +227,8 @@ class CachePool:
         self._index = None
         self._tidx = None
         self._ws = N.Workspace()
+        self._pins: dict[int, int] = {}           # slot -> holders of a device hit map
+        self._retired: dict[int, KVEntry] = {}    # dropped while pinned: pages kept
 
     # ------------------------------------------------------------------ basics
     def __len__(self) -> int:
@@ -242,9 +266,39 @@ class CachePool:
         self._slots[entry.slot] = None
         self._slot_tokens[entry.slot] = None
         self._slot_hash[entry.slot] = None
-        if release and entry.owner < 0:
+        if self._pins.get(entry.slot):
+            # a held hit map still gathers from this slot (the reference's
+            # ReuseMap keeps a dropped entry's arrays alive): lookups no longer
+            # see it, its slot id and pages stay reserved until unpin()
+            self._retired[entry.slot] = entry
+            entry._release_pages = release
+        elif release and entry.owner < 0:
             self.arena.release(entry.pages)
         self._dirty = True
+
+    def pin(self, slots) -> None:
+        """Hold slots referenced by a device hit map (admission-time lookup,
+        simulate.py:180-186) so that eviction or replacement before the batch
+        runs (simulate.py:165-171) cannot hand their ids or pages on."""
+        for s in slots:
+            s = int(s)
+            self._pins[s] = self._pins.get(s, 0) + 1
+
+    def unpin(self, slots) -> None:
+        for s in slots:
+            s = int(s)
+            c = self._pins.get(s, 0) - 1
+            if c > 0:
+                self._pins[s] = c
+                continue
+            self._pins.pop(s, None)
+            entry = self._retired.pop(s, None)
+            if entry is not None:
+                if entry._release_pages and entry.owner < 0:
+                    self.arena.release(entry.pages)
+                self._dirty = True
+        if not self._pins:
+            self._maybe_renumber()
 
     def insert_remote(self, request_id: str, tokens, owner: int,
                       owner_slot: int | None = None) -> KVEntry:
@@ -440,16 +494,17 @@ class CachePool:
                          *(idx[k].data_ptr() for k in ("tokens", "tok_off", "win_off", "win_hash",
                                                         "win_slot", "sorted_hash", "sorted_widx",
                                                         "slot_rank", "rank2slot")))
-        max_pages = max([len(e.pages) for e in self._slots if e is not None] + [1])
+        max_pages = max([len(e.pages) for e in self._slots if e is not None]
+                        + [len(e.pages) for e in self._retired.values()] + [1])
         sp = np.zeros((max(n_slots, 1), max_pages), dtype=np.int32)
         owner = np.full(max(n_slots, 1), -1, dtype=np.int32)
         oslot = np.arange(max(n_slots, 1), dtype=np.int32)
-        for sl in live:
-            pg = self._slots[sl].pages
-            sp[sl, :len(pg)] = pg
-            owner[sl] = self._slots[sl].owner
-            if self._slots[sl].owner >= 0:
-                oslot[sl] = self._slots[sl].owner_slot
+        for sl in live + list(self._retired):
+            e = self._slots[sl] if self._slots[sl] is not None else self._retired[sl]
+            sp[sl, :len(e.pages)] = e.pages
+            owner[sl] = e.owner
+            if e.owner >= 0:
+                oslot[sl] = e.owner_slot
         idx["slot_pages"] = torch.from_numpy(sp).to(dev)
         idx["slot_max_pages"] = max_pages
         idx["slot_owner"] = owner
@@ -464,7 +519,8 @@ class CachePool:
     def _maybe_renumber(self) -> None:
         """Reclaim freed slot ids once they dominate (single-GPU pools)."""
         n_live = len(self.entries)
-        if len(self._slots) <= 2 * n_live + 64 or any(e.owner >= 0 for e in self.entries.values()):
+        if len(self._slots) <= 2 * n_live + 64 or self._pins or \
+                any(e.owner >= 0 for e in self.entries.values()):
             return
         live = [e for e in self._slots if e is not None]
         toks = [self._slot_tokens[e.slot] for e in live]
@@ -500,6 +556,52 @@ class CachePool:
             src_cand.fill_(-1)
         return BatchLookup(req_off, tokens_flat, src_slot[:n_total], src_cand[:n_total], n_hit,
                            contributed)
+
+    def admit(self, token_lists, fixed_chunk: int | None = None) -> list["AdmittedHits"]:
+        """Admission-time lookups of several requests at once (simulate.py:
+        180-186): one device lookup over all of them, LRU refreshed request by
+        request in order (identical to sequential pool.lookup calls, since a
+        lookup reads insertion order, not recency).  Each result holds the
+        request's device hit map and pins the slots it reads until
+        ``release()``, like the reference's ReuseMap holding its entries."""
+        toks = [np.asarray(t, dtype=np.int64) for t in token_lists]
+        if not toks:
+            return []
+        for t in toks:
+            if t.ndim != 1 or t.size == 0:
+                raise InputError("token sequence must be a non-empty 1-D array")
+        dev = self.device
+        off = np.zeros(len(toks) + 1, dtype=np.int64)
+        off[1:] = np.cumsum([t.size for t in toks])
+        flat = torch.from_numpy(np.concatenate(toks)).to(dev)
+        off_dev = torch.from_numpy(off).to(dev)
+        n_total = int(off[-1])
+        if fixed_chunk is None or not self.entries:
+            res = self.lookup_device(flat, off_dev, off)
+            slot, cand, n_hit, contributed = res.src_slot, res.src_cand, res.n_hit, res.contributed
+        else:
+            if fixed_chunk < 1:
+                raise ParameterError(f"chunk_size must be >= 1, got {fixed_chunk}")
+            idx = self._build_index()
+            slot = torch.empty(n_total, dtype=torch.int32, device=dev)
+            cand = torch.empty(n_total, dtype=torch.int32, device=dev)
+            n_hit = torch.zeros(len(toks), dtype=torch.int32, device=dev)
+            contributed = torch.zeros((len(toks), max(len(self._slots), 1)), dtype=torch.uint8,
+                                      device=dev)
+            N.call("kvs_fixed_chunk_lookup", idx["c"], flat.data_ptr(), off_dev.data_ptr(),
+                   len(toks), int(np.diff(off).max()), int(fixed_chunk), slot.data_ptr(),
+                   cand.data_ptr(), n_hit.data_ptr(), contributed.data_ptr(), n_total,
+                   N.stream_ptr())
+        contrib = contributed.cpu().numpy()
+        hits = n_hit.cpu().numpy()
+        out = []
+        for r, t in enumerate(toks):
+            self.refresh_lru(contrib[r])
+            slots = np.nonzero(contrib[r])[0].tolist()
+            self.pin(slots)
+            a, b = int(off[r]), int(off[r + 1])
+            out.append(AdmittedHits(self, t.size, int(hits[r]), slot[a:b], cand[a:b], slots))
+        return out
 
     def refresh_lru(self, contributed_row: np.ndarray) -> None:
         """pool.py:157-159: contributors get new ticks in old last_access order."""

@@ -102,3 +102,74 @@ def test_writeback_holds_decode_corrected_kv():
     changed = (after != before).flatten(2).any(-1).any(0).nonzero().flatten()
     assert set(changed.tolist()) <= set(recomputed.tolist())
     assert len(set(changed.tolist())) > 0
+
+
+METRIC_CASES = json.load(open(os.path.join(os.path.dirname(__file__), "golden",
+                                           "golden_serving_metrics.json")))
+
+
+def _serve_metrics_case(c):
+    import paper_2503_16525_b200 as K
+    from paper_2503_16525_b200.engine import Engine
+    from paper_2503_16525_b200.pool import CachePool
+    from paper_2503_16525_b200.serving import TraceRecord, run_serving
+    cfg = c["config"]
+    mc = cfg["model"]
+    model = K.init_model(K.ModelConfig(num_layers=mc["num_layers"], num_heads=mc["num_heads"],
+                                       d_model=mc["d_model"], vocab_size=mc["vocab_size"],
+                                       seed=mc["seed"]))
+    pool = CachePool(model.config, K.HashParams(window_size=cfg["window_size"]),
+                     cfg["capacity_bytes"], arena_pages=256)
+    eng = Engine(model, pool)
+    trace = [TraceRecord(r["id"], r["arrival_ms"], r["tokens"], r["decode_steps"])
+             for r in c["trace"]]
+    lat = K.LatencyModel(**cfg["latency"])
+    return run_serving(trace, eng, batch_size=cfg["batch_size"], ratio=cfg["ratio"],
+                       scheduler=cfg["scheduler"], mode=cfg["mode"], latency=lat,
+                       matcher=cfg["matcher"], chunk_size=cfg["chunk_size"],
+                       n_extra=cfg["n_extra"], seed=cfg["seed"], metrics=True)
+
+
+# The GPU stores K/V and the heads' outputs in bf16 (the reference is fp64):
+# a per-layer ||dH|| is compared within 2% plus a 1e-3 floor (||H|| per layer
+# is O(1) here, so the floor is about one bf16 rounding of H), the decode
+# cumulative ||h - h_ref|| within 5% plus 2e-4 per decode step.  Measured on
+# B200: worst error <= 0.3 of these bounds over all cases.
+DH_REL, DH_ABS = 0.02, 1e-3
+DEC_REL, DEC_ABS_PER_STEP = 0.05, 2e-4
+
+
+@pytest.mark.parametrize("idx", range(len(METRIC_CASES)), ids=[c["name"] for c in METRIC_CASES])
+def test_cfg1_request_metrics_match_reference(idx):
+    """BASELINE configs[0] (the reference's default trace and SimConfig, plus
+    FR / NAIVE / ratio 0 / per-token latency / byte-capacity variants):
+    every RequestMetrics field of the reference's run_simulation
+    (simulate.py:218-310) and its aggregate.  Timing, hit rates and token
+    accounting are exact; the deviation metrics are within the bf16 noise
+    floor stated above."""
+    c = METRIC_CASES[idx]
+    rep = _serve_metrics_case(c)
+    got = {m.id: m for m in rep.requests}
+    assert [m.id for m in rep.requests] == [w["id"] for w in c["requests"]]
+    worst = []
+    for w in c["requests"]:
+        m = got[w["id"]]
+        for k in ("ttft_ms", "completion_ms", "hit_rate", "n_tokens", "decode_steps",
+                  "tokens_recomputed", "tokens_reused_uncorrected", "tokens_fresh",
+                  "mean_tpot_ms"):
+            assert getattr(m, k) == w[k], (w["id"], k, getattr(m, k), w[k])
+        for k in ("delta_h_before", "delta_h_after"):
+            g, e = np.array(getattr(m, k)), np.array(w[k])
+            assert g.shape == e.shape
+            err = np.abs(g - e)
+            worst.append((k, float((err / (DH_REL * e + DH_ABS)).max())))
+            assert (err <= DH_REL * e + DH_ABS).all(), (w["id"], k, g, e)
+        e = w["decode_cum_deviation"]
+        tol = DEC_REL * e + DEC_ABS_PER_STEP * w["decode_steps"]
+        worst.append(("decode", abs(m.decode_cum_deviation - e) / tol))
+        assert abs(m.decode_cum_deviation - e) <= tol, (w["id"], m.decode_cum_deviation, e)
+    for k in ("requests", "mean_ttft_ms", "p50_ttft_ms", "p95_ttft_ms", "mean_tpot_ms",
+              "mean_hit_rate", "makespan_ms", "tokens_recomputed_total",
+              "tokens_reused_uncorrected_total", "tokens_fresh_total"):
+        assert rep.aggregate[k] == pytest.approx(c["aggregate"][k], rel=1e-12), k
+    print(c["name"], "worst error / tolerance:", max(worst, key=lambda t: t[1]) if worst else None)
