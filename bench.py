@@ -52,11 +52,15 @@ def parse():
                     help="model shape (BASELINE configs[1] = llama; qwen / yi = configs[2], [3])")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no e2e/cpu legs)")
     ap.add_argument("--mode", default="selective", choices=["selective", "full", "naive"])
+    ap.add_argument("--decode-steps", type=int, default=None,
+                    help="decode leg token steps (default 8; 128 for --shape qwen, SURVEY 8d cfg3)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo stages the remote-row exchange through the host (1-GPU test)")
     args = ap.parse_args()
     if args.layers is None:
         args.layers = {"llama": 32, "qwen": 28, "yi": 48}[args.shape]
+    if args.decode_steps is None:
+        args.decode_steps = 128 if args.shape == "qwen" else 8
     return args
 
 
@@ -512,7 +516,7 @@ def run_gpu(args, rank, world, device):
     res["e2e_ms"] = float(te.item())
     res["h2d_bytes"] = args.batch * args.seq * 8
     res["d2h_bytes"] = args.batch * cfg.d_model * 4
-    res["decode"] = decode_leg(args, eng, batches[args.warmup], cfg)
+    res["decode"] = decode_leg(args, eng, batches[args.warmup], cfg, args.decode_steps + 1)
     res["full_recompute_ms"] = full_recompute_leg(args, eng, batches, dev_tokens)
     return res
 
@@ -570,8 +574,17 @@ def decode_leg(args, eng, batch, cfg, n_tokens: int = 8):
     d3_bytes = float((ctx * G * d * 2 + 4 * lens + lens / 8 + 12).sum()) / max(len(d3), 1)
     d3_ms = float(np.mean(d3)) if d3 else float("nan")
     eng.release(st)
-    return {"tokens_per_step": len(batch), "ms_per_token_step": ms,
+    # HBM floor of a token step: every layer's weights once, every request's
+    # K/V at every layer once (the chosen rows' recompute reads the same
+    # cache), the probe layer's K once more for D3
+    m = eng.model
+    w_bytes = sum(w.numel() * w.element_size() for w in list(m.w_qkv) + list(m.w_o))
+    kv_bytes = float(ctx.sum()) / steps * cfg.num_layers * 2 * G * d * 2
+    floor_ms = (w_bytes + kv_bytes + d3_bytes) / (peaks()[0] * 1e9) * 1e3
+    return {"tokens_per_step": len(batch), "steps": steps, "ms_per_token_step": ms,
             "tok_s": len(batch) / (ms / 1000.0), "n_extra": 3,
+            "context": [int(x) for x in ctx0],
+            "hbm_floor_ms_per_token_step": floor_ms, "floor_over_measured": floor_ms / ms,
             "dhd_decode_select": {"bound": "hbm", "ms_per_call": d3_ms,
                                   "algorithmic_bytes": d3_bytes,
                                   "achieved": d3_bytes / (d3_ms / 1000.0) / 1e9, "unit": "GB/s"}}

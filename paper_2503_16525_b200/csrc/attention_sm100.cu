@@ -67,7 +67,7 @@ struct Params {
 __device__ __forceinline__ uint32_t align1024(uint32_t a) { return (a + 1023u) & ~1023u; }
 
 template <bool kPV>
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, kPV ? 1 : 2)
     fwd_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
                Params p) {
     extern __shared__ uint8_t dsmem[];
@@ -883,13 +883,12 @@ struct ColParams {
     float *alpha_part;                  // [n_total][kv_heads]
 };
 
-__global__ void __launch_bounds__(kThreads, 1)
+__global__ void __launch_bounds__(kThreads, 2)
     colsum_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
                   ColParams p) {
     extern __shared__ uint8_t dsmem[];
     __shared__ Smem sh;
     __shared__ float s_lse[2][BM];
-    __shared__ int32_t s_qn[2];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     // key tiles fastest: the CTAs of one kv group sweep a few requests at a
     // time, so those requests' query tiles are re-read from L2, not DRAM
@@ -980,14 +979,21 @@ __global__ void __launch_bounds__(kThreads, 1)
         const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
         float acc = 0.f;
         float s[BN];
+        // the query LSEs of iteration it+1 are loaded while iteration it
+        // computes (a load issued right before the barrier below would expose
+        // its L2 latency on every iteration)
+        auto lse_of = [&](int it) {
+            const int hh = it / n_qt, qt = q_first + it % n_qt;
+            const int qrow = qt * BM + i;
+            return qrow < n ? __ldg(p.lse + (s0 + qrow) * p.num_heads + g * hq + hh) : INFINITY;
+        };
+        float lse_next = n_it > 0 ? lse_of(0) : 0.f;
         for (int it = 0; it < n_it; ++it) {
             const int b = it & 1;
-            const int hh = it / n_qt, qt = q_first + it % n_qt;
-            const int h = g * hq + hh;
+            const int qt = q_first + it % n_qt;
             // stage this iteration's query LSEs (log2 units) in shared memory
-            const int qrow = qt * BM + i;
-            s_lse[b][i] = qrow < n ? p.lse[(s0 + qrow) * p.num_heads + h] * 1.4426950408889634f
-                                   : INFINITY;
+            s_lse[b][i] = lse_next * 1.4426950408889634f;
+            if (it + 1 < n_it) lse_next = lse_of(it + 1);
             asm volatile("bar.sync 1, 128;" ::: "memory");
             mbar_wait(&sh.s_full[b], (uint32_t)(it >> 1) & 1u);
             tc_fence_after();
