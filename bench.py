@@ -318,7 +318,7 @@ def build_engine(args, device, rank=0, world=1):
                   "yi": K.YI15_9B}[getattr(args, "shape", "llama")])
     if getattr(args, "layers", None):
         shape["num_layers"] = args.layers
-    cfg = K.ModelConfig(**shape, seed=0, max_positions=max(8192, args.seq + 64))
+    cfg = K.ModelConfig(**shape, seed=0, max_positions=max(8192, args.seq + (args.decode_steps or 8) + 256))
     model = K.ToyModel(cfg, device=device, init="device")
     src_pages = args.sources * ((args.seq + 63) // 64)
     # a rank's share of a partitioned batch can exceed B by the balance slack
@@ -543,37 +543,50 @@ def decode_leg(args, eng, batch, cfg, n_tokens: int = 8):
     request's new token, D3 (kvs_dhd_decode_select: unmasked softmax over the
     whole context at the probe layer x prefill dv-L1, top n_extra over the
     still-stale rows), and one layer-batched pass over chosen U {new} rows.
-    Device time per token step with CUDA events; D3's HBM roofline from its
-    own events.  Not part of the headline metric (a prefill throughput)."""
+    The step is timed twice on twin prefills of the batch: launched from
+    Python (eager) and replayed as one CUDA graph (Engine.decode_graph, the
+    serving path).  Device time per token step with CUDA events; D3's HBM
+    roofline from its own events in the eager run.  Not part of the headline
+    metric (a prefill throughput)."""
     import torch
     rng = np.random.default_rng(5)
-    st = eng.prefill_batch(batch, ratio=args.ratio, decode_capacity=n_tokens + 1)
     toks = torch.from_numpy(rng.integers(0, cfg.vocab_size, (n_tokens, len(batch)))).to(
         torch.int64).cuda()
-    eng.decode_step_device(st, toks[0], 3)                      # warm-up step
-    torch.cuda.synchronize()
-    timers = {}
-    eng.reset_timer_events(reserve=8 * n_tokens)
-    eng.timers = timers
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ctx0 = st.ctx_len.copy()
-    e0.record()
-    for t in range(1, n_tokens):                                # no host round trip per token
-        eng.decode_step_device(st, toks[t], 3)
-    e1.record()
-    torch.cuda.synchronize()
-    eng.timers = None
     steps = n_tokens - 1
-    ms = e0.elapsed_time(e1) / steps
+
+    def run(graph: bool):
+        st = eng.prefill_batch(batch, ratio=args.ratio, decode_capacity=n_tokens + 1)
+        eng.decode_step_device(st, toks[0], 3)                  # warm-up step (eager)
+        g = eng.decode_graph(st, 3) if graph else None
+        torch.cuda.synchronize()
+        timers = {}
+        if not graph:
+            eng.reset_timer_events(reserve=8 * n_tokens)
+            eng.timers = timers
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ctx0 = st.ctx_len.copy()
+        e0.record()
+        for t in range(1, n_tokens):                            # no host round trip per token
+            if graph:
+                g.replay(toks[t])
+            else:
+                eng.decode_step_device(st, toks[t], 3)
+        e1.record()
+        torch.cuda.synchronize()
+        eng.timers = None
+        lens = np.asarray(st.lengths)
+        eng.release(st)
+        return e0.elapsed_time(e1) / steps, timers, ctx0, lens
+
+    ms_eager, timers, ctx0, lens = run(False)
+    ms, _, _, _ = run(True)
     d3 = [a.elapsed_time(b) for a, b in timers.get("dhd_decode", [])]
     G, d = cfg.kv_heads, 128
     # SURVEY 8d D3 bytes per request-step: K at the probe layer over the context,
     # dv-L1 and eligibility of the prefill rows, the chosen indices
     ctx = ctx0 + np.arange(steps)[:, None]                       # context per step, request
-    lens = np.asarray(st.lengths)
     d3_bytes = float((ctx * G * d * 2 + 4 * lens + lens / 8 + 12).sum()) / max(len(d3), 1)
     d3_ms = float(np.mean(d3)) if d3 else float("nan")
-    eng.release(st)
     # HBM floor of a token step: every layer's weights once, every request's
     # K/V at every layer once (the chosen rows' recompute reads the same
     # cache), the probe layer's K once more for D3
@@ -582,6 +595,7 @@ def decode_leg(args, eng, batch, cfg, n_tokens: int = 8):
     kv_bytes = float(ctx.sum()) / steps * cfg.num_layers * 2 * G * d * 2
     floor_ms = (w_bytes + kv_bytes + d3_bytes) / (peaks()[0] * 1e9) * 1e3
     return {"tokens_per_step": len(batch), "steps": steps, "ms_per_token_step": ms,
+            "ms_per_token_step_eager": ms_eager, "launch": "one CUDA graph per token step",
             "tok_s": len(batch) / (ms / 1000.0), "n_extra": 3,
             "context": [int(x) for x in ctx0],
             "hbm_floor_ms_per_token_step": floor_ms, "floor_over_measured": floor_ms / ms,

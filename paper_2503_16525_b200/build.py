@@ -22,6 +22,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "--expt-relaxed-constexpr", "-diag-suppress", "177",
          "-I" + os.path.join(ROOT, "include")]
 SOURCES = ["capi.cu", "retriever.cu", "gather.cu", "dhd.cu", "attention_sm100.cu", "baselines.cu",
+           "decode_attn.cu",
            "decode_dhd.cu"]
 
 

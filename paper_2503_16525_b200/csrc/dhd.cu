@@ -1060,175 +1060,8 @@ __global__ void __launch_bounds__(1024) decode_select_kernel(
     }
 }
 
-// ---------------------------------------------------------------- decode attention
-// Few-row attention for decode steps (engine.py:104-109 _token_rows): grid
-// (row, kv head, split), 4 warps; every warp walks 32-key tiles.  Logits: lane
-// i owns key i of the tile and computes its dot products with the HQ query
-// heads of the group (q in shared memory, fp32).  A tile's softmax statistics
-// take two warp reductions per head; P.V then broadcasts each key's weight
-// and the lane accumulates its 4 output dims from the V row (coalesced 8-byte
-// loads).  All loops over heads/dims are compile-time (HQ, D = 128), so the
-// per-head state stays in registers.
-constexpr int kMaxGroup = 8;
-
-template <int HQ>
-__global__ void __launch_bounds__(128) decode_attn_partial_kernel(
-    const __nv_bfloat16 *__restrict__ q, const int32_t *__restrict__ row_req,
-    const int32_t *__restrict__ row_pos, int32_t H, const int32_t *__restrict__ kv_len,
-    int32_t causal, int32_t layer, ArenaC A, const int32_t *__restrict__ block_table,
-    int32_t max_pages, float scale_log2, int32_t n_splits, float *__restrict__ ws) {
-    constexpr int D = 128;
-    const int row = blockIdx.x, g = blockIdx.y, split = blockIdx.z;
-    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    __shared__ __align__(16) float sq[HQ][D];
-    for (int i = threadIdx.x; i < HQ * D; i += blockDim.x)
-        sq[i / D][i % D] = bf2f(q[((int64_t)row * H + g * HQ + i / D) * D + i % D]);
-    __syncthreads();
-    const int r = row_req[row];
-    const int kend = causal ? row_pos[row] + 1 : kv_len[r];
-    const int span = (((kend + n_splits - 1) / n_splits) + 31) & ~31;
-    const int kb = split * span, ke = min(kend, kb + span);
-    float m[HQ], l[HQ], acc[HQ][4];
-#pragma unroll
-    for (int hh = 0; hh < HQ; ++hh) {
-        m[hh] = -INFINITY;
-        l[hh] = 0.f;
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[hh][e] = 0.f;
-    }
-    const int64_t row_elems = (int64_t)A.G * D;
-    for (int t0 = kb + wid * 32; t0 < ke; t0 += 4 * 32) {
-        // a 32-key tile lies in one page (tiles start at multiples of 32):
-        // one page lookup, then every K and V load of the tile in flight
-        const int k = t0 + lane;
-        const bool live = k < ke;
-        const int nkeys = min(32, ke - t0);
-        const int64_t page = block_table[(int64_t)r * max_pages + t0 / A.P];
-        const __nv_bfloat16 *kbase = A.row(page, layer, 0, t0 % A.P) + g * D;
-        const __nv_bfloat16 *vbase = A.row(page, layer, 1, t0 % A.P) + g * D;
-        uint4 kx[D / 8];
-        uint2 vx[32];
-        if (live) {
-            const uint4 *kr = reinterpret_cast<const uint4 *>(kbase + lane * row_elems);
-#pragma unroll
-            for (int c = 0; c < D / 8; ++c) kx[c] = __ldg(kr + c);
-        }
-#pragma unroll
-        for (int j = 0; j < 32; ++j)
-            if (j < nkeys)
-                vx[j] = __ldg(reinterpret_cast<const uint2 *>(vbase + j * row_elems) + lane);
-        // logits of this lane's key for the group's query heads
-        float p[HQ];
-#pragma unroll
-        for (int hh = 0; hh < HQ; ++hh) p[hh] = 0.f;
-        if (live) {
-#pragma unroll
-            for (int c = 0; c < D / 8; ++c) {
-                const __nv_bfloat162 *h2 = reinterpret_cast<const __nv_bfloat162 *>(&kx[c]);
-                float kf[8];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const float2 f = __bfloat1622float2(h2[u]);
-                    kf[2 * u] = f.x;
-                    kf[2 * u + 1] = f.y;
-                }
-#pragma unroll
-                for (int hh = 0; hh < HQ; ++hh) {
-                    const float4 qa = *reinterpret_cast<const float4 *>(&sq[hh][8 * c]);
-                    const float4 qb = *reinterpret_cast<const float4 *>(&sq[hh][8 * c + 4]);
-                    p[hh] += kf[0] * qa.x + kf[1] * qa.y + kf[2] * qa.z + kf[3] * qa.w +
-                             kf[4] * qb.x + kf[5] * qb.y + kf[6] * qb.z + kf[7] * qb.w;
-                }
-            }
-        }
-#pragma unroll
-        for (int hh = 0; hh < HQ; ++hh) {
-            const float x = live ? p[hh] * scale_log2 : -INFINITY;
-            const float mt = fmaxf(m[hh], warp_max(x));
-            const float c = fast_exp2(m[hh] - mt);
-            p[hh] = live ? fast_exp2(x - mt) : 0.f;
-            l[hh] = l[hh] * c + warp_sum(p[hh]);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) acc[hh][e] *= c;
-            m[hh] = mt;
-        }
-        // P.V: weights broadcast key by key, lane accumulates dims 4*lane..+4
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-            if (j >= nkeys) break;
-            const __nv_bfloat162 *v2 = reinterpret_cast<const __nv_bfloat162 *>(&vx[j]);
-            const float2 va = __bfloat1622float2(v2[0]), vb = __bfloat1622float2(v2[1]);
-#pragma unroll
-            for (int hh = 0; hh < HQ; ++hh) {
-                const float w = __shfl_sync(0xffffffffu, p[hh], j);
-                acc[hh][0] += w * va.x;
-                acc[hh][1] += w * va.y;
-                acc[hh][2] += w * vb.x;
-                acc[hh][3] += w * vb.y;
-            }
-        }
-    }
-    // combine the 4 warps through shared memory
-    __shared__ float sm_m[4][HQ], sm_l[4][HQ];
-    __shared__ __align__(16) float sm_acc[4][HQ][D];
-    if (lane == 0) {
-#pragma unroll
-        for (int hh = 0; hh < HQ; ++hh) { sm_m[wid][hh] = m[hh]; sm_l[wid][hh] = l[hh]; }
-    }
-#pragma unroll
-    for (int hh = 0; hh < HQ; ++hh)
-        *reinterpret_cast<float4 *>(&sm_acc[wid][hh][4 * lane]) =
-            make_float4(acc[hh][0], acc[hh][1], acc[hh][2], acc[hh][3]);
-    __syncthreads();
-    // ws layout per (row, head, split): [m, l, acc[D]]
-    for (int idx = threadIdx.x; idx < HQ * D; idx += blockDim.x) {
-        const int hh = idx / D, d = idx % D;
-        float M = -INFINITY;
-#pragma unroll
-        for (int w = 0; w < 4; ++w) M = fmaxf(M, sm_m[w][hh]);
-        float L = 0.f, S = 0.f;
-#pragma unroll
-        for (int w = 0; w < 4; ++w) {
-            if (sm_m[w][hh] == -INFINITY) continue;
-            const float c = fast_exp2(sm_m[w][hh] - M);
-            L += sm_l[w][hh] * c;
-            S += sm_acc[w][hh][d] * c;
-        }
-        float *o = ws + (((int64_t)row * H + g * HQ + hh) * n_splits + split) * (D + 2);
-        if (d == 0) { o[0] = M; o[1] = L; }
-        o[2 + d] = S;
-    }
-}
-
-__global__ void decode_attn_combine_kernel(const float *__restrict__ ws, int32_t H, int32_t D,
-                                           int32_t n_splits, __nv_bfloat16 *__restrict__ out) {
-    const int row = blockIdx.x, h = blockIdx.y;
-    const float *base = ws + ((int64_t)row * H + h) * n_splits * (D + 2);
-    float M = -INFINITY;
-    for (int sp = 0; sp < n_splits; ++sp) M = fmaxf(M, base[sp * (D + 2)]);
-    for (int d = threadIdx.x; d < D; d += blockDim.x) {
-        float L = 0.f, S = 0.f;
-        for (int sp = 0; sp < n_splits; ++sp) {
-            const float *o = base + sp * (D + 2);
-            if (o[0] == -INFINITY) continue;
-            const float c = fast_exp2(o[0] - M);
-            L += o[1] * c;
-            S += o[2 + d] * c;
-        }
-        out[((int64_t)row * H + h) * D + d] = f2bf(L > 0.f ? S / L : 0.f);
-    }
-}
-
 static inline size_t align256(size_t x) { return (x + 255) & ~(size_t)255; }
 
-static int decode_splits(int64_t n_rows, int G, int max_kv) {
-    int64_t want = (8 * kNumSMs + n_rows * G - 1) / (n_rows * G);
-    int64_t cap = (max_kv + 127) / 128;
-    if (want > cap) want = cap;
-    if (want < 1) want = 1;
-    if (want > 64) want = 64;
-    return (int)want;
-}
 
 }  // namespace kvs
 
@@ -1362,53 +1195,6 @@ kvs_status kvs_dhd_decode_select(const void *q_t, int32_t num_heads, const int32
         num_heads, ctx_len, max_ctx, logits, part, dv_l1, eligible, batch->req_off, n_extra,
         chosen, n_chosen, scores);
     KVS_CHECK_LAUNCH("kvs_dhd_decode_select");
-    return KVS_OK;
-}
-
-size_t kvs_decode_attention_workspace(int64_t n_rows, int32_t num_heads, int32_t kv_heads,
-                                      int32_t head_dim, int32_t max_kv) {
-    const int splits = decode_splits(n_rows, kv_heads, max_kv);
-    return sizeof(float) * (size_t)n_rows * num_heads * splits * (head_dim + 2);
-}
-
-kvs_status kvs_decode_attention(const void *q, const int32_t *row_req, const int32_t *row_pos,
-                                int64_t n_rows, int32_t num_heads, const int32_t *kv_len,
-                                int32_t causal, int32_t layer, const kvs_kv_arena *arena,
-                                const kvs_batch *batch, float softmax_scale, void *out, void *ws,
-                                size_t ws_bytes, kvs_stream_t stream) {
-    KVS_REQUIRE(arena && batch, KVS_EPARAM, "null arena/batch");
-    const int G = arena->kv_heads, D = arena->head_dim;
-    KVS_REQUIRE(num_heads % G == 0 && num_heads / G <= kMaxGroup, KVS_ESHAPE,
-                "num_heads / kv_heads must be <= 8");
-    KVS_REQUIRE(D == 128, KVS_ESHAPE, "decode attention needs head_dim == 128 (padded heads)");
-    if (n_rows <= 0) return KVS_OK;
-    int max_kv = 0;
-    for (int64_t k = 0; k < (int64_t)batch->max_pages; ++k) max_kv += arena->page_size;
-    const int splits = decode_splits(n_rows, G, max_kv);
-    KVS_REQUIRE(ws_bytes >= sizeof(float) * (size_t)n_rows * num_heads * splits * (D + 2),
-                KVS_EPARAM, "workspace too small");
-    cudaStream_t s = (cudaStream_t)stream;
-    const float scale_log2 = softmax_scale * 1.4426950408889634f;
-    const dim3 grid((unsigned)n_rows, G, splits);
-    const int hq = num_heads / G;
-#define KVS_DECODE_ATTN(HQ)                                                                    \
-    decode_attn_partial_kernel<HQ><<<grid, 128, 0, s>>>(                                      \
-        (const __nv_bfloat16 *)q, row_req, row_pos, num_heads, kv_len, causal, layer,          \
-        arena_c(arena), batch->block_table, batch->max_pages, scale_log2, splits, (float *)ws)
-    switch (hq) {
-        case 1: KVS_DECODE_ATTN(1); break;
-        case 2: KVS_DECODE_ATTN(2); break;
-        case 3: KVS_DECODE_ATTN(3); break;
-        case 4: KVS_DECODE_ATTN(4); break;
-        case 5: KVS_DECODE_ATTN(5); break;
-        case 6: KVS_DECODE_ATTN(6); break;
-        case 7: KVS_DECODE_ATTN(7); break;
-        default: KVS_DECODE_ATTN(8); break;
-    }
-#undef KVS_DECODE_ATTN
-    decode_attn_combine_kernel<<<dim3((unsigned)n_rows, num_heads), 128, 0, s>>>(
-        (const float *)ws, num_heads, D, splits, (__nv_bfloat16 *)out);
-    KVS_CHECK_LAUNCH("kvs_decode_attention");
     return KVS_OK;
 }
 

@@ -727,7 +727,9 @@ class Engine:
         clears the chosen rows from st.eligible.  No host synchronisation."""
         cfg, dev, R = self.cfg, self.device, len(st.lengths)
         ctx = self._ctx_dev(st)
-        max_ctx = int(st.ctx_len.max())
+        # workspace and logits stride sized by the capacity, not the current
+        # context: the same launch is valid at every step (CUDA-graph replay)
+        max_ctx = int(st.capacity.max())
         chosen = torch.empty(R, max(n_extra, 1), dtype=torch.int32, device=dev)
         nch = torch.zeros(R, dtype=torch.int32, device=dev)
         ws = self._ws["dsel"].get(N.ws_bytes("kvs_dhd_decode_select_workspace", R, cfg.num_heads,
@@ -779,9 +781,20 @@ class Engine:
         x = self._embed(tok, rows)
         x = self.forward_rows(x, rows, range(self.cfg.num_layers), self.arena.c, st.batch_c,
                               decode=True, max_kv=int(st.capacity.max()))
-        st.ctx_len = st.ctx_len + 1
-        st._decoded = getattr(st, "_decoded", []) + [new_tokens]
+        ctx.add_(1)                        # the device context counter moves with the host one
+        self._advance_ctx_host(st, new_tokens)
         return x.view(R, E + 1, -1)[:, E], chosen, nch
+
+    @staticmethod
+    def _advance_ctx_host(st: BatchState, new_tokens) -> None:
+        st.ctx_len = st.ctx_len + 1
+        st._ctx_key = st.ctx_len.tobytes()
+        st._decoded = getattr(st, "_decoded", []) + [new_tokens]
+
+    def decode_graph(self, st: BatchState, n_extra: int) -> "DecodeGraph":
+        """decode_step_device captured once as a CUDA graph for this batch
+        (about 140 launches per token step replayed without host work)."""
+        return DecodeGraph(self, st, n_extra)
 
     def decode_step(self, st: BatchState, new_tokens, n_extra: int):
         """decode_step_device for host tokens, choices returned as host lists
@@ -802,3 +815,60 @@ class Engine:
             toks = flat[st.req_off_host[r]:st.req_off_host[r + 1]]
             self.pool.insert_pages(rid, toks, st.pages[r])
         st.pages = []
+
+
+class DecodeGraph:
+    """One decode token step of a batch (Engine.decode_step_device: probe
+    query, D3, chosen U {new} rows through every layer) as a CUDA graph.
+
+    The step's launches only depend on the batch's device state (block
+    table, eligibility, dv-L1, the device context counter it advances itself)
+    and on static shapes, so it is captured once and replayed per token: the
+    host issues one graph launch instead of ~140 kernel launches and the
+    Python around them.  The graph owns its scratch and workspace buffers
+    (the engine's grow-only buffers may be reallocated by later work).
+    replay(new_tokens) returns the same (hidden, chosen, n_chosen) tensors
+    every step - static outputs, overwritten by the next replay."""
+
+    def __init__(self, eng: Engine, st: BatchState, n_extra: int):
+        """Capture after at least one eager decode step of this batch (it
+        initialises cuBLAS for the step's shapes and sizes the engine's
+        buffers, which the graph's private buffers copy)."""
+        self.eng, self.st, self.n_extra = eng, st, int(n_extra)
+        R, dev = len(st.lengths), eng.device
+        if self.n_extra > 0 and st.eligible is not None:
+            eng.ensure_dv(st)                       # host-dependent set-up stays outside
+        eng._ctx_dev(st)
+        self.tok = torch.zeros(R, dtype=torch.int64, device=dev)
+        saved = (eng.scratch, eng._ws, eng.timers)
+        self.scratch = _Scratch(dev)
+        self.scratch.bufs = {k: torch.empty_like(v) for k, v in saved[0].bufs.items()}
+        self.ws = {}
+        for k, w in saved[1].items():
+            self.ws[k] = N.Workspace()
+            if w.buf is not None:
+                self.ws[k].buf = torch.zeros_like(w.buf)
+        ctx_host, key, dec = st.ctx_len.copy(), getattr(st, "_ctx_key", None), \
+            list(getattr(st, "_decoded", []))
+        eng.scratch, eng._ws, eng.timers, eng._xb_of = self.scratch, self.ws, None, None
+        try:
+            torch.cuda.synchronize()
+            # capture records the launches without running them; the host-side
+            # context bookkeeping the captured call did is undone
+            self.graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.graph):
+                self.out = eng.decode_step_device(st, self.tok, self.n_extra)
+            st.ctx_len, st._ctx_key, st._decoded = ctx_host, key, dec
+        finally:
+            eng.scratch, eng._ws, eng.timers = saved
+            eng._xb_of = None
+
+    def replay(self, new_tokens: torch.Tensor):
+        st = self.st
+        if (st.ctx_len + 1 > st.capacity).any():
+            raise InputError("decode capacity exhausted")
+        self.tok.copy_(new_tokens.view(-1), non_blocking=True)
+        self.graph.replay()
+        Engine._advance_ctx_host(st, new_tokens)
+        return self.out
+
