@@ -318,7 +318,7 @@ def build_engine(args, device, rank=0, world=1):
                   "yi": K.YI15_9B}[getattr(args, "shape", "llama")])
     if getattr(args, "layers", None):
         shape["num_layers"] = args.layers
-    cfg = K.ModelConfig(**shape, seed=0, max_positions=max(8192, args.seq + (args.decode_steps or 8) + 256))
+    cfg = K.ModelConfig(**shape, seed=0, max_positions=max(8192, args.seq + (getattr(args, "decode_steps", None) or 8) + 256))
     model = K.ToyModel(cfg, device=device, init="device")
     src_pages = args.sources * ((args.seq + 63) // 64)
     # a rank's share of a partitioned batch can exceed B by the balance slack

@@ -832,8 +832,7 @@ class DecodeGraph:
 
     def __init__(self, eng: Engine, st: BatchState, n_extra: int):
         """Capture after at least one eager decode step of this batch (it
-        initialises cuBLAS for the step's shapes and sizes the engine's
-        buffers, which the graph's private buffers copy)."""
+        initialises cuBLAS for the step's shapes)."""
         self.eng, self.st, self.n_extra = eng, st, int(n_extra)
         R, dev = len(st.lengths), eng.device
         if self.n_extra > 0 and st.eligible is not None:
@@ -841,13 +840,10 @@ class DecodeGraph:
         eng._ctx_dev(st)
         self.tok = torch.zeros(R, dtype=torch.int64, device=dev)
         saved = (eng.scratch, eng._ws, eng.timers)
+        # the graph's own buffers, allocated while capturing (from the graph's
+        # private memory pool), sized for this step only
         self.scratch = _Scratch(dev)
-        self.scratch.bufs = {k: torch.empty_like(v) for k, v in saved[0].bufs.items()}
-        self.ws = {}
-        for k, w in saved[1].items():
-            self.ws[k] = N.Workspace()
-            if w.buf is not None:
-                self.ws[k].buf = torch.zeros_like(w.buf)
+        self.ws = {k: N.Workspace() for k in saved[1]}
         ctx_host, key, dec = st.ctx_len.copy(), getattr(st, "_ctx_key", None), \
             list(getattr(st, "_decoded", []))
         eng.scratch, eng._ws, eng.timers, eng._xb_of = self.scratch, self.ws, None, None

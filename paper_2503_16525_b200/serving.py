@@ -159,15 +159,25 @@ def decode_batch(engine, st, streams, n_extra: int, ref_st=None):
         toks[:len(s), r] = s
     tok_dev = torch.from_numpy(toks).to(dev)
     counts, devs = [], []
+    g = g_ref = None
     for t in range(steps):
         for r, s in enumerate(streams):
             if len(s) == t and n_extra > 0:        # request r has no step t: no more recompute
                 a, b = int(st.req_off_host[r]), int(st.req_off_host[r + 1])
                 st.eligible[a:b] = 0
-        h, _, nch = engine.decode_step_device(st, tok_dev[t], n_extra)
+        if t == 1 and steps > 2:
+            # after one eager step, the rest replay one CUDA graph per token
+            g = engine.decode_graph(st, n_extra)
+            g_ref = engine.decode_graph(ref_st, 0) if ref_st is not None else None
+        if g is not None:
+            h, _, nch = g.replay(tok_dev[t])
+            h, nch = h.clone(), nch.clone()
+        else:
+            h, _, nch = engine.decode_step_device(st, tok_dev[t], n_extra)
         counts.append(nch)
         if ref_st is not None:
-            h_ref, _, _ = engine.decode_step_device(ref_st, tok_dev[t], 0)
+            h_ref = g_ref.replay(tok_dev[t])[0] if g_ref is not None else \
+                engine.decode_step_device(ref_st, tok_dev[t], 0)[0]
             devs.append(torch.linalg.vector_norm(h - h_ref, dim=1))
     return torch.stack(counts), (torch.stack(devs) if ref_st is not None else None)
 

@@ -68,7 +68,16 @@ def _spawn(world, backend="gloo"):
     procs = [ctx.Process(target=_run, args=(r, world, port, q, backend)) for r in range(world)]
     for p in procs:
         p.start()
-    res = [q.get(timeout=600) for _ in range(world)]
+    import queue
+    import time
+    res, t0 = [], time.time()
+    while len(res) < world:                  # fail fast when a rank dies
+        try:
+            res.append(q.get(timeout=5))
+        except queue.Empty:
+            dead = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            assert not dead, f"rank exited with {dead}"
+            assert time.time() - t0 < 600, "ranks did not report"
     for p in procs:
         p.join(timeout=120)
         assert p.exitcode == 0
