@@ -11,11 +11,12 @@
 // 256 B at the probe layer).  One cooperative launch of one CTA per SM:
 //
 // phase 1, streaming.  Work items are (request, 64-key page, kv head): 16 KB
-// of K plus the group's query heads.  A CTA takes pages b, b + grid, ... and
-// deals their kv-head items to its 6 warps; every warp keeps two of its own
-// items in flight (SWIZZLE_128B TMA loads with an L2 evict-first hint, one
-// mbarrier per stage, no producer warp, so no warp waits behind another's
-// stage), the arena pages of its next 32 items fetched in one warp load.
+// of K plus the group's query heads, handed out one at a time from a global
+// ticket to whichever of the CTAs' 6 warps is ready (faster SMs take more).
+// Every warp keeps two of its own items in flight (SWIZZLE_128B TMA loads
+// with an L2 evict-first hint, one mbarrier per stage, no producer warp, so
+// no warp waits behind another's stage); the next ticket and its arena page
+// are fetched one item ahead.
 // Q.K^T runs on the tensor cores (mma.sync m16n8k16 bf16 -> fp32; A = the
 // swizzled K tile through conflict-free ldmatrix, B = the group's <= 8 query
 // heads from the same stage), and the epilogue writes the logits (log2
@@ -519,38 +520,41 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     const int total = sm.item_off[p.n_req];
     const uint32_t qbytes = 2u * (uint32_t)p.HQ * 128u;
-    const int pages = total / p.G;
     // ---------------------------------------------------- phase 1: streaming
-    // the CTA takes pages b, b + grid, ... and deals the kv-head items of its
-    // pages to its warps round-robin (CTA-local item k -> warp k % kWarps);
-    // each warp keeps two of its items in flight (TMA, one mbarrier each)
-    auto item_of = [&](int k) -> int {
-        const int page = blockIdx.x + (k / p.G) * (int)gridDim.x;
-        return page < pages ? page * p.G + k % p.G : -1;
-    };
+    // Items (request, page, kv head) are handed out one at a time from a
+    // global ticket (ctr[0]) to whichever warp is ready, so SMs that stream
+    // slower simply take fewer items (a static page split left the slowest
+    // CTA finishing 20-60 us after the median).  A warp's tickets only grow,
+    // so its request cursors move forward.  Lane 0 keeps the next two
+    // tickets and the arena page of the first, so neither the ticket atomic
+    // nor the block-table load sits in front of a TMA issue.
     const uint64_t pol = l2_evict_first_policy();
-    // request cursors: a warp's items only move forward through the requests
-    int r_iss = 0, r_con = 0;
+    int r_iss = 0, r_con = 0, r_pf = 0;
     auto advance = [&](int &r, int it) {
         while (sm.item_off[r + 1] <= it) ++r;
         return r;
     };
-    // arena pages of the warp's next 32 items, one per lane, fetched together
-    // (the TMA issue path never waits on a block-table load)
-    int pf_base = -32, pf_page = 0, r_pf = 0;
-    auto issue = [&](int jn, int buf) {           // warp-collective; jn = warp-local item
-        if (jn >= pf_base + 32) {
-            pf_base = jn;
-            const int itl = item_of(warp + (jn + lane) * kWarps);
-            if (itl >= 0) {
-                const int rl = advance(r_pf, itl);
-                const int tl = (itl - sm.item_off[rl]) / p.G;
-                pf_page = __ldg(p.block_table + (int64_t)rl * p.max_pages + tl);
-            }
-        }
-        const int page = __shfl_sync(0xffffffffu, pf_page, jn - pf_base);
-        const int it = item_of(warp + jn * kWarps);
-        if (lane != 0 || it < 0) return;
+    auto page_of = [&](int it) -> int {
+        if (it >= total) return 0;
+        const int rl = advance(r_pf, it);
+        return __ldg(p.block_table + (int64_t)rl * p.max_pages + (it - sm.item_off[rl]) / p.G);
+    };
+    int t_a = 0, t_b = 0, pg_a = 0, held[kBuf];
+    if (lane == 0) {
+        t_a = atomicAdd(&p.ctr[0], 1);
+        t_b = atomicAdd(&p.ctr[0], 1);
+        pg_a = page_of(t_a);
+    }
+    auto issue = [&](int buf) {                   // lane 0: the warp's next ticket into buf
+        if (lane != 0) return;
+        const int it = t_a, page = pg_a;
+#pragma unroll
+        for (int q = 0; q < kBuf; ++q)
+            if (q == buf) held[q] = it;
+        t_a = t_b;
+        pg_a = page_of(t_a);
+        t_b = t_a < total ? atomicAdd(&p.ctr[0], 1) : total;
+        if (it >= total) return;
         const int r = advance(r_iss, it);
         const int rel = it - sm.item_off[r];
         const int g = rel % p.G;
@@ -568,12 +572,17 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch(&map_kv);
         tma_prefetch(&map_q);
     }
-    for (int j = 0; j < kBuf; ++j) issue(j, j);
+#pragma unroll
+    for (int j = 0; j < kBuf; ++j) issue(j);
     __syncwarp();
     for (int j = 0;; ++j) {
-        const int k = warp + j * kWarps, buf = j % kBuf;
-        const int it = item_of(k);
-        if (it < 0) break;
+        const int buf = j % kBuf;
+        int mine = 0;
+#pragma unroll
+        for (int q = 0; q < kBuf; ++q)
+            if (q == buf) mine = held[q];
+        const int it = __shfl_sync(0xffffffffu, mine, 0);
+        if (it >= total) break;
         mbar_wait(&sm.full[warp][buf], (j / kBuf) & 1);
         const int r = advance(r_con, it);
         const int rel = it - sm.item_off[r];
@@ -613,7 +622,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
         __syncwarp();
         // the stage is free again: this warp's item two ahead loads under the epilogue
-        issue(j + kBuf, buf);
+        issue(buf);
         // epilogue: key rows 16mt + lane/4 (+8), head columns 2(lane%4) + {0,1}
         const int col = 2 * (lane & 3);
         const int kb = tile * kTileKeys + (lane >> 2);
