@@ -721,15 +721,17 @@ def decode_select_batch_leg(n_req: int, ctx: int = 4096, hit: float = 0.5, ratio
 
 
 def ncu_traffic(kernel: str):
-    """DRAM bytes per launch of `kernel` from the committed ncu capture
-    (profiles/r1_ncu_traffic.json), or None."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "r1_ncu_traffic.json")) as fh:
-            k = json.load(fh)["kernels"][kernel]
-        return {"dram_bytes_per_launch": k["dram_bytes"], "launch": k["launch"],
-                "source": "profiles/r1_ncu_traffic.json"}
-    except (OSError, KeyError, ValueError):
-        return None
+    """DRAM bytes per launch of `kernel` from the newest committed ncu capture
+    (profiles/r2_ncu_traffic.json, else round 1's), or None."""
+    for name in ("r2_ncu_traffic.json", "r1_ncu_traffic.json"):
+        try:
+            with open(os.path.join(ROOT, "profiles", name)) as fh:
+                k = json.load(fh)["kernels"][kernel]
+            return {"dram_bytes_per_launch": k["dram_bytes"], "launch": k["launch"],
+                    "source": f"profiles/{name}"}
+        except (OSError, KeyError, ValueError):
+            continue
+    return None
 
 
 def peaks():
@@ -806,11 +808,14 @@ def main():
     c = res["counts"]
     att_ms = kern.get("attention", float("nan"))
     att_tflops = c["attention_flops"] / (att_ms / 1000.0) / 1e12 if att_ms == att_ms else None
+    # the committed ncu traffic is a capture of the default workload only
+    default_wl = (args.shape, args.seq, args.batch, args.hit) == ("llama", 4096, 8, 0.5)
     roof = {"kernel": "kvs_attention_fwd (A1 selective-recompute attention, tcgen05)",
             "bound": "tensor", "achieved": att_tflops, "peak": tflops_sus, "unit": "TFLOP/s",
             "frac": att_tflops / tflops_sus if att_tflops else None,
-            "traffic": ncu_traffic("kvs_attention_fwd"),
+            "traffic": ncu_traffic("kvs_attention_fwd") if default_wl else None,
             "peak_kind": f"{kind} bf16 sustained (kernel timed inside a long step)",
+            "peak_burst": tflops, "frac_of_burst": att_tflops / tflops if att_tflops else None,
             "ms_per_step": att_ms, "share_of_step": att_ms / ms_per_step,
             "launches_per_step": res["n_launch_attention"]}
     extra = {}
@@ -819,7 +824,7 @@ def main():
         extra["dhd_select"] = {"bound": "hbm", "achieved": gbs, "peak": hbm, "unit": "GB/s",
                                "frac": gbs / hbm, "ms_per_step": kern["dhd_select"],
                                "algorithmic_bytes": c["select_bytes"],
-                               "traffic": ncu_traffic("kvs_dhd_select")}
+                               "traffic": ncu_traffic("kvs_dhd_select") if default_wl else None}
     if "dhd_alpha" in kern:
         tf = c["alpha_flops"] / (kern["dhd_alpha"] / 1000.0) / 1e12
         extra["dhd_alpha"] = {"bound": "tensor", "achieved": tf, "peak": tflops_sus,

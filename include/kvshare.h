@@ -253,7 +253,9 @@ kvs_status kvs_attention_fwd(const void *q, const int32_t *row_pos, int64_t n_ro
 /* Few-row attention (decode steps, probe queries): same semantics as
  * kvs_attention_fwd for arbitrary rows (row_req per row; rows of one request
  * contiguous), split-K flash decoding on mma.sync tiles where a request's rows
- * share every K/V page; num_heads / kv_heads <= 8, page_size 64.          */
+ * share every K/V page; num_heads / kv_heads <= 8, page_size 64.  The
+ * workspace starts with 256 KB of split counters that must be zero when the
+ * buffer is first used; every call leaves them zero again.                */
 size_t kvs_decode_attention_workspace(int64_t n_rows, int32_t num_heads, int32_t kv_heads,
                                       int32_t head_dim, int32_t max_kv);
 kvs_status kvs_decode_attention(const void *q, const int32_t *row_req, const int32_t *row_pos,

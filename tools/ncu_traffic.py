@@ -18,7 +18,7 @@ def raw(rep):
     def val(v, k):
         x = float(v[h.index(k)].replace(",", ""))
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3,
-                 "usecond": 1.0, "msecond": 1e3}
+                 "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3}
         return x * scale.get(u[h.index(k)], 1)
     v = rows[2]
     return {"kernel": v[h.index("Kernel Name")].split("(")[0],
