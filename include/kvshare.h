@@ -201,7 +201,8 @@ kvs_status kvs_entry_export(const kvs_kv_arena *arena, const int32_t *pages, int
 /* Post-GEMM step for a set of query rows: qkv[row] = [q (H*d) | k (kvh*d) | v (kvh*d)]
  * bf16.  Rotates q,k by position (rope nullable), writes q to q_out[row][H][d],
  * writes k,v into the arena at (row_req, row_pos, layer) when write_kv[row]
- * != 0, and optionally dense copies k_out/v_out[row][kvh][d] (nullable).    */
+ * != 0, and optionally dense copies k_out/v_out[row][kvh][d] (nullable).
+ * q_out == NULL skips the query heads (kvs_attention_fwd_qkv rotates them). */
 kvs_status kvs_qkv_rope_scatter(const void *qkv, int64_t n_rows, int32_t num_heads,
                                 const int32_t *row_req, const int32_t *row_pos,
                                 const uint8_t *write_kv, int32_t layer,
@@ -249,6 +250,22 @@ kvs_status kvs_attention_fwd(const void *q, const int32_t *row_pos, int64_t n_ro
                              int32_t n_tiles, const int32_t *kv_len, int32_t causal,
                              int32_t layer, const kvs_kv_arena *arena, const kvs_batch *batch,
                              float softmax_scale, void *out, float *lse, kvs_stream_t stream);
+
+/* kvs_attention_fwd with the query rows read straight from the QKV
+ * projection: qkv[row][qkv_row_stride] bf16 whose first num_heads*128
+ * elements are the UN-rotated query heads; the kernel rotates each Q tile
+ * by row_pos in shared memory (rope nullable: no rotation) before the first
+ * Q.K^T, bit-identical to kvs_qkv_rope_scatter's rotation, so a caller can
+ * skip writing q (kvs_qkv_rope_scatter with q_out == NULL).  Replaces the
+ * same reference code as kvs_attention_fwd (model.py:110-129, 193-195, 201);
+ * even GQA groups and odd groups (the fwd3 / fwd6 kernels) only.          */
+kvs_status kvs_attention_fwd_qkv(const void *qkv, int64_t qkv_row_stride, const kvs_rope *rope,
+                                 const int32_t *row_pos, int64_t n_rows, int32_t num_heads,
+                                 const int32_t *tile_req, const int32_t *tile_row0,
+                                 const int32_t *tile_rows, int32_t n_tiles,
+                                 const int32_t *kv_len, int32_t causal, int32_t layer,
+                                 const kvs_kv_arena *arena, const kvs_batch *batch,
+                                 float softmax_scale, void *out, kvs_stream_t stream);
 
 /* Few-row attention (decode steps, probe queries): same semantics as
  * kvs_attention_fwd for arbitrary rows (row_req per row; rows of one request

@@ -16,6 +16,7 @@
 // S^T = K_tile . Q_j^T with one KEY per TMEM lane - so the causal column sum
 // sum_j exp(s_ji - lse_j) is a per-thread row reduction with no cross-thread
 // traffic and no P store.
+#include <algorithm>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -62,6 +63,47 @@ struct Params {
     __nv_bfloat16 *out;
     float *lse;
     int64_t n_rows;
+    // non-null: Q arrives un-rotated (straight from the QKV projection) and
+    // the softmax warps rotate the tile in shared memory before the first
+    // Q.K^T (fp32 [max_pos][64] cos/sin tables, the scatter's rotation)
+    const float *q_cos, *q_sin;
+};
+
+// In-place rotation of row i of a TMA-loaded [128 x 128] SW128 Q tile: chunk
+// c of the first half pairs with chunk c of the second half at the same
+// swizzled offset.  Rows past the tile's end hold other rows or zeros and are
+// rotated by position 0 (identity); their outputs are never stored.  The
+// row's 64 cos + 64 sin coefficients are loaded into registers BEFORE the
+// caller waits for the Q tile (load(), one L2 round trip hidden under the
+// TMA), because shared stores through a generic pointer would otherwise keep
+// the compiler from hoisting later chunks' table loads above them.
+struct RopeRow {
+    float4 c[16], s[16];
+    __device__ __forceinline__ void load(int pos, const float *cos_t, const float *sin_t) {
+        const float4 *c4 = reinterpret_cast<const float4 *>(cos_t + (size_t)pos * 64);
+        const float4 *s4 = reinterpret_cast<const float4 *>(sin_t + (size_t)pos * 64);
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+            c[k] = __ldg(c4 + k);
+            s[k] = __ldg(s4 + k);
+        }
+    }
+    __device__ __forceinline__ void apply(uint8_t *tile, int i) const {
+        uint8_t *row = tile + i * 128;
+        uint4 a[8], b[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            a[k] = *reinterpret_cast<const uint4 *>(row + ((k ^ (i & 7)) << 4));
+            b[k] = *reinterpret_cast<const uint4 *>(row + HALF_BYTES + ((k ^ (i & 7)) << 4));
+        }
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            uint4 lo, hi;
+            rope8_reg(a[k], b[k], lo, hi, c[2 * k], c[2 * k + 1], s[2 * k], s[2 * k + 1]);
+            *reinterpret_cast<uint4 *>(row + ((k ^ (i & 7)) << 4)) = lo;
+            *reinterpret_cast<uint4 *>(row + HALF_BYTES + ((k ^ (i & 7)) << 4)) = hi;
+        }
+    }
 };
 
 __device__ __forceinline__ uint32_t align1024(uint32_t a) { return (a + 1023u) & ~1023u; }
@@ -353,7 +395,7 @@ constexpr int kPolyEvery = KVS_POLY_EVERY;   // 1 in kPolyEvery exp2 pairs emula
 constexpr bool kPingPong = KVS_PINGPONG != 0;    // alternate the two heads' exp phases
 
 struct Smem3 {
-    uint64_t q_full;
+    uint64_t q_full, q_ready[2];
     uint64_t ring_full[RING3], ring_empty[RING3];
     uint64_t s_full[2], p_full[2], pv_done[2];
     uint32_t tmem_base;
@@ -387,6 +429,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
             mbar_init(&sh.s_full[i], 1);
             mbar_init(&sh.p_full[i], 128);
             mbar_init(&sh.pv_done[i], 1);
+            mbar_init(&sh.q_ready[i], 128);
         }
         fence_barrier_init();
     }
@@ -424,7 +467,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
         } else if (warp == 9 && lane == 0) {
             const uint32_t idesc_qk = umma_idesc_bf16(BM, BN, false);
             const uint32_t idesc_pv = umma_idesc_bf16(BM, HD, true);
-            mbar_wait(&sh.q_full, 0);
+            const bool qrope = p.q_cos != nullptr;
+            if (!qrope) mbar_wait(&sh.q_full, 0);
             auto issue_qk = [&](int t, int kb) {
                 const int slot = (2 * kb) % RING3;
 #pragma unroll
@@ -440,8 +484,13 @@ __global__ void __launch_bounds__(kThreads2, 1)
             if (n_kb >= 1) {
                 mbar_wait(&sh.ring_full[0], 0);
                 tc_fence_after();
-                issue_qk(0, 0);
-                issue_qk(1, 0);
+                for (int t = 0; t < 2; ++t) {
+                    if (qrope) {                       // head t's Q rotated in place
+                        mbar_wait(&sh.q_ready[t], 0);
+                        tc_fence_after();
+                    }
+                    issue_qk(t, 0);
+                }
                 umma_commit(&sh.ring_empty[0]);
             }
             for (int kb = 0; kb < n_kb; ++kb) {
@@ -483,6 +532,14 @@ __global__ void __launch_bounds__(kThreads2, 1)
         const int kend = !valid ? 0 : (p.causal ? p.row_pos[row0 + i] + 1 : kmax);
         const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
         const uint32_t tS = tmem + 128 * t + lane_off, tO = tmem + 256 + 128 * t + lane_off;
+        if (p.q_cos != nullptr) {
+            RopeRow rr;
+            rr.load(valid ? p.row_pos[row0 + i] : 0, p.q_cos, p.q_sin);
+            mbar_wait(&sh.q_full, 0);
+            rr.apply(gbase + t * TILE_BYTES, i);
+            fence_proxy_async_smem();                // generic writes -> tcgen05.mma reads
+            mbar_arrive(&sh.q_ready[t]);
+        }
         float m = -INFINITY, l = 0.f;
         float s[BN];
         for (int kb = 0; kb < n_kb; ++kb) {
@@ -629,6 +686,421 @@ __global__ void __launch_bounds__(kThreads2, 1)
     }
 }
 
+// ------------------------------------------------------------------ A1, head pairs, persistent
+// fwd3's pipeline in a persistent CTA (one per SM).  Work items (tile, head
+// pair), in the host's tile order with head pairs fastest, are handed out by
+// a global ticket: one-shot CTAs pay ~11 us of fixed cost each (metadata
+// loads, Q/K TMA latency, the first Q.K^T, the O read-back and store,
+// teardown) against ~1.9 us per 128-key block (tools/micro_attn_overhead.py),
+// and a static round-robin walk loses that back to load imbalance.
+//   * Warp 8 claims item k+1's ticket while item k streams, and publishes its
+//     metadata and 128 row positions in a shared-memory slot (depth 3: the
+//     softmax warps hold item k's slot until its epilogue), so no consumer
+//     issues a dependent global load at an item boundary.
+//   * Q_t(k+1) is loaded once the MMA warp commits q_empty[t] after item k's
+//     last Q_t.K^T; with fused RoPE (p.q_cos) the softmax warps of head t
+//     rotate it right after their last block of item k and arrive q_ready[t],
+//     so Q.K^T(k+1, 0) runs under item k's epilogue.
+//   * O_t(k) is read into registers and o_free[t] lets PV_t(k+1, 0) overwrite
+//     it (accumulate = 0) before the normalised rows are stored.
+// Barrier phases count blocks (s_full, p_full, ring) or items (q_*, pv_done,
+// o_free, item slots) over the CTA's whole walk.
+struct ItemSlot {
+    int w, req, row0, nrows, n_kb, kmax, h0, pad;
+    int pos[BM];
+};
+
+struct SmemP {
+    uint64_t q_full[2], q_empty[2], q_ready[2];
+    uint64_t ring_full[RING3], ring_empty[RING3];
+    uint64_t s_full[2], p_full[2], pv_done[2], o_free[2];
+    uint64_t item_full[3], item_empty[3];
+    uint32_t tmem_base;
+    ItemSlot item[3];
+};
+
+// [0] next ticket, [1] CTAs done; the last CTA of a launch zeroes both, so
+// launches on one stream start from 0 (concurrent fwdp launches on several
+// streams of one device would share the counter and are not supported)
+__device__ int g_fwdp_sched[2];
+
+__global__ void __launch_bounds__(kThreads2, 1)
+    fwdp_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
+                Params p, int32_t n_items) {
+    extern __shared__ uint8_t dsmem[];
+    __shared__ SmemP sh;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int pairs = p.num_heads / 2, group = p.num_heads / p.kv_heads;
+    const bool qrope = p.q_cos != nullptr;
+
+    const uint32_t base = align1024(smem_u32(dsmem));
+    const uint32_t sQ = base;                          // 2 tiles (one per head of the pair)
+    const uint32_t sR = sQ + 2 * TILE_BYTES;           // RING3 tiles
+    uint8_t *gbase = dsmem + (base - smem_u32(dsmem));
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < RING3; ++i) {
+            mbar_init(&sh.ring_full[i], 1);
+            mbar_init(&sh.ring_empty[i], 1);
+        }
+        for (int t = 0; t < 2; ++t) {
+            mbar_init(&sh.q_full[t], 1);
+            mbar_init(&sh.q_empty[t], 1);
+            mbar_init(&sh.q_ready[t], 128);
+            mbar_init(&sh.s_full[t], 1);
+            mbar_init(&sh.p_full[t], 128);
+            mbar_init(&sh.pv_done[t], 1);
+            mbar_init(&sh.o_free[t], 128);
+        }
+        for (int j = 0; j < 3; ++j) {
+            mbar_init(&sh.item_full[j], 1);
+            mbar_init(&sh.item_empty[j], 1 + 256);   // MMA lane + softmax threads
+        }
+        fence_barrier_init();
+    }
+    if (warp == 9) tmem_alloc(&sh.tmem_base, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sh.tmem_base;
+
+    if (warp >= 8) {
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+        if (warp == 8) {
+            // ------------------------------------------------ tickets, item slots, TMA
+            auto ticket = [&]() {
+                int w = 0;
+                if (lane == 0) w = atomicAdd(&g_fwdp_sched[0], 1);
+                return __shfl_sync(0xffffffffu, w, 0);
+            };
+            auto publish = [&](int k, int w) {       // item k = work item w -> slot k % 3
+                const int s = k % 3;
+                if (k >= 3) mbar_wait(&sh.item_empty[s], (uint32_t)((k / 3) - 1) & 1u);
+                ItemSlot &it = sh.item[s];
+                if (w < n_items) {
+                    const int tile = w / pairs;
+                    const int req = __ldg(p.tile_req + tile), row0 = __ldg(p.tile_row0 + tile);
+                    const int nrows = __ldg(p.tile_rows + tile);
+#pragma unroll
+                    for (int r = lane; r < BM; r += 32)
+                        it.pos[r] = r < nrows ? __ldg(p.row_pos + row0 + r) : 0;
+                    if (lane == 0) {
+                        const int kmax = p.causal ? __ldg(p.row_pos + row0 + nrows - 1) + 1
+                                                  : __ldg(p.kv_len + req);
+                        it.req = req;
+                        it.row0 = row0;
+                        it.nrows = nrows;
+                        it.kmax = kmax;
+                        it.n_kb = (kmax + BN - 1) / BN;
+                        it.h0 = 2 * (w - tile * pairs);
+                    }
+                }
+                if (lane == 0) it.w = w;
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&sh.item_full[s]);
+            };
+            if (lane == 0) {
+                tma_prefetch(&map_q);
+                tma_prefetch(&map_kv);
+            }
+            int w = ticket();
+            publish(0, w);
+            int gb = 0, k = 0;
+            while (w < n_items) {
+                const ItemSlot &it = sh.item[k % 3];
+                const int req = it.req, row0 = it.row0, n_kb = it.n_kb, kmax = it.kmax, h0 = it.h0;
+                int wn = 0;
+                {
+                    const int g = h0 / group;
+                    const int pages_needed = (kmax + p.page_size - 1) / p.page_size;
+                    const int32_t *bt = p.block_table + (int64_t)req * p.max_pages;
+                    for (int i2 = 0; i2 < 2 * n_kb; ++i2) {
+                        if (lane == 0) {
+                        if (i2 == 1) {
+                            // Q after the first K tile: each waits on item k-1's last Q.K^T
+                            for (int t = 0; t < 2; ++t) {
+                                if (k >= 1) mbar_wait(&sh.q_empty[t], (uint32_t)(k - 1) & 1u);
+                                TRACE(1 + t, k);
+                                mbar_expect_tx(&sh.q_full[t], TILE_BYTES);
+                                for (int hf = 0; hf < 2; ++hf)
+                                    tma_load_3d(gbase + t * TILE_BYTES + hf * HALF_BYTES, &map_q,
+                                                &sh.q_full[t], hf * 64, h0 + t, row0);
+                            }
+                        }
+                        const int git = 2 * gb + i2, kb = i2 >> 1, kv = i2 & 1, slot = git % RING3;
+                        if (git >= RING3)
+                            mbar_wait(&sh.ring_empty[slot], (uint32_t)((git / RING3) - 1) & 1u);
+                        mbar_expect_tx(&sh.ring_full[slot], TILE_BYTES);
+                        for (int q = 0; q < 2; ++q) {
+                            const int pi = 2 * kb + q;
+                            const int pg = bt[pi < pages_needed ? pi : 2 * kb];
+                            for (int hf = 0; hf < 2; ++hf)
+                                tma_load_4d(gbase + (sR - base) + slot * TILE_BYTES +
+                                                hf * HALF_BYTES + q * (HALF_BYTES / 2),
+                                            &map_kv, &sh.ring_full[slot], hf * 64, g, 0,
+                                            (pg * p.num_layers + p.layer) * 2 + kv);
+                        }
+                        }
+                        if (i2 == 1) {
+                            // item k's first K/V tiles and Q are in flight: claim and
+                            // publish item k+1 (its ticket and metadata round trips
+                            // overlap the ring waits that follow)
+                            wn = ticket();
+                            publish(k + 1, wn);
+                        }
+                    }
+                }
+                gb += n_kb;
+                w = wn;
+                ++k;
+            }
+            if (lane == 0 && atomicAdd(&g_fwdp_sched[1], 1) == (int)gridDim.x - 1) {
+                // every CTA has taken its last ticket: reset for the next launch
+                atomicExch(&g_fwdp_sched[0], 0);
+                atomicExch(&g_fwdp_sched[1], 0);
+            }
+        } else if (warp == 9 && lane == 0) {
+            // ------------------------------------------------ MMA issuer
+            const uint32_t idesc_qk = umma_idesc_bf16(BM, BN, false);
+            const uint32_t idesc_pv = umma_idesc_bf16(BM, HD, true);
+            auto issue_qk = [&](int t, int slot) {
+#pragma unroll
+                for (int k2 = 0; k2 < HD / 16; ++k2) {
+                    const uint64_t da = umma_desc_sw128(
+                        sQ + t * TILE_BYTES + (k2 >> 2) * HALF_BYTES + (k2 & 3) * 32, 16, 1024);
+                    const uint64_t db = umma_desc_sw128(
+                        sR + slot * TILE_BYTES + (k2 >> 2) * HALF_BYTES + (k2 & 3) * 32, 16, 1024);
+                    umma_bf16(tmem + 128 * t, da, db, idesc_qk, k2 > 0 ? 1u : 0u);
+                }
+                umma_commit(&sh.s_full[t]);
+            };
+            int gb = 0;
+            for (int k = 0;; ++k) {
+                mbar_wait(&sh.item_full[k % 3], (uint32_t)(k / 3) & 1u);
+                const int w = sh.item[k % 3].w, n_kb = sh.item[k % 3].n_kb;
+                mbar_arrive(&sh.item_empty[k % 3]);
+                if (w >= n_items) break;
+                {
+                    const int git = 2 * gb, slot = git % RING3;
+                    mbar_wait(&sh.ring_full[slot], (uint32_t)(git / RING3) & 1u);
+                    TRACE(3, k);
+                    for (int t = 0; t < 2; ++t) {
+                        mbar_wait(qrope ? &sh.q_ready[t] : &sh.q_full[t], (uint32_t)k & 1u);
+                        TRACE(4 + t, k);
+                        tc_fence_after();
+                        issue_qk(t, slot);
+                        if (n_kb == 1) umma_commit(&sh.q_empty[t]);
+                    }
+                    umma_commit(&sh.ring_empty[slot]);
+                }
+                for (int kb = 0; kb < n_kb; ++kb) {
+                    const int gk = gb + kb;
+                    const int itv = 2 * gk + 1, vslot = itv % RING3;
+                    const int itk = 2 * gk + 2, kslot = itk % RING3;
+                    const bool more = kb + 1 < n_kb;
+                    mbar_wait(&sh.ring_full[vslot], (uint32_t)(itv / RING3) & 1u);
+                    for (int t = 0; t < 2; ++t) {
+                        mbar_wait(&sh.p_full[t], (uint32_t)gk & 1u);
+                        // O_t of the previous item must have been read out
+                        if (kb == 0 && k >= 1) mbar_wait(&sh.o_free[t], (uint32_t)(k - 1) & 1u);
+                        TRACE(6 + t, gk);
+                        tc_fence_after();
+#pragma unroll
+                        for (int k2 = 0; k2 < BN / 16; ++k2) {
+                            const uint64_t db = umma_desc_sw128(sR + vslot * TILE_BYTES + k2 * 2048,
+                                                                HALF_BYTES, 1024);
+                            umma_bf16_ts(tmem + 256 + 128 * t, tmem + 128 * t + 8 * k2, db,
+                                         idesc_pv, (kb > 0 || k2 > 0) ? 1u : 0u);
+                        }
+                        if (!more) umma_commit(&sh.pv_done[t]);
+                        if (more) {
+                            if (t == 0) mbar_wait(&sh.ring_full[kslot], (uint32_t)(itk / RING3) & 1u);
+                            issue_qk(t, kslot);
+                            if (kb + 2 == n_kb) umma_commit(&sh.q_empty[t]);
+                        }
+                    }
+                    umma_commit(&sh.ring_empty[vslot]);
+                    if (more) umma_commit(&sh.ring_empty[kslot]);
+                }
+                gb += n_kb;
+            }
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------ softmax warpgroups
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+        const int t = warp >> 2;                 // head of this warpgroup
+        const int i = threadIdx.x & 127;         // row within tile == TMEM lane
+        const uint32_t lane_off = (uint32_t)((warp & 3) * 32) << 16;
+        const uint32_t tS = tmem + 128 * t + lane_off, tO = tmem + 256 + 128 * t + lane_off;
+        // item kk's slot: published by warp 8, held until kk's epilogue has read it
+        auto wait_item = [&](int kk) {
+            mbar_wait(&sh.item_full[kk % 3], (uint32_t)(kk / 3) & 1u);
+        };
+        // rotate item kk's Q_t in place (row i's position) and release it to the MMA warp
+        auto rope_q = [&](int kk) {
+            RopeRow rr;
+            rr.load(sh.item[kk % 3].pos[i], p.q_cos, p.q_sin);
+            mbar_wait(&sh.q_full[t], (uint32_t)kk & 1u);
+            rr.apply(gbase + t * TILE_BYTES, i);
+            fence_proxy_async_smem();
+            mbar_arrive(&sh.q_ready[t]);
+        };
+        int gb = 0, k = 0;
+        wait_item(0);
+        if (qrope && sh.item[0].w < n_items) rope_q(0);
+        while (sh.item[k % 3].w < n_items) {
+            const int slot = k % 3;
+            const int n_kb = sh.item[slot].n_kb;
+            const int kend = i >= sh.item[slot].nrows ? 0
+                             : (p.causal ? sh.item[slot].pos[i] + 1 : sh.item[slot].kmax);
+            float m = -INFINITY, l = 0.f;
+            float s[BN];
+            for (int kb = 0; kb < n_kb; ++kb) {
+                const int gk = gb + kb;
+                mbar_wait(&sh.s_full[t], (uint32_t)gk & 1u);
+                if (i == 0) TRACE(20 + 10 * t, gk);
+                tc_fence_after();
+#pragma unroll
+                for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS + c * 32, s + c * 32);
+                tmem_ld_wait();
+                const int kbase = kb * BN;
+                if (kbase + BN > kend) {
+#pragma unroll
+                    for (int c = 0; c < BN; ++c) s[c] = (kbase + c < kend) ? s[c] : -INFINITY;
+                }
+                float ls[8];
+                auto exp_pass = [&](float mu, bool track, float &bmax) {
+                    float mx[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        ls[j] = 0.f;
+                        mx[j] = -INFINITY;
+                    }
+#pragma unroll
+                    for (int hf = 0; hf < 2; ++hf) {
+                        uint32_t pk[32];
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) {
+                            const float s0 = s[hf * 64 + 2 * q], s1 = s[hf * 64 + 2 * q + 1];
+                            if (track) mx[q & 7] = fmaxf(mx[q & 7], fmaxf(s0, s1));
+                            const float e0 = fast_exp2(fmaf(s0, p.scale_log2, -mu));
+                            const float e1 = fast_exp2(fmaf(s1, p.scale_log2, -mu));
+                            ls[(2 * q) & 7] += e0;
+                            ls[(2 * q + 1) & 7] += e1;
+                            pk[q] = pack_bf16x2(e0, e1);
+                        }
+                        tmem_st32(tS + hf * 32, reinterpret_cast<const float *>(pk));
+                    }
+                    if (track)
+                        bmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                     fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+                };
+                auto row_max = [&]() {
+                    float mx[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
+#pragma unroll
+                    for (int c = 0; c < BN; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
+                    return fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+                };
+                auto rescale = [&](float mloc) {
+                    const bool grow =
+                        mloc > m + kRescaleThreshold || (m == -INFINITY && mloc > -INFINITY);
+                    const bool touch_o = grow && kb >= 1 && m != -INFINITY;
+                    float factor = 1.f;
+                    if (grow) {
+                        factor = (m == -INFINITY) ? 0.f : fast_exp2(m - mloc);
+                        l *= factor;
+                        m = mloc;
+                    }
+                    if (__any_sync(0xffffffffu, touch_o)) {
+                        // PV_t(kb-1) retired before QK_t(kb) (in-order), so O is quiescent
+                        const float f = touch_o ? factor : 1.f;
+                        float o[32];
+#pragma unroll
+                        for (int c = 0; c < HD / 32; ++c) {
+                            tmem_ld32(tO + c * 32, o);
+                            tmem_ld_wait();
+#pragma unroll
+                            for (int e = 0; e < 32; ++e) o[e] *= f;
+                            tmem_st32(tO + c * 32, o);
+                        }
+                    }
+                };
+                // ping-pong over the CTA's whole walk: head 1 waits on head 0's
+                // exp phase of the same block, head 0 on head 1's previous one
+                if (kPingPong && (t == 1 || gk > 0))
+                    asm volatile("bar.sync %0, 256;" ::"r"(1 + t) : "memory");
+                float bmax = -INFINITY;
+                if (__all_sync(0xffffffffu, m != -INFINITY)) {
+                    exp_pass(m, true, bmax);
+                    if (__any_sync(0xffffffffu, bmax * p.scale_log2 > m + kRescaleThreshold)) {
+                        rescale(bmax * p.scale_log2);
+                        exp_pass(m, false, bmax);
+                    }
+                } else {
+                    rescale(row_max() * p.scale_log2);
+                    exp_pass((m == -INFINITY) ? 0.f : m, false, bmax);
+                }
+                if (kPingPong) asm volatile("bar.arrive %0, 256;" ::"r"(2 - t) : "memory");
+                l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
+                tmem_st_wait();
+                tc_fence_before();
+                mbar_arrive(&sh.p_full[t]);
+                if (i == 0) TRACE(22 + 10 * t, gk);
+            }
+            // the next item's Q first (its Q.K^T then runs under this epilogue),
+            // then O_t into registers, release it, normalise + store
+            wait_item(k + 1);
+            if (qrope && sh.item[(k + 1) % 3].w < n_items) rope_q(k + 1);
+            if (i == 0) TRACE(25 + 10 * t, k);
+            mbar_wait(&sh.pv_done[t], (uint32_t)k & 1u);
+            if (i == 0) TRACE(26 + 10 * t, k);
+            tc_fence_after();
+            float o[HD];
+#pragma unroll
+            for (int c = 0; c < HD / 32; ++c) tmem_ld32(tO + c * 32, o + c * 32);
+            tmem_ld_wait();
+            tc_fence_before();
+            mbar_arrive(&sh.o_free[t]);
+            const int64_t grow = (int64_t)sh.item[slot].row0 + i;
+            const int h = sh.item[slot].h0 + t;
+            const bool valid = i < sh.item[slot].nrows;
+            mbar_arrive(&sh.item_empty[slot]);
+            const float inv = l > 0.f ? 1.f / l : 0.f;
+            if (valid) {
+                uint4 *dst = reinterpret_cast<uint4 *>(p.out + (grow * p.num_heads + h) * HD);
+#pragma unroll
+                for (int v = 0; v < HD / 8; ++v) {
+                    uint4 wv;
+                    wv.x = pack_bf16x2(o[8 * v + 0] * inv, o[8 * v + 1] * inv);
+                    wv.y = pack_bf16x2(o[8 * v + 2] * inv, o[8 * v + 3] * inv);
+                    wv.z = pack_bf16x2(o[8 * v + 4] * inv, o[8 * v + 5] * inv);
+                    wv.w = pack_bf16x2(o[8 * v + 6] * inv, o[8 * v + 7] * inv);
+                    dst[v] = wv;
+                }
+                if (p.lse != nullptr)
+                    p.lse[grow * p.num_heads + h] =
+                        (l > 0.f) ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+            }
+            if (i == 0) TRACE(27 + 10 * t, k);
+            gb += n_kb;
+            ++k;
+        }
+        mbar_arrive(&sh.item_empty[k % 3]);       // the terminal slot
+        // consume head 1's last exp-phase arrival
+        if (kPingPong && t == 0 && gb >= 1) asm volatile("bar.sync 1, 256;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 9) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
 // ------------------------------------------------------------------ A1, one head, S double-buffered
 // One query head per CTA; TMEM holds S0 | S1 | O (128 fp32 columns each).
 // The softmax writes P (bf16) over the S buffer it read and O += P.V runs
@@ -642,7 +1114,7 @@ constexpr int RING6 = 6;
 constexpr int kThreads6 = 192;
 
 struct Smem6 {
-    uint64_t q_full;
+    uint64_t q_full, q_ready;
     uint64_t ring_full[RING6], ring_empty[RING6];
     uint64_t s_full[2], p_full[2], pv_done[2];
     uint32_t tmem_base;
@@ -677,6 +1149,7 @@ __global__ void __launch_bounds__(kThreads6, 1)
             mbar_init(&sh.p_full[i], 128);
             mbar_init(&sh.pv_done[i], 1);
         }
+        mbar_init(&sh.q_ready, 128);
         fence_barrier_init();
     }
     if (warp == 5) tmem_alloc(&sh.tmem_base, 512);
@@ -713,7 +1186,12 @@ __global__ void __launch_bounds__(kThreads6, 1)
         if (lane == 0) {
             const uint32_t idesc_qk = umma_idesc_bf16(BM, BN, false);
             const uint32_t idesc_pv = umma_idesc_bf16(BM, HD, true);
-            mbar_wait(&sh.q_full, 0);
+            if (p.q_cos != nullptr) {                // Q rotated in place by the softmax warps
+                mbar_wait(&sh.q_ready, 0);
+                tc_fence_after();
+            } else {
+                mbar_wait(&sh.q_full, 0);
+            }
             auto issue_qk = [&](int kb) {
                 const int it = 2 * kb, slot = it % RING6, b = kb & 1;
                 mbar_wait(&sh.ring_full[slot], (uint32_t)(it / RING6) & 1u);
@@ -758,6 +1236,14 @@ __global__ void __launch_bounds__(kThreads6, 1)
         const int kend = !valid ? 0 : (p.causal ? p.row_pos[row0 + i] + 1 : kmax);
         const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
         const uint32_t tO = tmem + 256 + lane_off;
+        if (p.q_cos != nullptr) {
+            RopeRow rr;
+            rr.load(valid ? p.row_pos[row0 + i] : 0, p.q_cos, p.q_sin);
+            mbar_wait(&sh.q_full, 0);
+            rr.apply(gbase, i);
+            fence_proxy_async_smem();
+            mbar_arrive(&sh.q_ready);
+        }
         float m = -INFINITY, l = 0.f;
         float s[BN];
         for (int kb = 0; kb < n_kb; ++kb) {
@@ -1046,9 +1532,13 @@ __global__ void alpha_reduce_kernel(const float *__restrict__ part, int64_t n, i
 
 }  // namespace attn
 
-static bool make_q_map(CUtensorMap *m, const void *q, int64_t n_rows, int H, int D) {
+// q: [n_rows][row_stride] bf16 whose first H*D elements are the query heads
+// (row_stride = H*D for a dense q, (H+2G)*D for rows of the QKV projection)
+static bool make_q_map(CUtensorMap *m, const void *q, int64_t n_rows, int H, int D,
+                       int64_t row_stride = 0) {
+    if (row_stride == 0) row_stride = (int64_t)H * D;
     uint64_t dims[3] = {(uint64_t)D, (uint64_t)H, (uint64_t)n_rows};
-    uint64_t strides[2] = {(uint64_t)D * 2, (uint64_t)H * D * 2};
+    uint64_t strides[2] = {(uint64_t)D * 2, (uint64_t)row_stride * 2};
     uint32_t box[3] = {64, 1, 128};
     return encode_tmap(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void *>(q), dims, strides,
                        box, CU_TENSOR_MAP_SWIZZLE_128B);
@@ -1072,22 +1562,27 @@ static size_t fwd_smem() {
 
 using namespace kvs;
 
-extern "C" {
-
-kvs_status kvs_attention_fwd(const void *q, const int32_t *row_pos, int64_t n_rows,
-                             int32_t num_heads, const int32_t *tile_req, const int32_t *tile_row0,
-                             const int32_t *tile_rows, int32_t n_tiles, const int32_t *kv_len,
-                             int32_t causal, int32_t layer, const kvs_kv_arena *arena,
-                             const kvs_batch *batch, float softmax_scale, void *out, float *lse,
-                             kvs_stream_t stream) {
+static kvs_status attention_fwd_impl(const void *q, int64_t q_row_stride, const kvs_rope *rope,
+                                     const int32_t *row_pos, int64_t n_rows, int32_t num_heads,
+                                     const int32_t *tile_req, const int32_t *tile_row0,
+                                     const int32_t *tile_rows, int32_t n_tiles,
+                                     const int32_t *kv_len, int32_t causal, int32_t layer,
+                                     const kvs_kv_arena *arena, const kvs_batch *batch,
+                                     float softmax_scale, void *out, float *lse,
+                                     kvs_stream_t stream) {
     kvs_status st = check_arena(arena, num_heads);
     if (st != KVS_OK) return st;
     KVS_REQUIRE(batch != nullptr, KVS_EPARAM, "null batch");
     KVS_REQUIRE(causal || kv_len != nullptr, KVS_EPARAM, "non-causal attention needs kv_len");
+    KVS_REQUIRE(rope == nullptr || (rope->cos != nullptr && rope->sin != nullptr), KVS_EPARAM,
+                "rope tables are null");
+    KVS_REQUIRE(q_row_stride >= (int64_t)num_heads * 128 && q_row_stride % 8 == 0, KVS_ESHAPE,
+                "q row stride %lld below H*128 or not 16-byte aligned", (long long)q_row_stride);
     if (n_tiles <= 0 || n_rows <= 0) return KVS_OK;
     KVS_REQUIRE(n_tiles <= 65535, KVS_ESHAPE, "more than 65535 row tiles in one launch");
     CUtensorMap mq, mkv;
-    KVS_REQUIRE(make_q_map(&mq, q, n_rows, num_heads, 128), KVS_ECUDA, "Q tensor map");
+    KVS_REQUIRE(make_q_map(&mq, q, n_rows, num_heads, 128, q_row_stride), KVS_ECUDA,
+                "Q tensor map");
     KVS_REQUIRE(make_kv_map(&mkv, arena), KVS_ECUDA, "KV tensor map");
     attn::Params p;
     p.row_pos = row_pos;
@@ -1107,23 +1602,35 @@ kvs_status kvs_attention_fwd(const void *q, const int32_t *row_pos, int64_t n_ro
     p.out = (__nv_bfloat16 *)out;
     p.lse = lse;
     p.n_rows = n_rows;
+    p.q_cos = rope != nullptr ? rope->cos : nullptr;
+    p.q_sin = rope != nullptr ? rope->sin : nullptr;
     cudaStream_t s = (cudaStream_t)stream;
     const int group = num_heads / arena->kv_heads;
     const char *variant = getenv("KVS_ATTN");
-    // default: head pairs (fwd3) for even GQA groups, single heads with
-    // double-buffered S (fwd6) otherwise; KVS_ATTN=1|3|6 pins a variant
-    // (1: the single-head kernel with P through shared memory)
-    const char v = variant != nullptr ? variant[0] : (group % 2 == 0 ? '3' : '6');
+    // default: persistent head pairs (fwdp) for even GQA groups, single heads
+    // with double-buffered S (fwd6) otherwise; KVS_ATTN=1|3|6|p pins a variant
+    // (1: the single-head kernel with P through shared memory, 3: one-shot
+    // head-pair CTAs)
+    const char v = variant != nullptr ? variant[0] : (group % 2 == 0 ? 'p' : '6');
     if (out != nullptr && (v == '6' || (v != '1' && group % 2 != 0))) {
         const size_t smem = 1024 + attn::TILE_BYTES * (1 + attn::RING6);
         cudaFuncSetAttribute(attn::fwd6_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         attn::fwd6_kernel<<<dim3(num_heads, n_tiles), attn::kThreads6, smem, s>>>(mq, mkv, p);
+    } else if (out != nullptr && group % 2 == 0 && v == 'p') {
+        const size_t smem = 1024 + attn::TILE_BYTES * (2 + attn::RING3);
+        cudaFuncSetAttribute(attn::fwdp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        const int n_items = n_tiles * (num_heads / 2);
+        attn::fwdp_kernel<<<std::min(n_items, kNumSMs), attn::kThreads2, smem, s>>>(mq, mkv, p,
+                                                                                  n_items);
     } else if (out != nullptr && group % 2 == 0 && v == '3') {
         const size_t smem = 1024 + attn::TILE_BYTES * (2 + attn::RING3);
         cudaFuncSetAttribute(attn::fwd3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
         attn::fwd3_kernel<<<dim3(num_heads / 2, n_tiles), attn::kThreads2, smem, s>>>(mq, mkv, p);
+    } else if (rope != nullptr) {
+        KVS_REQUIRE(false, KVS_EPARAM, "in-kernel Q rotation needs the fwd3/fwd6 kernels");
     } else if (out != nullptr) {
         const size_t smem = fwd_smem<true>();
         cudaFuncSetAttribute(attn::fwd_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1137,6 +1644,32 @@ kvs_status kvs_attention_fwd(const void *q, const int32_t *row_pos, int64_t n_ro
     }
     KVS_CHECK_LAUNCH("kvs_attention_fwd");
     return KVS_OK;
+}
+
+extern "C" {
+
+kvs_status kvs_attention_fwd(const void *q, const int32_t *row_pos, int64_t n_rows,
+                             int32_t num_heads, const int32_t *tile_req, const int32_t *tile_row0,
+                             const int32_t *tile_rows, int32_t n_tiles, const int32_t *kv_len,
+                             int32_t causal, int32_t layer, const kvs_kv_arena *arena,
+                             const kvs_batch *batch, float softmax_scale, void *out, float *lse,
+                             kvs_stream_t stream) {
+    return attention_fwd_impl(q, (int64_t)num_heads * 128, nullptr, row_pos, n_rows, num_heads,
+                              tile_req, tile_row0, tile_rows, n_tiles, kv_len, causal, layer,
+                              arena, batch, softmax_scale, out, lse, stream);
+}
+
+kvs_status kvs_attention_fwd_qkv(const void *qkv, int64_t qkv_row_stride, const kvs_rope *rope,
+                                 const int32_t *row_pos, int64_t n_rows, int32_t num_heads,
+                                 const int32_t *tile_req, const int32_t *tile_row0,
+                                 const int32_t *tile_rows, int32_t n_tiles,
+                                 const int32_t *kv_len, int32_t causal, int32_t layer,
+                                 const kvs_kv_arena *arena, const kvs_batch *batch,
+                                 float softmax_scale, void *out, kvs_stream_t stream) {
+    KVS_REQUIRE(out != nullptr, KVS_EPARAM, "null out");
+    return attention_fwd_impl(qkv, qkv_row_stride, rope, row_pos, n_rows, num_heads, tile_req,
+                              tile_row0, tile_rows, n_tiles, kv_len, causal, layer, arena, batch,
+                              softmax_scale, out, nullptr, stream);
 }
 
 int32_t kvs_attn_trace_dump(int64_t *host, int32_t max_pairs) {

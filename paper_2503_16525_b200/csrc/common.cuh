@@ -36,6 +36,30 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     return *reinterpret_cast<uint32_t *>(&v);
 }
 
+// Rotate-half RoPE on 8 dims [8c, 8c+8) of a head's first half (lo) and the
+// paired dims of its second half (hi), coefficients in registers (two float4
+// each).  Shared by the q/k scatter and the attention kernels' in-place Q
+// rotation, so both produce the same bf16 bits.
+__device__ __forceinline__ void rope8_reg(const uint4 &lo_in, const uint4 &hi_in, uint4 &lo_out,
+                                          uint4 &hi_out, const float4 c0, const float4 c1,
+                                          const float4 s0, const float4 s1) {
+    const __nv_bfloat162 *x1 = reinterpret_cast<const __nv_bfloat162 *>(&lo_in);
+    const __nv_bfloat162 *x2 = reinterpret_cast<const __nv_bfloat162 *>(&hi_in);
+    uint32_t *o1 = reinterpret_cast<uint32_t *>(&lo_out);
+    uint32_t *o2 = reinterpret_cast<uint32_t *>(&hi_out);
+    const float cs[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    const float sn[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+        const float2 a = __bfloat1622float2(x1[k]), b = __bfloat1622float2(x2[k]);
+        // explicit fma/mul (no contraction choice left to the compiler)
+        o1[k] = pack_bf16x2(__fmaf_rn(a.x, cs[2 * k], -__fmul_rn(b.x, sn[2 * k])),
+                            __fmaf_rn(a.y, cs[2 * k + 1], -__fmul_rn(b.y, sn[2 * k + 1])));
+        o2[k] = pack_bf16x2(__fmaf_rn(b.x, cs[2 * k], __fmul_rn(a.x, sn[2 * k])),
+                            __fmaf_rn(b.y, cs[2 * k + 1], __fmul_rn(a.y, sn[2 * k + 1])));
+    }
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_sum(T v) {
 #pragma unroll

@@ -98,24 +98,6 @@ __global__ void __launch_bounds__(128) gather_kv_kernel(
     }
 }
 
-// Rotate-half on 8 dims with the coefficients in registers (two float4 each).
-__device__ __forceinline__ void rope8_reg(const uint4 &lo_in, const uint4 &hi_in, uint4 &lo_out,
-                                          uint4 &hi_out, const float4 c0, const float4 c1,
-                                          const float4 s0, const float4 s1) {
-    const __nv_bfloat162 *x1 = reinterpret_cast<const __nv_bfloat162 *>(&lo_in);
-    const __nv_bfloat162 *x2 = reinterpret_cast<const __nv_bfloat162 *>(&hi_in);
-    uint32_t *o1 = reinterpret_cast<uint32_t *>(&lo_out);
-    uint32_t *o2 = reinterpret_cast<uint32_t *>(&hi_out);
-    const float cs[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
-    const float sn[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        const float2 a = __bfloat1622float2(x1[k]), b = __bfloat1622float2(x2[k]);
-        o1[k] = pack_bf16x2(a.x * cs[2 * k] - b.x * sn[2 * k], a.y * cs[2 * k + 1] - b.y * sn[2 * k + 1]);
-        o2[k] = pack_bf16x2(b.x * cs[2 * k] + a.x * sn[2 * k], b.y * cs[2 * k + 1] + a.y * sn[2 * k + 1]);
-    }
-}
-
 // One CTA per query row.  qkv row = [q (H*D) | k (G*D) | v (G*D)].  Work
 // items: (H+G)*D/16 rotation items (two 16-byte vectors each) followed by
 // G*D/8 V vectors; a thread takes two items per round and issues all of its
@@ -243,7 +225,10 @@ __global__ void __launch_bounds__(kScatThreads) qkv_scatter2_kernel(
     __shared__ __align__(8) uint64_t bars[kScatSlots];
     const int G = A.G, D = A.D, chunks = D / 16, vph = D / 8;
     const int64_t width = (int64_t)(H + 2 * G) * D;
-    const uint32_t row_bytes = (uint32_t)(width * 2);
+    // q_out == nullptr: the query heads are left to the attention kernel and
+    // only the row's k|v part is staged (4 of 12 KB at Llama width)
+    const int64_t col0 = q_out != nullptr ? 0 : (int64_t)H * D;
+    const uint32_t row_bytes = (uint32_t)((width - col0) * 2);
     const int tid = threadIdx.x;
     const int64_t n_mine = n_rows > (int64_t)blockIdx.x
                                ? (n_rows - 1 - (int64_t)blockIdx.x) / gridDim.x + 1 : 0;
@@ -260,8 +245,8 @@ __global__ void __launch_bounds__(kScatThreads) qkv_scatter2_kernel(
         if (tid == 0) {
             mbar_expect_tx(&bars[slot], row_bytes);
             const int64_t src = src_row != nullptr ? (int64_t)src_row[row] : row;
-            bulk_g2s(smem_u32(s_rows) + (uint32_t)slot * row_bytes, qkv + src * width, row_bytes,
-                     &bars[slot]);
+            bulk_g2s(smem_u32(s_rows) + (uint32_t)slot * row_bytes, qkv + src * width + col0,
+                     row_bytes, &bars[slot]);
         } else if (tid >= 32 && tid < 64) {
             const int lane = tid - 32;
             const int32_t pos = row_pos[row];
@@ -290,7 +275,9 @@ __global__ void __launch_bounds__(kScatThreads) qkv_scatter2_kernel(
         stage(k + kScatSlots - 1);                 // refills the slot freed last iteration
         mbar_wait(&bars[slot], (uint32_t)((k / kScatSlots) & 1));
         const int64_t row = (int64_t)blockIdx.x + k * gridDim.x;
-        const uint4 *src = reinterpret_cast<const uint4 *>(s_rows + (size_t)slot * row_bytes);
+        // staged vector v of the row is row vector v + col0 / 8
+        const uint4 *src = reinterpret_cast<const uint4 *>(s_rows + (size_t)slot * row_bytes) -
+                           col0 / 8;
         const ScatMeta m = s_meta[slot];
         uint4 *dk = m.dst >= 0 ? reinterpret_cast<uint4 *>(A.base + m.dst) : nullptr;
         uint4 *dv = m.dst >= 0 ? reinterpret_cast<uint4 *>(A.base + m.dst + (int64_t)A.P * G * D)
@@ -533,7 +520,8 @@ static kvs_status qkv_scatter_impl(const void *qkv, const int32_t *src_row, int6
     KVS_REQUIRE(num_heads % arena->kv_heads == 0, KVS_ESHAPE, "num_heads % kv_heads != 0");
     if (n_rows <= 0) return KVS_OK;
     cudaStream_t s = (cudaStream_t)stream;
-    const size_t row_bytes = (size_t)(num_heads + 2 * arena->kv_heads) * arena->head_dim * 2;
+    const size_t row_bytes = (size_t)((q_out != nullptr ? num_heads : 0) + 2 * arena->kv_heads) *
+                             arena->head_dim * 2;
     const size_t smem = kScatSlots * row_bytes;
     if (arena->head_dim == 128 && smem <= 200 * 1024 && getenv("KVS_SCATTER_V1") == nullptr) {
         cudaFuncSetAttribute(qkv_scatter2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -222,6 +222,11 @@ class Engine:
         self._ev_next = 0
         self.scratch = _Scratch(self.device)
         self._xb_of = None
+        # KVS_FUSED_Q_ROPE=1: A1 takes q straight from the projection rows and
+        # rotates it in shared memory (the scatter then moves only k|v).  Off by
+        # default: measured in the step, the rotation on the softmax warps' item
+        # boundary costs more A1 time (+2.8 ms) than the scatter saves (-2.3 ms)
+        self.fused_q_rope = os.environ.get("KVS_FUSED_Q_ROPE", "0") == "1"
         self.layer0_fast = True     # prefill_batch: probe layer 0 doubles as the prefill's
         self._side = torch.cuda.Stream(self.device) if torch.cuda.is_available() else None
         self._fetch_stream = torch.cuda.Stream(self.device) if torch.cuda.is_available() else None
@@ -305,6 +310,16 @@ class Engine:
                rows.tiles[2].data_ptr(), rows.n_tiles, None, 1, layer, arena_c, batch_c,
                self.scale, N.ptr(out), N.ptr(lse), N.stream_ptr())
 
+    def _attention_qkv(self, qkv, rows: RowSet, layer: int, arena_c, batch_c, out):
+        """A1 reading the un-rotated query heads straight from the QKV
+        projection rows (rotated in the kernel's shared memory): the scatter
+        then moves only k|v (no q round trip through HBM)."""
+        self._timed("attention", N.call, "kvs_attention_fwd_qkv", qkv.data_ptr(), qkv.shape[1],
+                    self._rope(), rows.row_pos.data_ptr(), rows.n_rows, self.cfg.num_heads,
+                    rows.tiles[0].data_ptr(), rows.tiles[1].data_ptr(), rows.tiles[2].data_ptr(),
+                    rows.n_tiles, None, 1, layer, arena_c, batch_c, self.scale, out.data_ptr(),
+                    N.stream_ptr())
+
     def _decode_attention(self, q, rows: RowSet, layer: int, arena_c, batch_c, out, max_kv):
         cfg = self.cfg
         nb = N.ws_bytes("kvs_decode_attention_workspace", rows.n_rows, cfg.num_heads,
@@ -320,12 +335,12 @@ class Engine:
         if src_row is not None:
             N.call("kvs_qkv_rope_scatter_rows", qkv.data_ptr(), src_row.data_ptr(), rows.n_rows,
                    self.cfg.num_heads, rows.row_req.data_ptr(), rows.row_pos.data_ptr(),
-                   N.ptr(wk), layer, arena_c, batch_c, self._rope(), q_out.data_ptr(),
+                   N.ptr(wk), layer, arena_c, batch_c, self._rope(), N.ptr(q_out),
                    N.ptr(k_out), N.ptr(v_out), N.stream_ptr())
             return
         N.call("kvs_qkv_rope_scatter", qkv.data_ptr(), rows.n_rows, self.cfg.num_heads,
                rows.row_req.data_ptr(), rows.row_pos.data_ptr(), N.ptr(wk), layer, arena_c,
-               batch_c, self._rope(), q_out.data_ptr(), N.ptr(k_out), N.ptr(v_out),
+               batch_c, self._rope(), N.ptr(q_out), N.ptr(k_out), N.ptr(v_out),
                N.stream_ptr())
 
     def _embed(self, tokens_flat, rows: RowSet, scratch: bool = False) -> torch.Tensor:
@@ -355,6 +370,13 @@ class Engine:
             if i == 0 and first_qkv is not None:
                 self._scatter(first_qkv[0], rows, layer, arena_c, batch_c, q, write_kv=wk,
                               src_row=first_qkv[1])
+            elif not decode and capture is None and self.fused_q_rope:
+                # q stays in the projection rows; A1 rotates it in shared memory
+                qkv = self._qkv(x, layer)
+                self._scatter(qkv, rows, layer, arena_c, batch_c, None, write_kv=wk)
+                self._attention_qkv(qkv, rows, layer, arena_c, batch_c, o)
+                self._out_proj(x, o, layer)
+                continue
             else:
                 qkv = self._qkv(x, layer)
                 self._scatter(qkv, rows, layer, arena_c, batch_c, q, write_kv=wk)
@@ -445,8 +467,12 @@ class Engine:
             q = self.scratch.get("q", (n, H, HEAD_DIM), torch.bfloat16)
             o = self.scratch.get("o", (n, H, HEAD_DIM), torch.bfloat16)
             qkv = self._qkv(x, 0)
-            self._scatter(qkv, rows, 0, self.arena.c, st.batch_c, q, use_write=False)
-            self._attention(q, rows, 0, self.arena.c, st.batch_c, o)
+            if self.fused_q_rope:
+                self._scatter(qkv, rows, 0, self.arena.c, st.batch_c, None, use_write=False)
+                self._attention_qkv(qkv, rows, 0, self.arena.c, st.batch_c, o)
+            else:
+                self._scatter(qkv, rows, 0, self.arena.c, st.batch_c, q, use_write=False)
+                self._attention(q, rows, 0, self.arena.c, st.batch_c, o)
             self._out_proj(x, o, 0)
             st._x_probe = x
         elif p == 1:

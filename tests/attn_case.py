@@ -11,12 +11,13 @@ import torch
 
 
 def build_case(R=2, n=1000, H=8, G=2, frac=0.6, seed=0, layers=2, layer=1, device="cuda",
-               scale_kv=1.0, scale_q=1.0):
+               scale_kv=1.0, scale_q=1.0, rope_theta=None):
     import paper_2503_16525_b200 as K
     from paper_2503_16525_b200.engine import Engine, RowSet
     from paper_2503_16525_b200.pool import CachePool, KVArena
+    extra = {} if rope_theta is None else {"rope_theta": rope_theta}
     cfg = K.ModelConfig(num_layers=layers, num_heads=H, num_kv_heads=G, d_model=H * 128,
-                        vocab_size=100, max_positions=n + 64)
+                        vocab_size=100, max_positions=n + 64, **extra)
     model = K.ToyModel(cfg, init="device")
     pages = R * ((n + 63) // 64)
     arena = KVArena(cfg, pages + 2)

@@ -43,3 +43,35 @@ def test_attention_large_logits_rescale(scale_q):
     err = (got[:, [0, 5]].float() - want).norm() / want.norm()
     assert err < ATTN_TOL, f"relative Frobenius error {err:.3e}"
     assert torch.isfinite(got).all()
+
+
+@pytest.mark.parametrize("R,n,H,G,frac", [
+    (2, 700, 8, 2, 0.6), (1, 1500, 28, 4, 0.55), (2, 300, 4, 4, 1.0), (1, 2048, 32, 8, 0.6),
+    (3, 129, 8, 1, 0.5)])
+def test_attention_qkv_fused_rope_bit_exact(R, n, H, G, frac):
+    """kvs_attention_fwd_qkv (un-rotated q read from the projection rows and
+    rotated in shared memory) equals the scatter-rotated q through
+    kvs_attention_fwd bit for bit, for head pairs (fwd3) and single heads
+    (fwd6); the scatter's K/V writes are identical with q_out == NULL."""
+    eng, st, rows, _, layer = build_case(R, n, H, G, frac, seed=n + G, rope_theta=5e5)
+    assert eng.rope_c is not None
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    m = rows.n_rows
+    qkv = (torch.randn(m, (H + 2 * G) * 128, generator=gen, device="cuda") * 2).to(torch.bfloat16)
+    before = eng.arena.data.clone()
+    q = torch.empty(m, H, 128, dtype=torch.bfloat16, device="cuda")
+    eng._scatter(qkv, rows, layer, eng.arena.c, st.batch_c, q, use_write=False)
+    want = _run(eng, st, rows, q, layer)
+    arena_a = eng.arena.data.clone()
+    eng.arena.data.copy_(before)
+    eng._scatter(qkv, rows, layer, eng.arena.c, st.batch_c, None, use_write=False)
+    torch.cuda.synchronize()
+    assert torch.equal(eng.arena.data, arena_a), "scatter without q changed the K/V writes"
+    got = torch.empty_like(want)
+    eng._attention_qkv(qkv, rows, layer, eng.arena.c, st.batch_c, got)
+    torch.cuda.synchronize()
+    assert torch.equal(got, want), \
+        f"fused-rope attention differs: max |d| {(got.float() - want.float()).abs().max():.3e}"
+    ref = reference(eng, st, rows, q, layer, [0, H - 1])
+    err = (got[:, [0, H - 1]].float() - ref).norm() / ref.norm()
+    assert err < ATTN_TOL
