@@ -42,8 +42,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--batch", type=int, default=8, help="requests per scheduled batch per GPU")
-    ap.add_argument("--seq", type=int, default=4096)
+    ap.add_argument("--batch", type=int, default=None,
+                    help="requests per scheduled batch per GPU (default 8; 2 for --shape qwen)")
+    ap.add_argument("--seq", type=int, default=None,
+                    help="tokens per request (default 4096; 16384 for --shape qwen, SURVEY 8d cfg3)")
     ap.add_argument("--hit", type=float, default=0.5)
     ap.add_argument("--ratio", type=float, default=0.2)
     ap.add_argument("--sources", type=int, default=16)
@@ -61,6 +63,10 @@ def parse():
         args.layers = {"llama": 32, "qwen": 28, "yi": 48}[args.shape]
     if args.decode_steps is None:
         args.decode_steps = 128 if args.shape == "qwen" else 8
+    if args.seq is None:
+        args.seq = 16384 if args.shape == "qwen" else 4096
+    if args.batch is None:
+        args.batch = 2 if args.shape == "qwen" else 8
     return args
 
 
@@ -757,6 +763,15 @@ def spawn_ranks(args) -> int:
     return subprocess.call(cmd)
 
 
+def l2_note(args) -> str:
+    """Bytes streamed per step against the 126 MB L2 (no flush needed)."""
+    H, G, dm = {"llama": (32, 8, 4096), "qwen": (28, 4, 3584), "yi": (32, 4, 4096)}[args.shape]
+    w = args.layers * (dm * (H + 2 * G) * 128 + H * 128 * dm) * 2
+    kv = args.batch * args.seq * args.layers * 2 * G * 128 * 2
+    return (f"inputs larger than L2 ({w / 1e9:.1f} GB projection weights + {kv / 2**30:.1f} GiB "
+            f"KV streamed per step)")
+
+
 def main():
     args = parse()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
@@ -777,7 +792,7 @@ def main():
                "parallelism": f"dp{args.gpus} (requests partitioned, per-GPU pool)",
                "hand_off": "schedule(queue, N*B)[0] -> partition_batch (owner-of-hit-bytes, "
                            "cost-balanced); admission lookup before the timed loop",
-               "l2": "inputs larger than L2 (2.7 GB weights + 4 GiB KV streamed per step)"}
+               "l2": l2_note(args)}
     if args.impl == "reference":
         if rank != 0:
             return

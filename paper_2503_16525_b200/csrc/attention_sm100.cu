@@ -256,6 +256,27 @@ __global__ void __launch_bounds__(kThreads, kPV ? 1 : 2)
             tc_fence_before();
             mbar_arrive(&sh.s_empty[b]);
             const int kbase = kb * BN;
+            if (!kPV && __all_sync(0xffffffffu, m != -INFINITY)) {
+                // LSE pass (D1 pass 1): exponentials against the running max with
+                // no max pass; only rows whose block sum exceeds 2^8 can hold a
+                // term above 2^8 (fwdp's rule), and only their warps take the
+                // exact path below
+                if (kbase + BN > kend) {
+#pragma unroll
+                    for (int c = 0; c < BN; ++c) s[c] = (kbase + c < kend) ? s[c] : -INFINITY;
+                }
+                float ls[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) ls[j] = 0.f;
+#pragma unroll
+                for (int c = 0; c < BN; ++c) ls[c & 7] += fast_exp2(fmaf(s[c], p.scale_log2, -m));
+                const float bsum =
+                    ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
+                if (!__any_sync(0xffffffffu, !(bsum <= 256.f))) {
+                    l += bsum;
+                    continue;
+                }
+            }
             // row max of the raw scores (scale > 0 commutes with max); the
             // position mask is only evaluated on blocks that cross this row's end
             float mx[8];
@@ -1035,10 +1056,19 @@ __global__ void __launch_bounds__(kThreads2, 1)
                     asm volatile("bar.sync %0, 256;" ::"r"(1 + t) : "memory");
                 float bmax = -INFINITY;
                 if (__all_sync(0xffffffffu, m != -INFINITY)) {
-                    exp_pass(m, true, bmax);
-                    if (__any_sync(0xffffffffu, bmax * p.scale_log2 > m + kRescaleThreshold)) {
-                        rescale(bmax * p.scale_log2);
-                        exp_pass(m, false, bmax);
+                    // speculative pass against the running max with no per-element
+                    // max tracking: a block term above 2^8 forces its sum above
+                    // 2^8, so only rows whose block sum exceeds 2^8 (rare: terms
+                    // are mostly < 1) take the exact max and maybe the redo
+                    exp_pass(m, false, bmax);
+                    const float bsum =
+                        ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
+                    if (__any_sync(0xffffffffu, !(bsum <= 256.f))) {
+                        bmax = row_max();
+                        if (__any_sync(0xffffffffu, bmax * p.scale_log2 > m + kRescaleThreshold)) {
+                            rescale(bmax * p.scale_log2);
+                            exp_pass(m, false, bmax);
+                        }
                     }
                 } else {
                     rescale(row_max() * p.scale_log2);
@@ -1071,15 +1101,16 @@ __global__ void __launch_bounds__(kThreads2, 1)
             mbar_arrive(&sh.item_empty[slot]);
             const float inv = l > 0.f ? 1.f / l : 0.f;
             if (valid) {
-                uint4 *dst = reinterpret_cast<uint4 *>(p.out + (grow * p.num_heads + h) * HD);
+                // 32-byte stores: each fills a whole sector of the row (16-byte
+                // stores of rows 8 KB apart held the LSU ~1.5 us per item)
+                __nv_bfloat16 *dst = p.out + (grow * p.num_heads + h) * HD;
 #pragma unroll
-                for (int v = 0; v < HD / 8; ++v) {
-                    uint4 wv;
-                    wv.x = pack_bf16x2(o[8 * v + 0] * inv, o[8 * v + 1] * inv);
-                    wv.y = pack_bf16x2(o[8 * v + 2] * inv, o[8 * v + 3] * inv);
-                    wv.z = pack_bf16x2(o[8 * v + 4] * inv, o[8 * v + 5] * inv);
-                    wv.w = pack_bf16x2(o[8 * v + 6] * inv, o[8 * v + 7] * inv);
-                    dst[v] = wv;
+                for (int v = 0; v < HD / 16; ++v) {
+                    uint32_t wv[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        wv[j] = pack_bf16x2(o[16 * v + 2 * j] * inv, o[16 * v + 2 * j + 1] * inv);
+                    st_global_v8(dst + 16 * v, wv);
                 }
                 if (p.lse != nullptr)
                     p.lse[grow * p.num_heads + h] =
@@ -1255,62 +1286,83 @@ __global__ void __launch_bounds__(kThreads6, 1)
             for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS + c * 32, s + c * 32);
             tmem_ld_wait();
             const int kbase = kb * BN;
-            float mx[8];
+            if (kbase + BN > kend) {                      // boundary block: position mask
 #pragma unroll
-            for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
-            if (kbase + BN <= kend) {
+                for (int c = 0; c < BN; ++c) s[c] = (kbase + c < kend) ? s[c] : -INFINITY;
+            }
+            float ls[8];
+            auto row_max = [&]() {
+                float mx[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
 #pragma unroll
                 for (int c = 0; c < BN; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
+                return fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                             fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+            };
+            // lazy rescale (threshold 2^8); tcgen05.ld/st are warp-collective, so
+            // the O pass runs for the whole warp when any of its rows needs it
+            auto rescale = [&](float mloc) {
+                const bool grow =
+                    mloc > m + kRescaleThreshold || (m == -INFINITY && mloc > -INFINITY);
+                const bool touch_o = grow && kb >= 1 && m != -INFINITY;
+                float factor = 1.f;
+                if (grow) {
+                    factor = (m == -INFINITY) ? 0.f : fast_exp2(m - mloc);
+                    l *= factor;
+                    m = mloc;
+                }
+                if (__any_sync(0xffffffffu, touch_o)) {
+                    // PV(kb-1) may still run: O is touched only after it retired
+                    mbar_wait(&sh.pv_done[(kb - 1) & 1], (uint32_t)((kb - 1) >> 1) & 1u);
+                    tc_fence_after();
+                    const float f = touch_o ? factor : 1.f;
+                    float o[32];
+#pragma unroll
+                    for (int c = 0; c < HD / 32; ++c) {
+                        tmem_ld32(tO + c * 32, o);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) o[e] *= f;
+                        tmem_st32(tO + c * 32, o);
+                    }
+                    tmem_st_wait();
+                }
+            };
+            auto exp_pass = [&](float mu) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) ls[j] = 0.f;
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf) {
+                    uint32_t pk[32];
+#pragma unroll
+                    for (int q = 0; q < 32; ++q) {
+                        const float e0 = fast_exp2(fmaf(s[hf * 64 + 2 * q], p.scale_log2, -mu));
+                        const float e1 = fast_exp2(fmaf(s[hf * 64 + 2 * q + 1], p.scale_log2, -mu));
+                        ls[(2 * q) & 7] += e0;
+                        ls[(2 * q + 1) & 7] += e1;
+                        pk[q] = pack_bf16x2(e0, e1);
+                    }
+                    tmem_st32(tS + hf * 32, reinterpret_cast<const float *>(pk));
+                }
+            };
+            if (__all_sync(0xffffffffu, m != -INFINITY)) {
+                // speculative pass against the running max (fwdp's rule: only rows
+                // whose block sum exceeds 2^8 can hold a term above 2^8)
+                exp_pass(m);
+                const float bsum =
+                    ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
+                if (__any_sync(0xffffffffu, !(bsum <= 256.f))) {
+                    const float bmax = row_max() * p.scale_log2;
+                    if (__any_sync(0xffffffffu, bmax > m + kRescaleThreshold)) {
+                        tmem_st_wait();                  // P stores done before S is rewritten
+                        rescale(bmax);
+                        exp_pass(m);
+                    }
+                }
             } else {
-#pragma unroll
-                for (int c = 0; c < BN; ++c) {
-                    s[c] = (kbase + c < kend) ? s[c] : -INFINITY;
-                    mx[c & 7] = fmaxf(mx[c & 7], s[c]);
-                }
-            }
-            const float mloc = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                     fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) *
-                               p.scale_log2;
-            const bool grow = mloc > m + kRescaleThreshold || (m == -INFINITY && mloc > -INFINITY);
-            const bool touch_o = grow && kb >= 1 && m != -INFINITY;
-            float factor = 1.f;
-            if (grow) {
-                factor = (m == -INFINITY) ? 0.f : fast_exp2(m - mloc);
-                l *= factor;
-                m = mloc;
-            }
-            if (__any_sync(0xffffffffu, touch_o)) {     // warp-collective tcgen05.ld/st
-                // PV(kb-1) may still run: O is touched only after it retired
-                mbar_wait(&sh.pv_done[(kb - 1) & 1], (uint32_t)((kb - 1) >> 1) & 1u);
-                tc_fence_after();
-                const float f = touch_o ? factor : 1.f;
-                float o[32];
-#pragma unroll
-                for (int c = 0; c < HD / 32; ++c) {
-                    tmem_ld32(tO + c * 32, o);
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int e = 0; e < 32; ++e) o[e] *= f;
-                    tmem_st32(tO + c * 32, o);
-                }
-                tmem_st_wait();
-            }
-            const float mu = (m == -INFINITY) ? 0.f : m;
-            float ls[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) ls[j] = 0.f;
-#pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                uint32_t pk[32];
-#pragma unroll
-                for (int q = 0; q < 32; ++q) {
-                    const float e0 = fast_exp2(fmaf(s[hf * 64 + 2 * q], p.scale_log2, -mu));
-                    const float e1 = fast_exp2(fmaf(s[hf * 64 + 2 * q + 1], p.scale_log2, -mu));
-                    ls[(2 * q) & 7] += e0;
-                    ls[(2 * q + 1) & 7] += e1;
-                    pk[q] = pack_bf16x2(e0, e1);
-                }
-                tmem_st32(tS + hf * 32, reinterpret_cast<const float *>(pk));
+                rescale(row_max() * p.scale_log2);
+                exp_pass((m == -INFINITY) ? 0.f : m);
             }
             l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
             tmem_st_wait();

@@ -33,15 +33,22 @@ lib.kvs_attn_trace_dump.restype = ctypes.c_int32
 lib.kvs_attn_trace_dump.argtypes = [ctypes.c_void_p, ctypes.c_int32]
 from attn_case import build_case  # noqa: E402
 
-n_kb = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+arg = sys.argv[1] if len(sys.argv) > 1 else "4"
 H, G = 32, 8
-reqs = 74
-eng, st, rows, q, layer = build_case(reqs, 128 * n_kb, H, G, 1.0, seed=1, rope_theta=5e5)
-last0 = torch.tensor([int(rows.row_off[r + 1]) - 128 for r in range(reqs)], dtype=torch.int32,
-                     device="cuda")
-rows.tiles = torch.stack([torch.arange(reqs, dtype=torch.int32, device="cuda"), last0,
-                          torch.full((reqs,), 128, dtype=torch.int32, device="cuda")]).contiguous()
-rows.n_tiles = reqs
+if arg == "real":
+    # the bench's DHD row set shape: 8 x 4096 tokens, 60% of positions
+    n_kb = 0
+    eng, st, rows, q, layer = build_case(8, 4096, H, G, 0.6, seed=1, rope_theta=5e5)
+else:
+    n_kb = int(arg)
+    reqs = 74
+    eng, st, rows, q, layer = build_case(reqs, 128 * n_kb, H, G, 1.0, seed=1, rope_theta=5e5)
+    last0 = torch.tensor([int(rows.row_off[r + 1]) - 128 for r in range(reqs)],
+                         dtype=torch.int32, device="cuda")
+    rows.tiles = torch.stack([torch.arange(reqs, dtype=torch.int32, device="cuda"), last0,
+                              torch.full((reqs,), 128, dtype=torch.int32,
+                                         device="cuda")]).contiguous()
+    rows.n_tiles = reqs
 qkv = torch.randn(rows.n_rows, (H + 2 * G) * 128, device="cuda").to(torch.bfloat16)
 o = torch.empty(rows.n_rows, H, 128, dtype=torch.bfloat16, device="cuda")
 fused = os.environ.get("FUSED", "0") == "1"
