@@ -1406,6 +1406,377 @@ __global__ void __launch_bounds__(kThreads6, 1)
     }
 }
 
+// ------------------------------------------------------------------ A1, one head, persistent
+// fwd6's pipeline (one query head, S double-buffered in TMEM, QK(kb+1) under
+// softmax(kb)) in a persistent CTA walking (tile, head) items from a global
+// ticket (fwdp's machinery: warp 4 publishes item metadata and row positions
+// in shared memory).  Q is double-buffered (2 tiles + a 5-tile K/V ring), so
+// item k+1's Q is loaded while item k runs and its first Q.K^T is issued
+// right after item k's last one: the S-buffer alternation and the softmax
+// warps run straight across item boundaries; only item k's epilogue (O read
+// after its last P.V, then the stores) sits between softmax(k, last) and
+// softmax(k+1, 0).  Barrier phases count blocks over the CTA's whole walk.
+constexpr int RING6P = 5;
+
+struct Smem6P {
+    uint64_t q_full[2], q_empty[2];
+    uint64_t ring_full[RING6P], ring_empty[RING6P];
+    uint64_t s_full[2], p_full[2], pv_done[2];
+    uint64_t item_full[3], item_empty[3];
+    uint32_t tmem_base;
+    ItemSlot item[3];
+};
+
+__device__ int g_fwd6p_sched[2];
+
+__global__ void __launch_bounds__(kThreads6, 1)
+    fwd6p_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
+                 Params p, int32_t n_items) {
+    extern __shared__ uint8_t dsmem[];
+    __shared__ Smem6P sh;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int H = p.num_heads, group = p.num_heads / p.kv_heads;
+
+    const uint32_t base = align1024(smem_u32(dsmem));
+    const uint32_t sQ = base;                          // 2 tiles: item k uses Q buffer k & 1
+    const uint32_t sR = sQ + 2 * TILE_BYTES;           // RING6P tiles
+    uint8_t *gbase = dsmem + (base - smem_u32(dsmem));
+
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < RING6P; ++i) {
+            mbar_init(&sh.ring_full[i], 1);
+            mbar_init(&sh.ring_empty[i], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&sh.q_full[b], 1);
+            mbar_init(&sh.q_empty[b], 1);
+            mbar_init(&sh.s_full[b], 1);
+            mbar_init(&sh.p_full[b], 128);
+            mbar_init(&sh.pv_done[b], 1);
+        }
+        for (int j = 0; j < 3; ++j) {
+            mbar_init(&sh.item_full[j], 1);
+            mbar_init(&sh.item_empty[j], 1 + 128);   // MMA lane + softmax threads
+        }
+        fence_barrier_init();
+    }
+    if (warp == 5) tmem_alloc(&sh.tmem_base, 512);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = sh.tmem_base;
+
+    if (warp == 4) {
+        // ------------------------------------------------ tickets, item slots, TMA
+        auto ticket = [&]() {
+            int w = 0;
+            if (lane == 0) w = atomicAdd(&g_fwd6p_sched[0], 1);
+            return __shfl_sync(0xffffffffu, w, 0);
+        };
+        auto publish = [&](int k, int w) {           // item k = work item w -> slot k % 3
+            const int s = k % 3;
+            if (k >= 3) mbar_wait(&sh.item_empty[s], (uint32_t)((k / 3) - 1) & 1u);
+            ItemSlot &it = sh.item[s];
+            if (w < n_items) {
+                const int tile = w / H;
+                const int req = __ldg(p.tile_req + tile), row0 = __ldg(p.tile_row0 + tile);
+                const int nrows = __ldg(p.tile_rows + tile);
+#pragma unroll
+                for (int r = lane; r < BM; r += 32)
+                    it.pos[r] = r < nrows ? __ldg(p.row_pos + row0 + r) : 0;
+                if (lane == 0) {
+                    const int kmax = p.causal ? __ldg(p.row_pos + row0 + nrows - 1) + 1
+                                              : __ldg(p.kv_len + req);
+                    it.req = req;
+                    it.row0 = row0;
+                    it.nrows = nrows;
+                    it.kmax = kmax;
+                    it.n_kb = (kmax + BN - 1) / BN;
+                    it.h0 = w - tile * H;
+                }
+            }
+            if (lane == 0) it.w = w;
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&sh.item_full[s]);
+        };
+        auto load_q = [&](int k) {                   // item k's Q into buffer k & 1
+            const ItemSlot &it = sh.item[k % 3];
+            if (lane == 0 && it.w < n_items) {
+                const int b = k & 1;
+                if (k >= 2) mbar_wait(&sh.q_empty[b], (uint32_t)((k >> 1) - 1) & 1u);
+                mbar_expect_tx(&sh.q_full[b], TILE_BYTES);
+                for (int hf = 0; hf < 2; ++hf)
+                    tma_load_3d(gbase + b * TILE_BYTES + hf * HALF_BYTES, &map_q, &sh.q_full[b],
+                                hf * 64, it.h0, it.row0);
+            }
+        };
+        if (lane == 0) {
+            tma_prefetch(&map_q);
+            tma_prefetch(&map_kv);
+        }
+        int w = ticket();
+        publish(0, w);
+        load_q(0);
+        int gb = 0, k = 0;
+        while (w < n_items) {
+            const ItemSlot &it = sh.item[k % 3];
+            const int req = it.req, n_kb = it.n_kb, kmax = it.kmax, gk = it.h0 / group;
+            int wn = 0;
+            const int pages_needed = (kmax + p.page_size - 1) / p.page_size;
+            const int32_t *bt = p.block_table + (int64_t)req * p.max_pages;
+            for (int i2 = 0; i2 < 2 * n_kb; ++i2) {
+                if (lane == 0) {
+                    const int git = 2 * gb + i2, kb = i2 >> 1, kv = i2 & 1, slot = git % RING6P;
+                    if (git >= RING6P)
+                        mbar_wait(&sh.ring_empty[slot], (uint32_t)((git / RING6P) - 1) & 1u);
+                    mbar_expect_tx(&sh.ring_full[slot], TILE_BYTES);
+                    for (int q = 0; q < 2; ++q) {
+                        const int pi = 2 * kb + q;
+                        const int pg = bt[pi < pages_needed ? pi : 2 * kb];
+                        for (int hf = 0; hf < 2; ++hf)
+                            tma_load_4d(gbase + (sR - base) + slot * TILE_BYTES + hf * HALF_BYTES +
+                                            q * (HALF_BYTES / 2),
+                                        &map_kv, &sh.ring_full[slot], hf * 64, gk, 0,
+                                        (pg * p.num_layers + p.layer) * 2 + kv);
+                    }
+                }
+                if (i2 == 1) {
+                    // item k's first tiles are in flight: claim item k+1, publish
+                    // it and start its Q load (buffer (k+1) & 1)
+                    wn = ticket();
+                    publish(k + 1, wn);
+                    load_q(k + 1);
+                }
+            }
+            gb += n_kb;
+            w = wn;
+            ++k;
+        }
+        if (lane == 0 && atomicAdd(&g_fwd6p_sched[1], 1) == (int)gridDim.x - 1) {
+            atomicExch(&g_fwd6p_sched[0], 0);
+            atomicExch(&g_fwd6p_sched[1], 0);
+        }
+    } else if (warp == 5) {
+        if (lane == 0) {
+            // ------------------------------------------------ MMA issuer
+            const uint32_t idesc_qk = umma_idesc_bf16(BM, BN, false);
+            const uint32_t idesc_pv = umma_idesc_bf16(BM, HD, true);
+            // QK of global block g (item buffer qb) into S[g & 1]
+            auto issue_qk = [&](int g, int qb) {
+                const int it = 2 * g, slot = it % RING6P;
+                mbar_wait(&sh.ring_full[slot], (uint32_t)(it / RING6P) & 1u);
+                tc_fence_after();
+#pragma unroll
+                for (int k2 = 0; k2 < HD / 16; ++k2) {
+                    const uint64_t da = umma_desc_sw128(
+                        sQ + qb * TILE_BYTES + (k2 >> 2) * HALF_BYTES + (k2 & 3) * 32, 16, 1024);
+                    const uint64_t db = umma_desc_sw128(
+                        sR + slot * TILE_BYTES + (k2 >> 2) * HALF_BYTES + (k2 & 3) * 32, 16, 1024);
+                    umma_bf16(tmem + 128 * (g & 1), da, db, idesc_qk, k2 > 0 ? 1u : 0u);
+                }
+                umma_commit(&sh.s_full[g & 1]);
+                umma_commit(&sh.ring_empty[slot]);
+            };
+            auto issue_pv = [&](int g, bool first) {
+                const int it = 2 * g + 1, slot = it % RING6P, b = g & 1;
+                mbar_wait(&sh.p_full[b], (uint32_t)(g >> 1) & 1u);
+                mbar_wait(&sh.ring_full[slot], (uint32_t)(it / RING6P) & 1u);
+                tc_fence_after();
+#pragma unroll
+                for (int k2 = 0; k2 < BN / 16; ++k2) {
+                    const uint64_t db = umma_desc_sw128(sR + slot * TILE_BYTES + k2 * 2048,
+                                                        HALF_BYTES, 1024);
+                    umma_bf16_ts(tmem + 256, tmem + 128 * b + 8 * k2, db, idesc_pv,
+                                 (!first || k2 > 0) ? 1u : 0u);
+                }
+                umma_commit(&sh.pv_done[b]);
+                umma_commit(&sh.ring_empty[slot]);
+            };
+            int gb = 0;
+            bool qk0_done = false;                   // item k's first QK issued under item k-1
+            for (int k = 0;; ++k) {
+                const int s = k % 3;
+                mbar_wait(&sh.item_full[s], (uint32_t)(k / 3) & 1u);
+                const int w = sh.item[s].w, n_kb = sh.item[s].n_kb;
+                mbar_arrive(&sh.item_empty[s]);
+                if (w >= n_items) break;
+                if (!qk0_done) {
+                    mbar_wait(&sh.q_full[k & 1], (uint32_t)(k >> 1) & 1u);
+                    issue_qk(gb, k & 1);
+                    if (n_kb == 1) umma_commit(&sh.q_empty[k & 1]);
+                }
+                qk0_done = false;
+                for (int kb = 0; kb < n_kb; ++kb) {
+                    const int g = gb + kb;
+                    if (kb + 1 < n_kb) {
+                        issue_qk(g + 1, k & 1);
+                        if (kb + 2 == n_kb) umma_commit(&sh.q_empty[k & 1]);
+                    } else {
+                        // the next item's first QK goes ahead of this item's last P.V
+                        const int s1 = (k + 1) % 3;
+                        mbar_wait(&sh.item_full[s1], (uint32_t)((k + 1) / 3) & 1u);
+                        if (sh.item[s1].w < n_items) {
+                            mbar_wait(&sh.q_full[(k + 1) & 1], (uint32_t)((k + 1) >> 1) & 1u);
+                            issue_qk(g + 1, (k + 1) & 1);
+                            if (sh.item[s1].n_kb == 1) umma_commit(&sh.q_empty[(k + 1) & 1]);
+                            qk0_done = true;
+                        }
+                    }
+                    issue_pv(g, kb == 0);
+                }
+                gb += n_kb;
+            }
+        }
+        __syncwarp();
+    } else {
+        // ------------------------------------------------ softmax warps 0-3
+        const int i = threadIdx.x;               // row within tile == TMEM lane
+        const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+        const uint32_t tO = tmem + 256 + lane_off;
+        int gb = 0, k = 0;
+        for (;; ++k) {
+            const int slot = k % 3;
+            mbar_wait(&sh.item_full[slot], (uint32_t)(k / 3) & 1u);
+            if (sh.item[slot].w >= n_items) {
+                mbar_arrive(&sh.item_empty[slot]);
+                break;
+            }
+            const int n_kb = sh.item[slot].n_kb;
+            const int kend = i >= sh.item[slot].nrows ? 0
+                             : (p.causal ? sh.item[slot].pos[i] + 1 : sh.item[slot].kmax);
+            float m = -INFINITY, l = 0.f;
+            float s[BN];
+            for (int kb = 0; kb < n_kb; ++kb) {
+                const int g = gb + kb, b = g & 1;
+                const uint32_t tS = tmem + 128 * b + lane_off;
+                mbar_wait(&sh.s_full[b], (uint32_t)(g >> 1) & 1u);
+                tc_fence_after();
+#pragma unroll
+                for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS + c * 32, s + c * 32);
+                tmem_ld_wait();
+                const int kbase = kb * BN;
+                if (kbase + BN > kend) {
+#pragma unroll
+                    for (int c = 0; c < BN; ++c) s[c] = (kbase + c < kend) ? s[c] : -INFINITY;
+                }
+                float ls[8];
+                auto row_max = [&]() {
+                    float mx[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) mx[j] = -INFINITY;
+#pragma unroll
+                    for (int c = 0; c < BN; ++c) mx[c & 7] = fmaxf(mx[c & 7], s[c]);
+                    return fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+                };
+                auto rescale = [&](float mloc) {
+                    const bool grow =
+                        mloc > m + kRescaleThreshold || (m == -INFINITY && mloc > -INFINITY);
+                    const bool touch_o = grow && kb >= 1 && m != -INFINITY;
+                    float factor = 1.f;
+                    if (grow) {
+                        factor = (m == -INFINITY) ? 0.f : fast_exp2(m - mloc);
+                        l *= factor;
+                        m = mloc;
+                    }
+                    if (__any_sync(0xffffffffu, touch_o)) {
+                        // PV(g-1) may still run: O is touched only after it retired
+                        mbar_wait(&sh.pv_done[(g - 1) & 1], (uint32_t)((g - 1) >> 1) & 1u);
+                        tc_fence_after();
+                        const float f = touch_o ? factor : 1.f;
+                        float o[32];
+#pragma unroll
+                        for (int c = 0; c < HD / 32; ++c) {
+                            tmem_ld32(tO + c * 32, o);
+                            tmem_ld_wait();
+#pragma unroll
+                            for (int e = 0; e < 32; ++e) o[e] *= f;
+                            tmem_st32(tO + c * 32, o);
+                        }
+                        tmem_st_wait();
+                    }
+                };
+                auto exp_pass = [&](float mu) {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) ls[j] = 0.f;
+#pragma unroll
+                    for (int hf = 0; hf < 2; ++hf) {
+                        uint32_t pk[32];
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) {
+                            const float e0 = fast_exp2(fmaf(s[hf * 64 + 2 * q], p.scale_log2, -mu));
+                            const float e1 =
+                                fast_exp2(fmaf(s[hf * 64 + 2 * q + 1], p.scale_log2, -mu));
+                            ls[(2 * q) & 7] += e0;
+                            ls[(2 * q + 1) & 7] += e1;
+                            pk[q] = pack_bf16x2(e0, e1);
+                        }
+                        tmem_st32(tS + hf * 32, reinterpret_cast<const float *>(pk));
+                    }
+                };
+                if (__all_sync(0xffffffffu, m != -INFINITY)) {
+                    exp_pass(m);
+                    const float bsum =
+                        ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
+                    if (__any_sync(0xffffffffu, !(bsum <= 256.f))) {
+                        const float bmax = row_max() * p.scale_log2;
+                        if (__any_sync(0xffffffffu, bmax > m + kRescaleThreshold)) {
+                            tmem_st_wait();
+                            rescale(bmax);
+                            exp_pass(m);
+                        }
+                    }
+                } else {
+                    rescale(row_max() * p.scale_log2);
+                    exp_pass((m == -INFINITY) ? 0.f : m);
+                }
+                l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
+                tmem_st_wait();
+                tc_fence_before();
+                mbar_arrive(&sh.p_full[b]);
+                // consume PV(g-1)'s phase (free: it ran under this block's softmax)
+                if (kb >= 1) mbar_wait(&sh.pv_done[(g - 1) & 1], (uint32_t)((g - 1) >> 1) & 1u);
+            }
+            // epilogue: O after the item's last P.V, read before the next item's
+            // first P.V (issued only after this thread's next p_full arrival)
+            const int gl = gb + n_kb - 1;
+            mbar_wait(&sh.pv_done[gl & 1], (uint32_t)(gl >> 1) & 1u);
+            tc_fence_after();
+            float o[HD];
+#pragma unroll
+            for (int c = 0; c < HD / 32; ++c) tmem_ld32(tO + c * 32, o + c * 32);
+            tmem_ld_wait();
+            tc_fence_before();
+            const int64_t grow = (int64_t)sh.item[slot].row0 + i;
+            const int h = sh.item[slot].h0;
+            const bool valid = i < sh.item[slot].nrows;
+            mbar_arrive(&sh.item_empty[slot]);
+            const float inv = l > 0.f ? 1.f / l : 0.f;
+            if (valid) {
+                __nv_bfloat16 *dst = p.out + (grow * p.num_heads + h) * HD;
+#pragma unroll
+                for (int v = 0; v < HD / 16; ++v) {
+                    uint32_t wv[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        wv[j] = pack_bf16x2(o[16 * v + 2 * j] * inv, o[16 * v + 2 * j + 1] * inv);
+                    st_global_v8(dst + 16 * v, wv);
+                }
+                if (p.lse != nullptr)
+                    p.lse[grow * p.num_heads + h] =
+                        (l > 0.f) ? (m + __log2f(l)) * 0.6931471805599453f : -INFINITY;
+            }
+            gb += n_kb;
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 5) {
+        tc_fence_after();
+        tmem_dealloc(tmem, 512);
+    }
+}
+
 // ------------------------------------------------------------------ D1 pass 2
 // CTA = (key tile kt of request r, kv head g).  Loops over the group's query
 // heads and the query tiles that can see the keys; S^T lands with one key per
@@ -1659,12 +2030,19 @@ static kvs_status attention_fwd_impl(const void *q, int64_t q_row_stride, const 
     cudaStream_t s = (cudaStream_t)stream;
     const int group = num_heads / arena->kv_heads;
     const char *variant = getenv("KVS_ATTN");
-    // default: persistent head pairs (fwdp) for even GQA groups, single heads
-    // with double-buffered S (fwd6) otherwise; KVS_ATTN=1|3|6|p pins a variant
-    // (1: the single-head kernel with P through shared memory, 3: one-shot
-    // head-pair CTAs)
-    const char v = variant != nullptr ? variant[0] : (group % 2 == 0 ? 'p' : '6');
-    if (out != nullptr && (v == '6' || (v != '1' && group % 2 != 0))) {
+    // default: persistent head pairs (fwdp) for even GQA groups, persistent
+    // single heads with double-buffered S (fwd6p; fwd6 when Q is rotated in
+    // the kernel) otherwise; KVS_ATTN=1|3|6|p|q pins a variant (1: the
+    // single-head kernel with P through shared memory, 3 / 6: one-shot CTAs)
+    const char v = variant != nullptr ? variant[0] : (group % 2 == 0 ? 'p' : 'q');
+    if (out != nullptr && rope == nullptr && (v == 'q' || (v == 'p' && group % 2 != 0))) {
+        const size_t smem = 1024 + attn::TILE_BYTES * (2 + attn::RING6P);
+        cudaFuncSetAttribute(attn::fwd6p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem);
+        const int n_items = n_tiles * num_heads;
+        attn::fwd6p_kernel<<<std::min(n_items, kNumSMs), attn::kThreads6, smem, s>>>(mq, mkv, p,
+                                                                                    n_items);
+    } else if (out != nullptr && (v == '6' || v == 'q' || (v != '1' && group % 2 != 0))) {
         const size_t smem = 1024 + attn::TILE_BYTES * (1 + attn::RING6);
         cudaFuncSetAttribute(attn::fwd6_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
