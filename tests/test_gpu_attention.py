@@ -75,3 +75,22 @@ def test_attention_qkv_fused_rope_bit_exact(R, n, H, G, frac):
     ref = reference(eng, st, rows, q, layer, [0, H - 1])
     err = (got[:, [0, H - 1]].float() - ref).norm() / ref.norm()
     assert err < ATTN_TOL
+
+
+@pytest.mark.parametrize("R,n,H,G,frac,one_shot", [
+    (8, 1500, 32, 8, 0.6, "3"), (2, 3000, 28, 4, 0.55, "6"), (1, 300, 8, 1, 1.0, "6"),
+    (1, 129, 2, 1, 1.0, "3")])
+def test_persistent_kernels_match_one_shot(R, n, H, G, frac, one_shot, monkeypatch):
+    """The persistent kernels (fwdp for even GQA groups, fwd6p for odd) walk
+    ticketed (tile, head) items; each item's arithmetic is the one-shot
+    kernel's (fwd3 / fwd6), so outputs are bit-identical, and a second launch
+    (the ticket counter reset by the previous launch's last CTA) repeats them."""
+    eng, st, rows, q, layer = build_case(R, n, H, G, frac, seed=R * n + G)
+    monkeypatch.delenv("KVS_ATTN", raising=False)
+    got = _run(eng, st, rows, q, layer)
+    again = _run(eng, st, rows, q, layer)
+    monkeypatch.setenv("KVS_ATTN", one_shot)
+    want = _run(eng, st, rows, q, layer)
+    assert torch.equal(got, again), "persistent kernel not deterministic across launches"
+    assert torch.equal(got, want), \
+        f"persistent vs one-shot: max |d| {(got.float() - want.float()).abs().max():.3e}"
