@@ -1005,8 +1005,13 @@ __global__ void __launch_bounds__(kThreads2, 1)
                         for (int q = 0; q < 32; ++q) {
                             const float s0 = s[hf * 64 + 2 * q], s1 = s[hf * 64 + 2 * q + 1];
                             if (track) mx[q & 7] = fmaxf(mx[q & 7], fmaxf(s0, s1));
-                            const float e0 = fast_exp2(fmaf(s0, p.scale_log2, -mu));
-                            const float e1 = fast_exp2(fmaf(s1, p.scale_log2, -mu));
+                            const float x0 = fmaf(s0, p.scale_log2, -mu);
+                            const float x1 = fmaf(s1, p.scale_log2, -mu);
+                            // every kPolyEvery-th pair on the FMA pipe (0: all on MUFU)
+                            const bool poly = kPolyEvery > 0 &&
+                                              q % (kPolyEvery > 0 ? kPolyEvery : 1) == kPolyEvery - 1;
+                            const float e0 = poly ? exp2_poly(x0) : fast_exp2(x0);
+                            const float e1 = poly ? exp2_poly(x1) : fast_exp2(x1);
                             ls[(2 * q) & 7] += e0;
                             ls[(2 * q + 1) & 7] += e1;
                             pk[q] = pack_bf16x2(e0, e1);
