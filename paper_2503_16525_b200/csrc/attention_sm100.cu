@@ -726,6 +726,14 @@ __global__ void __launch_bounds__(kThreads2, 1)
 //     it (accumulate = 0) before the normalised rows are stored.
 // Barrier phases count blocks (s_full, p_full, ring) or items (q_*, pv_done,
 // o_free, item slots) over the CTA's whole walk.
+// exp-phase coupling of the two heads: 0 = none (both heads' softmax warps
+// share each SMSP freely), 1 = strict ping-pong (one head's exp phase at a
+// time), 2 = half offset (a head starts when the other is half done)
+#ifndef KVS_PP_P
+#define KVS_PP_P 0
+#endif
+constexpr int kPingPongP = KVS_PP_P;
+
 struct ItemSlot {
     int w, req, row0, nrows, n_kb, kmax, h0, pad;
     int pos[BM];
@@ -991,7 +999,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
                     for (int c = 0; c < BN; ++c) s[c] = (kbase + c < kend) ? s[c] : -INFINITY;
                 }
                 float ls[8];
-                auto exp_pass = [&](float mu, bool track, float &bmax) {
+                auto exp_pass = [&](float mu, bool track, float &bmax, bool hook) {
                     float mx[8];
 #pragma unroll
                     for (int j = 0; j < 8; ++j) {
@@ -1017,6 +1025,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
                             pk[q] = pack_bf16x2(e0, e1);
                         }
                         tmem_st32(tS + hf * 32, reinterpret_cast<const float *>(pk));
+                        if (kPingPongP == 2 && hook && hf == 0)
+                            asm volatile("bar.arrive %0, 256;" ::"r"(2 - t) : "memory");
                     }
                     if (track)
                         bmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
@@ -1057,7 +1067,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 };
                 // ping-pong over the CTA's whole walk: head 1 waits on head 0's
                 // exp phase of the same block, head 0 on head 1's previous one
-                if (kPingPong && (t == 1 || gk > 0))
+                if (kPingPongP != 0 && (t == 1 || gk > 0))
                     asm volatile("bar.sync %0, 256;" ::"r"(1 + t) : "memory");
                 float bmax = -INFINITY;
                 if (__all_sync(0xffffffffu, m != -INFINITY)) {
@@ -1065,21 +1075,21 @@ __global__ void __launch_bounds__(kThreads2, 1)
                     // max tracking: a block term above 2^8 forces its sum above
                     // 2^8, so only rows whose block sum exceeds 2^8 (rare: terms
                     // are mostly < 1) take the exact max and maybe the redo
-                    exp_pass(m, false, bmax);
+                    exp_pass(m, false, bmax, true);
                     const float bsum =
                         ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
                     if (__any_sync(0xffffffffu, !(bsum <= 256.f))) {
                         bmax = row_max();
                         if (__any_sync(0xffffffffu, bmax * p.scale_log2 > m + kRescaleThreshold)) {
                             rescale(bmax * p.scale_log2);
-                            exp_pass(m, false, bmax);
+                            exp_pass(m, false, bmax, false);
                         }
                     }
                 } else {
                     rescale(row_max() * p.scale_log2);
-                    exp_pass((m == -INFINITY) ? 0.f : m, false, bmax);
+                    exp_pass((m == -INFINITY) ? 0.f : m, false, bmax, true);
                 }
-                if (kPingPong) asm volatile("bar.arrive %0, 256;" ::"r"(2 - t) : "memory");
+                if (kPingPongP == 1) asm volatile("bar.arrive %0, 256;" ::"r"(2 - t) : "memory");
                 l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
                 tmem_st_wait();
                 tc_fence_before();
@@ -1127,7 +1137,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
         }
         mbar_arrive(&sh.item_empty[k % 3]);       // the terminal slot
         // consume head 1's last exp-phase arrival
-        if (kPingPong && t == 0 && gb >= 1) asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (kPingPongP != 0 && t == 0 && gb >= 1) asm volatile("bar.sync 1, 256;" ::: "memory");
     }
     tc_fence_before();
     __syncthreads();
