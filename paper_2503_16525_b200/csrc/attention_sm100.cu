@@ -269,7 +269,11 @@ __global__ void __launch_bounds__(kThreads, kPV ? 1 : 2)
 #pragma unroll
                 for (int j = 0; j < 8; ++j) ls[j] = 0.f;
 #pragma unroll
-                for (int c = 0; c < BN; ++c) ls[c & 7] += fast_exp2(fmaf(s[c], p.scale_log2, -m));
+                for (int c = 0; c < BN; c += 2) {
+                    float x0, x1;
+                    fma2(x0, x1, s[c], s[c + 1], p.scale_log2, p.scale_log2, -m, -m);
+                    add2(ls[c & 7], ls[(c + 1) & 7], fast_exp2(x0), fast_exp2(x1));
+                }
                 const float bsum =
                     ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
                 if (!__any_sync(0xffffffffu, !(bsum <= 256.f))) {
@@ -1013,15 +1017,14 @@ __global__ void __launch_bounds__(kThreads2, 1)
                         for (int q = 0; q < 32; ++q) {
                             const float s0 = s[hf * 64 + 2 * q], s1 = s[hf * 64 + 2 * q + 1];
                             if (track) mx[q & 7] = fmaxf(mx[q & 7], fmaxf(s0, s1));
-                            const float x0 = fmaf(s0, p.scale_log2, -mu);
-                            const float x1 = fmaf(s1, p.scale_log2, -mu);
+                            float x0, x1;
+                            fma2(x0, x1, s0, s1, p.scale_log2, p.scale_log2, -mu, -mu);
                             // every kPolyEvery-th pair on the FMA pipe (0: all on MUFU)
                             const bool poly = kPolyEvery > 0 &&
                                               q % (kPolyEvery > 0 ? kPolyEvery : 1) == kPolyEvery - 1;
                             const float e0 = poly ? exp2_poly(x0) : fast_exp2(x0);
                             const float e1 = poly ? exp2_poly(x1) : fast_exp2(x1);
-                            ls[(2 * q) & 7] += e0;
-                            ls[(2 * q + 1) & 7] += e1;
+                            add2(ls[(2 * q) & 7], ls[(2 * q + 1) & 7], e0, e1);
                             pk[q] = pack_bf16x2(e0, e1);
                         }
                         tmem_st32(tS + hf * 32, reinterpret_cast<const float *>(pk));
@@ -1352,10 +1355,11 @@ __global__ void __launch_bounds__(kThreads6, 1)
                     uint32_t pk[32];
 #pragma unroll
                     for (int q = 0; q < 32; ++q) {
-                        const float e0 = fast_exp2(fmaf(s[hf * 64 + 2 * q], p.scale_log2, -mu));
-                        const float e1 = fast_exp2(fmaf(s[hf * 64 + 2 * q + 1], p.scale_log2, -mu));
-                        ls[(2 * q) & 7] += e0;
-                        ls[(2 * q + 1) & 7] += e1;
+                        float x0, x1;
+                        fma2(x0, x1, s[hf * 64 + 2 * q], s[hf * 64 + 2 * q + 1], p.scale_log2,
+                             p.scale_log2, -mu, -mu);
+                        const float e0 = fast_exp2(x0), e1 = fast_exp2(x1);
+                        add2(ls[(2 * q) & 7], ls[(2 * q + 1) & 7], e0, e1);
                         pk[q] = pack_bf16x2(e0, e1);
                     }
                     tmem_st32(tS + hf * 32, reinterpret_cast<const float *>(pk));
@@ -1719,11 +1723,11 @@ __global__ void __launch_bounds__(kThreads6, 1)
                         uint32_t pk[32];
 #pragma unroll
                         for (int q = 0; q < 32; ++q) {
-                            const float e0 = fast_exp2(fmaf(s[hf * 64 + 2 * q], p.scale_log2, -mu));
-                            const float e1 =
-                                fast_exp2(fmaf(s[hf * 64 + 2 * q + 1], p.scale_log2, -mu));
-                            ls[(2 * q) & 7] += e0;
-                            ls[(2 * q + 1) & 7] += e1;
+                            float x0, x1;
+                            fma2(x0, x1, s[hf * 64 + 2 * q], s[hf * 64 + 2 * q + 1], p.scale_log2,
+                                 p.scale_log2, -mu, -mu);
+                            const float e0 = fast_exp2(x0), e1 = fast_exp2(x1);
+                            add2(ls[(2 * q) & 7], ls[(2 * q + 1) & 7], e0, e1);
                             pk[q] = pack_bf16x2(e0, e1);
                         }
                         tmem_st32(tS + hf * 32, reinterpret_cast<const float *>(pk));
@@ -1933,13 +1937,21 @@ __global__ void __launch_bounds__(kThreads, 2)
             if (!p.causal || qbase >= k0 + BM - 1) {
                 // every query of this tile sees every key of the key tile
 #pragma unroll
-                for (int c = 0; c < BN; ++c)
-                    ps[c & 7] += fast_exp2(fmaf(s[c], p.scale_log2, -s_lse[b][c]));
+                for (int c = 0; c < BN; c += 2) {
+                    float x0, x1;
+                    fma2(x0, x1, s[c], s[c + 1], p.scale_log2, p.scale_log2, -s_lse[b][c],
+                         -s_lse[b][c + 1]);
+                    add2(ps[c & 7], ps[(c + 1) & 7], fast_exp2(x0), fast_exp2(x1));
+                }
             } else {
 #pragma unroll
-                for (int c = 0; c < BN; ++c) {
-                    const float e = fast_exp2(fmaf(s[c], p.scale_log2, -s_lse[b][c]));
-                    ps[c & 7] += (qbase + c >= kpos) ? e : 0.f;
+                for (int c = 0; c < BN; c += 2) {
+                    float x0, x1;
+                    fma2(x0, x1, s[c], s[c + 1], p.scale_log2, p.scale_log2, -s_lse[b][c],
+                         -s_lse[b][c + 1]);
+                    const float e0 = fast_exp2(x0), e1 = fast_exp2(x1);
+                    add2(ps[c & 7], ps[(c + 1) & 7], (qbase + c >= kpos) ? e0 : 0.f,
+                         (qbase + c + 1 >= kpos) ? e1 : 0.f);
                 }
             }
             const float part = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));

@@ -78,6 +78,24 @@ __device__ __forceinline__ float fast_exp2(float x) {
     return y;
 }
 
+// Packed fp32 pairs (sm_100 FFMA2 / FADD2): two lanes of work per instruction,
+// each rounded exactly like the scalar fmaf / fadd it replaces.
+__device__ __forceinline__ void fma2(float &o0, float &o1, float a0, float a1, float b0, float b1,
+                                     float c0, float c1) {
+    asm("{\n.reg .b64 A, B, C, D;\n"
+        "mov.b64 A, {%2, %3};\nmov.b64 B, {%4, %5};\nmov.b64 C, {%6, %7};\n"
+        "fma.rn.f32x2 D, A, B, C;\nmov.b64 {%0, %1}, D;\n}"
+        : "=f"(o0), "=f"(o1)
+        : "f"(a0), "f"(a1), "f"(b0), "f"(b1), "f"(c0), "f"(c1));
+}
+__device__ __forceinline__ void add2(float &a0, float &a1, float b0, float b1) {
+    asm("{\n.reg .b64 A, B, D;\n"
+        "mov.b64 A, {%0, %1};\nmov.b64 B, {%2, %3};\n"
+        "add.rn.f32x2 D, A, B;\nmov.b64 {%0, %1}, D;\n}"
+        : "+f"(a0), "+f"(a1)
+        : "f"(b0), "f"(b1));
+}
+
 // 2^x on the FMA pipe (no MUFU): round-to-nearest split x = j + f with the
 // 1.5*2^23 magic add, cubic minimax for 2^f on [-0.5, 0.5] (relative error
 // 7.5e-5, far below the bf16 rounding of P), exponent add for 2^j.  Used for
