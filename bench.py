@@ -614,8 +614,10 @@ def select_batch_leg(n_req: int, seq: int = 4096, hit: float = 0.5, ratio: float
                      iters: int = 10):
     """D2 (kvs_dhd_select) on a larger scheduled batch than the step's, as
     SURVEY 8d asks ("measure batched over all requests of a scheduled batch"):
-    n_req Llama-shape requests (kv_heads 8, head dim 128) with reused spans of
-    64-1024 tokens covering ~hit of each, a 2-layer arena (D2 reads the probe
+    n_req Llama-shape requests (kv_heads 8, head dim 128) drawn from the same
+    seeded multi-tenant stream as the step (workload.request_batches: spans of
+    64-1024 tokens copied from 16 pooled sources at the given hit rate), hit
+    maps from the real pool lookup (R2), a 2-layer arena (D2 reads the probe
     layer only), L2 flushed before every launch, CUDA events around each
     launch.  Returns the achieved algorithmic GB/s."""
     import torch
@@ -623,25 +625,22 @@ def select_batch_leg(n_req: int, seq: int = 4096, hit: float = 0.5, ratio: float
     from paper_2503_16525_b200 import _native as N
     from paper_2503_16525_b200.engine import Engine
     from paper_2503_16525_b200.pool import CachePool, KVArena
+    from paper_2503_16525_b200.workload import request_batches, source_requests
     dev = torch.device("cuda", torch.cuda.current_device())
     shape = dict(K.LLAMA31_8B)
-    shape.update(num_layers=2, vocab_size=1000)
+    shape.update(num_layers=2)
     cfg = K.ModelConfig(**shape, max_positions=seq + 64)
-    arena = KVArena(cfg, n_req * ((seq + 63) // 64) + 4)
+    n_src = 16
+    arena = KVArena(cfg, (n_req + n_src) * ((seq + 63) // 64) + 4)
     eng = Engine(K.ToyModel(cfg, init="device"), CachePool(cfg, arena=arena))
-    rng = np.random.default_rng(0)
-    st = eng.new_batch([rng.integers(0, 1000, seq) for _ in range(n_req)])
+    sources = source_requests(n_src, seq, cfg.vocab_size, seed=0)
+    st_src = eng.new_batch(sources)
+    eng.write_back(st_src, [f"src{j}" for j in range(n_src)])    # zero-copy pool entries
+    st = eng.new_batch(request_batches(sources, 1, n_req, seq, hit, cfg.vocab_size, seed=5)[0])
+    eng.lookup(st)                                   # R2: the real hit maps
     arena.data.normal_()
     n = n_req * seq
-    src = np.full(n, -1, dtype=np.int32)
-    for r in range(n_req):
-        p = 0
-        while p < seq:
-            span = int(rng.integers(64, 1025))
-            if rng.random() < hit:
-                src[r * seq + p: r * seq + min(seq, p + span)] = 0
-            p += span
-    st.src_slot = torch.from_numpy(src).to(dev)
+    src = st.src_slot.cpu().numpy()
     v_true = (torch.randn(n, cfg.kv_heads, 128, device=dev) * 0.5).to(torch.bfloat16)
     alpha = torch.rand(n, device=dev)
     n_hit = np.array([(src[r * seq:(r + 1) * seq] >= 0).sum() for r in range(n_req)])
@@ -668,9 +667,10 @@ def select_batch_leg(n_req: int, seq: int = 4096, hit: float = 0.5, ratio: float
         if it >= 2:
             ts.append(e0.elapsed_time(e1))
     ms = float(np.median(ts))
-    del arena, eng, st, v_true, flush
+    del arena, eng, st, st_src, v_true, flush
     torch.cuda.empty_cache()
     return {"requests": n_req, "reused_rows": int(n_hit.sum()), "algorithmic_bytes": nbytes,
+            "data": "workload.request_batches stream, hit maps from the pool lookup",
             "ms": ms, "achieved": nbytes / (ms / 1000.0) / 1e9, "unit": "GB/s"}
 
 

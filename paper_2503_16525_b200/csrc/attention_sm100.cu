@@ -84,8 +84,8 @@ struct RopeRow {
         const float4 *s4 = reinterpret_cast<const float4 *>(sin_t + (size_t)pos * 64);
 #pragma unroll
         for (int k = 0; k < 16; ++k) {
-            c[k] = __ldg(c4 + k);
-            s[k] = __ldg(s4 + k);
+            c[k] = c4[k];
+            s[k] = s4[k];
         }
     }
     __device__ __forceinline__ void apply(uint8_t *tile, int i) const {
@@ -786,7 +786,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
             mbar_init(&sh.o_free[t], 128);
         }
         for (int j = 0; j < 3; ++j) {
-            mbar_init(&sh.item_full[j], 1);
+            mbar_init(&sh.item_full[j], 32);   // every producer lane releases its writes
             mbar_init(&sh.item_empty[j], 1 + 256);   // MMA lane + softmax threads
         }
         fence_barrier_init();
@@ -829,8 +829,8 @@ __global__ void __launch_bounds__(kThreads2, 1)
                     }
                 }
                 if (lane == 0) it.w = w;
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&sh.item_full[s]);
+                mbar_arrive(&sh.item_full[s]);
+                __syncwarp();                        // lane 0's fields, for the warp's own reads
             };
             if (lane == 0) {
                 tma_prefetch(&map_q);
@@ -1474,7 +1474,7 @@ __global__ void __launch_bounds__(kThreads6, 1)
             mbar_init(&sh.pv_done[b], 1);
         }
         for (int j = 0; j < 3; ++j) {
-            mbar_init(&sh.item_full[j], 1);
+            mbar_init(&sh.item_full[j], 32);   // every producer lane releases its writes
             mbar_init(&sh.item_empty[j], 1 + 128);   // MMA lane + softmax threads
         }
         fence_barrier_init();
@@ -1515,8 +1515,8 @@ __global__ void __launch_bounds__(kThreads6, 1)
                 }
             }
             if (lane == 0) it.w = w;
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&sh.item_full[s]);
+            mbar_arrive(&sh.item_full[s]);
+            __syncwarp();                            // lane 0's fields, for the warp's own reads
         };
         auto load_q = [&](int k) {                   // item k's Q into buffer k & 1
             const ItemSlot &it = sh.item[k % 3];
@@ -2026,6 +2026,8 @@ static kvs_status attention_fwd_impl(const void *q, int64_t q_row_stride, const 
     KVS_REQUIRE(causal || kv_len != nullptr, KVS_EPARAM, "non-causal attention needs kv_len");
     KVS_REQUIRE(rope == nullptr || (rope->cos != nullptr && rope->sin != nullptr), KVS_EPARAM,
                 "rope tables are null");
+    KVS_REQUIRE(rope == nullptr || ((((uintptr_t)rope->cos) | ((uintptr_t)rope->sin)) & 15) == 0,
+                KVS_EPARAM, "rope tables must be 16-byte aligned");
     KVS_REQUIRE(q_row_stride >= (int64_t)num_heads * 128 && q_row_stride % 8 == 0, KVS_ESHAPE,
                 "q row stride %lld below H*128 or not 16-byte aligned", (long long)q_row_stride);
     if (n_tiles <= 0 || n_rows <= 0) return KVS_OK;
