@@ -108,6 +108,14 @@ struct RopeRow {
 
 __device__ __forceinline__ uint32_t align1024(uint32_t a) { return (a + 1023u) & ~1023u; }
 
+// D1 pass 1 (LSE, kPV = false): every kLsePoly-th exponential pair on the FMA
+// pipe (exp2_poly2), 0 = all on MUFU.  1 in 4: 0.687 -> 0.643 ms (1 in 2 is
+// slower, 0.784; A1 with its bf16 pack gets slower at any ratio)
+#ifndef KVS_LSE_POLY
+#define KVS_LSE_POLY 4
+#endif
+constexpr int kLsePoly = KVS_LSE_POLY;
+
 template <bool kPV>
 __global__ void __launch_bounds__(kThreads, kPV ? 1 : 2)
     fwd_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
@@ -270,9 +278,15 @@ __global__ void __launch_bounds__(kThreads, kPV ? 1 : 2)
                 for (int j = 0; j < 8; ++j) ls[j] = 0.f;
 #pragma unroll
                 for (int c = 0; c < BN; c += 2) {
-                    float x0, x1;
+                    float x0, x1, e0, e1;
                     fma2(x0, x1, s[c], s[c + 1], p.scale_log2, p.scale_log2, -m, -m);
-                    add2(ls[c & 7], ls[(c + 1) & 7], fast_exp2(x0), fast_exp2(x1));
+                    if (kLsePoly > 0 && (c / 2) % (kLsePoly > 0 ? kLsePoly : 1) == kLsePoly - 1) {
+                        exp2_poly2(e0, e1, x0, x1);
+                    } else {
+                        e0 = fast_exp2(x0);
+                        e1 = fast_exp2(x1);
+                    }
+                    add2(ls[c & 7], ls[(c + 1) & 7], e0, e1);
                 }
                 const float bsum =
                     ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
@@ -1022,8 +1036,13 @@ __global__ void __launch_bounds__(kThreads2, 1)
                             // every kPolyEvery-th pair on the FMA pipe (0: all on MUFU)
                             const bool poly = kPolyEvery > 0 &&
                                               q % (kPolyEvery > 0 ? kPolyEvery : 1) == kPolyEvery - 1;
-                            const float e0 = poly ? exp2_poly(x0) : fast_exp2(x0);
-                            const float e1 = poly ? exp2_poly(x1) : fast_exp2(x1);
+                            float e0, e1;
+                            if (poly) {
+                                exp2_poly2(e0, e1, x0, x1);
+                            } else {
+                                e0 = fast_exp2(x0);
+                                e1 = fast_exp2(x1);
+                            }
                             add2(ls[(2 * q) & 7], ls[(2 * q + 1) & 7], e0, e1);
                             pk[q] = pack_bf16x2(e0, e1);
                         }
@@ -1797,6 +1816,16 @@ __global__ void __launch_bounds__(kThreads6, 1)
 }
 
 // ------------------------------------------------------------------ D1 pass 2
+// D1's exponentials have no bf16 pack and two softmax warps per SMSP keep the
+// MUFU pipe busy, so half of the colsum / LSE-pass pairs go to the FMA pipe
+// (exp2_poly2): colsum 0.979 -> 0.913 ms (tools/micro_alpha.py)
+#ifndef KVS_D1_POLY
+#define KVS_D1_POLY 2
+#endif
+#ifndef KVS_D1_POLY_NUM
+#define KVS_D1_POLY_NUM 1
+#endif
+constexpr int kD1Poly = KVS_D1_POLY, kD1PolyNum = KVS_D1_POLY_NUM;
 // CTA = (key tile kt of request r, kv head g).  Loops over the group's query
 // heads and the query tiles that can see the keys; S^T lands with one key per
 // TMEM lane, so each softmax thread accumulates its key's column sum.
@@ -1938,10 +1967,17 @@ __global__ void __launch_bounds__(kThreads, 2)
                 // every query of this tile sees every key of the key tile
 #pragma unroll
                 for (int c = 0; c < BN; c += 2) {
-                    float x0, x1;
+                    float x0, x1, e0, e1;
                     fma2(x0, x1, s[c], s[c + 1], p.scale_log2, p.scale_log2, -s_lse[b][c],
                          -s_lse[b][c + 1]);
-                    add2(ps[c & 7], ps[(c + 1) & 7], fast_exp2(x0), fast_exp2(x1));
+                    // every KVS_D1_POLY-th pair of exponentials on the FMA pipe
+                    if (kD1Poly > 0 && (c / 2) % (kD1Poly > 0 ? kD1Poly : 1) >= kD1Poly - kD1PolyNum) {
+                        exp2_poly2(e0, e1, x0, x1);
+                    } else {
+                        e0 = fast_exp2(x0);
+                        e1 = fast_exp2(x1);
+                    }
+                    add2(ps[c & 7], ps[(c + 1) & 7], e0, e1);
                 }
             } else {
 #pragma unroll

@@ -116,6 +116,23 @@ __device__ __forceinline__ void st_global_v8(void *ptr, const uint32_t (&v)[8]) 
                  : "memory");
 }
 
+// exp2 of a pair on the FMA pipe with packed FADD2/FFMA2 (exp2_poly's
+// rounding split and cubic, two lanes per instruction); the 2^j scaling is an
+// integer add per lane.  Inputs clamped at -126.
+__device__ __forceinline__ void exp2_poly2(float &y0, float &y1, float x0, float x1) {
+    x0 = fmaxf(x0, -126.f);
+    x1 = fmaxf(x1, -126.f);
+    float t0, t1, r0, r1, f0, f1, p0, p1;
+    fma2(t0, t1, x0, x1, 1.f, 1.f, 12582912.f, 12582912.f);       // x + 1.5*2^23
+    fma2(r0, r1, t0, t1, 1.f, 1.f, -12582912.f, -12582912.f);     // round(x)
+    fma2(f0, f1, r0, r1, -1.f, -1.f, x0, x1);                     // x - round(x)
+    fma2(p0, p1, f0, f1, 0.0551716685f, 0.0551716685f, 0.242611155f, 0.242611155f);
+    fma2(p0, p1, p0, p1, f0, f1, 0.693260968f, 0.693260968f);
+    fma2(p0, p1, p0, p1, f0, f1, 0.999928057f, 0.999928057f);
+    y0 = __int_as_float(__float_as_int(p0) + (__float_as_int(t0) << 23));
+    y1 = __int_as_float(__float_as_int(p1) + (__float_as_int(t1) << 23));
+}
+
 // ---------------------------------------------------------------- smem / mbarrier
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
