@@ -58,6 +58,10 @@ def parse():
                     help="decode leg token steps (default 8; 128 for --shape qwen, SURVEY 8d cfg3)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo stages the remote-row exchange through the host (1-GPU test)")
+    ap.add_argument("--transport", default="peer", choices=["peer", "nccl"],
+                    help="remote-shard rows: peer = G1 reads the owner's arena through peer "
+                         "memory (CUDA IPC / NVLink) in the gather launch; nccl = device-side "
+                         "plan, pack, all-to-all and unpack through torch.distributed")
     args = ap.parse_args()
     if args.layers is None:
         args.layers = {"llama": 32, "qwen": 28, "yi": 48}[args.shape]
@@ -343,15 +347,27 @@ def build_engine(args, device, rank=0, world=1):
         for r, i in enumerate(ids):
             pages[i] = st.pages[r]
         st.pages = []
+    peer = world > 1 and getattr(args, "transport", "peer") == "peer"
+    owned = {}
+    if peer:
+        # every rank learns the page ids of the entries the others own
+        from paper_2503_16525_b200.shard import share_entry_pages
+        owned = share_entry_pages(pool, {f"src{i}": pages[i] for i in pages})
     for i, toks in enumerate(sources):
         if i in pages:
             pool.insert_pages(f"src{i}", toks, pages[i])
         else:
-            pool.insert_remote(f"src{i}", toks, owner=i % world)
-    if world > 1:
+            pool.insert_remote(f"src{i}", toks, owner=i % world,
+                               pages=owned[f"src{i}"][1] if peer else None)
+    torch.cuda.synchronize()
+    if peer:
+        import torch.distributed as dist
+        from paper_2503_16525_b200.shard import PeerArenas
+        dist.barrier()                       # every owner's pages are written
+        eng.peers = PeerArenas(eng)
+    elif world > 1:
         from paper_2503_16525_b200.shard import RemoteFetcher
         eng.fetcher = RemoteFetcher(eng)
-    torch.cuda.synchronize()
     return cfg, model, pool, eng, sources
 
 
@@ -405,6 +421,21 @@ def algorithmic_counts(eng, st, cfg):
     sel_bytes = n_r * (2 * G * d * 2 + 12) + 4 * B
     return {"attention_flops": sess + probe, "alpha_flops": alpha, "select_bytes": sel_bytes,
             "hit": n_r / float(st.lengths.sum())}      # device scalars: no sync in the loop
+
+
+def close_peers(eng, world):
+    """Every rank releases its peer-memory mappings before any owner exits."""
+    if world > 1 and getattr(eng, "peers", None) is not None:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.synchronize()
+        eng.peers.close()
+        eng.peers = None
+        import gc
+        gc.collect()
+        dist.barrier()
+        torch.cuda.ipc_collect()             # owners: the peers' references are gone
+        dist.barrier()
 
 
 def run_gpu(args, rank, world, device):
@@ -501,6 +532,7 @@ def run_gpu(args, rank, world, device):
            "hit": float(np.mean(n_hit)), "launches": launches // max(args.steps, 1),
            "clocks": clk, "n_launch_attention": len(timers.get("attention", [])) // args.steps}
     if args.profile:
+        close_peers(eng, world)
         return res
     # ---------------- e2e: public API, tokens from pinned host memory, result read back
     pinned = [torch.from_numpy(np.concatenate(b)).pin_memory() for b in batches]
@@ -524,6 +556,7 @@ def run_gpu(args, rank, world, device):
     res["d2h_bytes"] = args.batch * cfg.d_model * 4
     res["decode"] = decode_leg(args, eng, batches[args.warmup], cfg, args.decode_steps + 1)
     res["full_recompute_ms"] = full_recompute_leg(args, eng, batches, dev_tokens)
+    close_peers(eng, world)
     return res
 
 
@@ -869,6 +902,7 @@ def main():
     }
     if world > 1:
         line["dist_backend"] = args.dist_backend
+        line["transport"] = args.transport
         line["gpus_active"] = min(world, ngpu)
     if "full_recompute_ms" in res:
         extra["full_recompute"] = {"ms_per_step": res["full_recompute_ms"],

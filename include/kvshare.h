@@ -153,6 +153,21 @@ kvs_status kvs_gather_kv(const kvs_kv_arena *arena, const kvs_batch *batch,
                          const int32_t *slot_pages, int32_t slot_max_pages,
                          int32_t layer_begin, int32_t layer_end, const kvs_rope *rope,
                          kvs_stream_t stream);
+/* G1 over a sharded pool with peer memory (multi-GPU): slot s is
+ * owned by GPU slot_owner[s] (-1 = this GPU) and its pages (slot_pages, in the
+ * owner's page numbering) are read from peer_base[owner], the owner's arena
+ * base mapped into this process (CUDA IPC; NVLink loads between GPUs).  The
+ * remote-shard fetch and the gather with RoPE re-alignment are one kernel -
+ * the peer-memory alternative to the kvs_pack_rows / exchange /
+ * kvs_unpack_rows path.  Replaces the same reference code as kvs_gather_kv
+ * plus the cross-GPU read of the pool (simulate.py:182-189 reads one shared
+ * pool).  slot_owner: int32 [n_slots]; peer_base: uint64 [world] (device). */
+kvs_status kvs_gather_kv_peer(const kvs_kv_arena *arena, const kvs_batch *batch,
+                              const int32_t *src_slot, const int32_t *src_cand,
+                              const int32_t *slot_pages, int32_t slot_max_pages,
+                              const int32_t *slot_owner, const uint64_t *peer_base,
+                              int32_t layer_begin, int32_t layer_end, const kvs_rope *rope,
+                              kvs_stream_t stream);
 
 /* X1 remote-shard fetch (multi-GPU).  The owner packs the rows
  * (slot, cand) a peer hit - all layers, K and V - into a dense buffer

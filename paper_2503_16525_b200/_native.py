@@ -49,6 +49,8 @@ _SIGS = {
     "kvs_pool_lookup": [P(TokenIndex), c_vp, c_vp, c_i32, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp,
                         c_size, c_vp],
     "kvs_gather_kv": [P(KVArena), P(Batch), c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, P(Rope), c_vp],
+    "kvs_gather_kv_peer": [P(KVArena), P(Batch), c_vp, c_vp, c_vp, c_i32, c_vp, c_vp, c_i32, c_i32,
+                           P(Rope), c_vp],
     "kvs_qkv_rope_scatter": [c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_i32, P(KVArena), P(Batch),
                              P(Rope), c_vp, c_vp, c_vp, c_vp],
     "kvs_qkv_rope_scatter_rows": [c_vp, c_vp, c_i64, c_i32, c_vp, c_vp, c_vp, c_i32, P(KVArena),
@@ -94,7 +96,7 @@ _lib = None
 # kernels launched per entry point (for the bench's gpu_launches claim)
 KERNELS_PER_CALL = {
     "kvs_window_hashes": 1, "kvs_match_pairs": 9, "kvs_index_sort": 5, "kvs_pool_lookup": 4,
-    "kvs_gather_kv": 1, "kvs_qkv_rope_scatter": 1, "kvs_qkv_rope_scatter_rows": 1, "kvs_embed_rows": 1, "kvs_build_rows": 1,
+    "kvs_gather_kv": 1, "kvs_gather_kv_peer": 1, "kvs_qkv_rope_scatter": 1, "kvs_qkv_rope_scatter_rows": 1, "kvs_embed_rows": 1, "kvs_build_rows": 1,
     "kvs_attention_fwd": 1, "kvs_attention_fwd_qkv": 1, "kvs_decode_attention": 2, "kvs_dhd_alpha": 3,
     "kvs_dhd_select": 1, "kvs_ideal_scores": 3, "kvs_dhd_decode_select": 1, "kvs_pack_rows": 1, "kvs_unpack_rows": 1,
 }

@@ -54,15 +54,25 @@ __device__ __forceinline__ void rope8(const uint4 &lo_in, const uint4 &hi_in, ui
 
 // One CTA per flat position; misses exit.  Each layer moves one K and one V
 // row (G*D bf16) with 16-byte vector loads/stores; K rotated in registers.
+// With slot_owner / peer_base (multi-GPU, peer memory): a slot owned by GPU r
+// (slot_owner[slot] = r >= 0) is read straight from r's arena, mapped into
+// this process (CUDA IPC; NVLink loads across GPUs), with the same page
+// geometry - the remote fetch and the gather are one pass, no pack/exchange.
 __global__ void __launch_bounds__(128) gather_kv_kernel(
     Arena A, const int64_t *__restrict__ req_off, int32_t n_req,
     const int32_t *__restrict__ block_table, int32_t max_pages,
     const int32_t *__restrict__ src_slot, const int32_t *__restrict__ src_cand,
     const int32_t *__restrict__ slot_pages, int32_t slot_max_pages, int32_t l0, int32_t l1,
-    const float *__restrict__ cos_t, const float *__restrict__ sin_t) {
+    const float *__restrict__ cos_t, const float *__restrict__ sin_t,
+    const int32_t *__restrict__ slot_owner, const unsigned long long *__restrict__ peer_base) {
     const int64_t t = blockIdx.x;
     const int32_t slot = src_slot[t];
     if (slot < 0) return;
+    Arena S = A;                                  // where the source rows live
+    if (slot_owner != nullptr) {
+        const int32_t owner = slot_owner[slot];
+        if (owner >= 0) S.base = reinterpret_cast<__nv_bfloat16 *>(peer_base[owner]);
+    }
     int lo = 0, hi = n_req;
     while (hi - lo > 1) {
         int mid = (lo + hi) >> 1;
@@ -78,8 +88,8 @@ __global__ void __launch_bounds__(128) gather_kv_kernel(
     const int vvec = A.G * A.D / 8;                         // 16-byte vectors per V row
     const int32_t delta = pos - cand;
     for (int layer = l0; layer < l1; ++layer) {
-        const uint4 *sk = reinterpret_cast<const uint4 *>(A.row(spage, layer, 0, srow));
-        const uint4 *sv = reinterpret_cast<const uint4 *>(A.row(spage, layer, 1, srow));
+        const uint4 *sk = reinterpret_cast<const uint4 *>(S.row(spage, layer, 0, srow));
+        const uint4 *sv = reinterpret_cast<const uint4 *>(S.row(spage, layer, 1, srow));
         uint4 *dk = reinterpret_cast<uint4 *>(A.row(dpage, layer, 0, drow));
         uint4 *dv = reinterpret_cast<uint4 *>(A.row(dpage, layer, 1, drow));
         for (int v = threadIdx.x; v < vvec; v += blockDim.x) dv[v] = sv[v];
@@ -490,23 +500,47 @@ __global__ void __launch_bounds__(128) entry_rows_kernel(Arena A, const int32_t 
 
 extern "C" {
 
-kvs_status kvs_gather_kv(const kvs_kv_arena *arena, const kvs_batch *batch,
-                         const int32_t *src_slot, const int32_t *src_cand,
-                         const int32_t *slot_pages, int32_t slot_max_pages, int32_t layer_begin,
-                         int32_t layer_end, const kvs_rope *rope, kvs_stream_t stream) {
+static kvs_status gather_impl(const kvs_kv_arena *arena, const kvs_batch *batch,
+                              const int32_t *src_slot, const int32_t *src_cand,
+                              const int32_t *slot_pages, int32_t slot_max_pages,
+                              const int32_t *slot_owner, const unsigned long long *peer_base,
+                              int32_t layer_begin, int32_t layer_end, const kvs_rope *rope,
+                              kvs_stream_t stream) {
     KVS_REQUIRE(arena && batch, KVS_EPARAM, "null arena/batch");
     KVS_REQUIRE(arena->head_dim % 16 == 0, KVS_ESHAPE, "head_dim must be a multiple of 16");
     KVS_REQUIRE(0 <= layer_begin && layer_begin <= layer_end && layer_end <= arena->num_layers,
                 KVS_EPARAM, "bad layer range");
+    KVS_REQUIRE((slot_owner == nullptr) == (peer_base == nullptr), KVS_EPARAM,
+                "slot_owner and peer_base go together");
     if (batch->n_total <= 0 || layer_begin == layer_end) return KVS_OK;
     KVS_REQUIRE(batch->n_total < (1ll << 31), KVS_EPARAM, "batch too large");
     cudaStream_t s = (cudaStream_t)stream;
     gather_kv_kernel<<<(unsigned)batch->n_total, 128, 0, s>>>(
         make_arena(arena), batch->req_off, batch->n_req, batch->block_table, batch->max_pages,
         src_slot, src_cand, slot_pages, slot_max_pages, layer_begin, layer_end,
-        rope ? rope->cos : nullptr, rope ? rope->sin : nullptr);
+        rope ? rope->cos : nullptr, rope ? rope->sin : nullptr, slot_owner, peer_base);
     KVS_CHECK_LAUNCH("kvs_gather_kv");
     return KVS_OK;
+}
+
+kvs_status kvs_gather_kv(const kvs_kv_arena *arena, const kvs_batch *batch,
+                         const int32_t *src_slot, const int32_t *src_cand,
+                         const int32_t *slot_pages, int32_t slot_max_pages, int32_t layer_begin,
+                         int32_t layer_end, const kvs_rope *rope, kvs_stream_t stream) {
+    return gather_impl(arena, batch, src_slot, src_cand, slot_pages, slot_max_pages, nullptr,
+                       nullptr, layer_begin, layer_end, rope, stream);
+}
+
+kvs_status kvs_gather_kv_peer(const kvs_kv_arena *arena, const kvs_batch *batch,
+                              const int32_t *src_slot, const int32_t *src_cand,
+                              const int32_t *slot_pages, int32_t slot_max_pages,
+                              const int32_t *slot_owner, const uint64_t *peer_base,
+                              int32_t layer_begin, int32_t layer_end, const kvs_rope *rope,
+                              kvs_stream_t stream) {
+    KVS_REQUIRE(slot_owner && peer_base, KVS_EPARAM, "null slot_owner/peer_base");
+    return gather_impl(arena, batch, src_slot, src_cand, slot_pages, slot_max_pages, slot_owner,
+                       reinterpret_cast<const unsigned long long *>(peer_base), layer_begin,
+                       layer_end, rope, stream);
 }
 
 static kvs_status qkv_scatter_impl(const void *qkv, const int32_t *src_row, int64_t n_rows,

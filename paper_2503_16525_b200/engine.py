@@ -218,6 +218,7 @@ class Engine:
         self.probe_layer = 1 if self.cfg.num_layers >= 2 else 0
         self.timers = None          # {name: [(start_event, end_event), ...]} when profiling
         self.fetcher = None         # shard.RemoteFetcher when the pool is sharded over GPUs
+        self.peers = None           # shard.PeerArenas: remote shards read through peer memory
         self._events: list = []
         self._ev_next = 0
         self.scratch = _Scratch(self.device)
@@ -435,6 +436,10 @@ class Engine:
         begin, end = layers if layers is not None else (0, self.cfg.num_layers)
         idx = self.pool._build_index()
         slot = st.src_slot if slot is None else slot
+        if self.peers is not None:
+            # remote shards' rows read from their owners' arenas in the same launch
+            self._timed("gather", self.peers.gather, st, idx, slot, (begin, end))
+            return
         if self.fetcher is not None:
             # remote-shard rows come through the fetcher (plain path: whole
             # exchange here; the fast path of prefill_batch overlaps it)

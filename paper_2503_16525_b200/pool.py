@@ -88,6 +88,7 @@ class KVEntry:
     insert_seq: int = 0
     owner: int = -1          # GPU rank holding the K/V pages (-1 = this GPU)
     owner_slot: int = -1     # the entry's slot id on its owner (remote entries)
+    remote_pages: list = field(default_factory=list)   # the owner's page ids (peer memory)
 
     @property
     def n_tokens(self) -> int:
@@ -301,13 +302,15 @@ class CachePool:
             self._maybe_renumber()
 
     def insert_remote(self, request_id: str, tokens, owner: int,
-                      owner_slot: int | None = None) -> KVEntry:
+                      owner_slot: int | None = None, pages=None) -> KVEntry:
         """Replicate the token side of an entry whose K/V pages live on GPU
         ``owner`` in its slot ``owner_slot`` (sharded pool).
         Lookups see it like any other entry; its rows are fetched from the
         owner by shard.RemoteFetcher.  ``owner_slot`` defaults to this pool's
         slot, which is the owner's too when every rank inserts in one order
-        (slot ids are append-only and sharded pools never evict or renumber)."""
+        (slot ids are append-only and sharded pools never evict or renumber).
+        ``pages``: the entry's page ids in the owner's arena, for G1 reading
+        them through peer memory (shard.PeerArenas)."""
         if self.capacity_bytes is not None:
             # every rank evicts on its own LRU: victims (and slot ids) would
             # diverge between the ranks that share this entry's owner slot
@@ -315,6 +318,7 @@ class CachePool:
         entry = self.insert_pages(request_id, tokens, [])
         entry.owner = int(owner)
         entry.owner_slot = entry.slot if owner_slot is None else int(owner_slot)
+        entry.remote_pages = [] if pages is None else [int(x) for x in pages]
         self._dirty = True
         return entry
 
@@ -494,14 +498,16 @@ class CachePool:
                          *(idx[k].data_ptr() for k in ("tokens", "tok_off", "win_off", "win_hash",
                                                         "win_slot", "sorted_hash", "sorted_widx",
                                                         "slot_rank", "rank2slot")))
-        max_pages = max([len(e.pages) for e in self._slots if e is not None]
-                        + [len(e.pages) for e in self._retired.values()] + [1])
+        def _pg(e):                  # remote entries: the owner's pages (peer memory)
+            return e.remote_pages if e.owner >= 0 else e.pages
+        max_pages = max([len(_pg(e)) for e in self._slots if e is not None]
+                        + [len(_pg(e)) for e in self._retired.values()] + [1])
         sp = np.zeros((max(n_slots, 1), max_pages), dtype=np.int32)
         owner = np.full(max(n_slots, 1), -1, dtype=np.int32)
         oslot = np.arange(max(n_slots, 1), dtype=np.int32)
         for sl in live + list(self._retired):
             e = self._slots[sl] if self._slots[sl] is not None else self._retired[sl]
-            sp[sl, :len(e.pages)] = e.pages
+            sp[sl, :len(_pg(e))] = _pg(e)
             owner[sl] = e.owner
             if e.owner >= 0:
                 oslot[sl] = e.owner_slot

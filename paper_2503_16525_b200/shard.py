@@ -22,6 +22,14 @@ Collectives go through torch.distributed: NCCL over NVLink on a multi-GPU
 box, gloo (staged through host memory) for the CPU tests and for the
 two-ranks-on-one-GPU functional test.  Nothing else on the path
 communicates.
+
+PeerArenas is the peer-memory transport: every rank's KV arena is mapped into
+every other rank's process once (CUDA IPC handles swapped through
+torch.distributed), the token index carries each remote entry's page ids in
+its owner's arena, and G1 (kvs_gather_kv_peer) reads remote rows straight from
+the owner's memory - NVLink loads between GPUs - in the same launch that
+gathers the local ones, with the RoPE re-alignment fused: no plan, count
+exchange, pack, all-to-all or unpack, and no host round trip.
 """
 from __future__ import annotations
 
@@ -146,3 +154,62 @@ class RemoteFetcher:
         rf = self.begin(st, idx).finish()
         rf.unpack(st, layers or (0, self.engine.cfg.num_layers))
         return rf.n_rows
+
+
+class PeerArenas:
+    """Peer-memory transport (see the module docstring).  Construct on every
+    rank (collective); keeps the mapped peer storages alive."""
+
+    def __init__(self, engine, group=None):
+        self.engine = engine
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        data = engine.arena.data
+        stor = data.untyped_storage()
+        share = stor._share_cuda_()           # (device, handle, size, offset, refcount..., event...)
+        off = data.data_ptr() - stor.data_ptr()
+        infos = [None] * self.world
+        dist.all_gather_object(infos, (share, off), group=group)
+        self._mapped = []
+        bases = []
+        for r, (sh, o) in enumerate(infos):
+            if r == self.rank:
+                bases.append(data.data_ptr())
+                continue
+            s = torch.UntypedStorage._new_shared_cuda(*sh)
+            self._mapped.append(s)
+            bases.append(s.data_ptr() + o)
+        # uint64 addresses carried in an int64 tensor (the kernel reads the bits)
+        self.peer_base = torch.tensor([b if b < (1 << 63) else b - (1 << 64) for b in bases],
+                                      dtype=torch.int64, device=engine.device)
+
+    def close(self):
+        """Drop the peer mappings (before the owners' processes exit)."""
+        self._mapped.clear()
+        self.peer_base = None
+
+    def gather(self, st, idx, slot, layers):
+        """G1 for layers [begin, end) over local and remote slots in one launch."""
+        eng = self.engine
+        owner = idx.get("slot_owner_i32")
+        if owner is None:
+            owner = idx["slot_owner_dev"].to(torch.int32)
+            idx["slot_owner_i32"] = owner
+        N.call("kvs_gather_kv_peer", eng.arena.c, st.batch_c, slot.data_ptr(),
+               st.src_cand.data_ptr(), idx["slot_pages"].data_ptr(), idx["slot_max_pages"],
+               owner.data_ptr(), self.peer_base.data_ptr(), layers[0], layers[1], eng._rope(),
+               N.stream_ptr())
+
+
+def share_entry_pages(pool, ids_pages: dict, group=None) -> dict:
+    """All-gather {request_id: page ids} of the entries each rank owns, so
+    every rank can register the others' entries with their pages."""
+    world = dist.get_world_size(group)
+    got = [None] * world
+    dist.all_gather_object(got, dict(ids_pages), group=group)
+    out = {}
+    for r, d in enumerate(got):
+        for rid, pages in d.items():
+            out[rid] = (r, list(pages))
+    return out

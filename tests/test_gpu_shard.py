@@ -4,8 +4,11 @@ the same scheduled batch through the bench's fast prefill path, fetching the
 rows it hits on the other rank's shard on the fetch stream (device-side
 plan, count exchange, request lists, kvs_pack_rows -> exchange ->
 kvs_unpack_rows for layers >= 1 under the probe, layer 0 after selection).
-The hit maps must equal the single-rank run bit for bit and the first-token
-states must agree to within GEMM-shape rounding.  gloo with both ranks on
+With the peer-memory transport (shard.PeerArenas) the arenas are mapped
+across the two processes through CUDA IPC and G1 reads the other shard's rows
+in the gather launch itself.  The hit maps must equal the single-rank run
+bit for bit and the first-token states must agree to within GEMM-shape
+rounding.  gloo with both ranks on
 cuda:0 (the driver's boxes have one GPU); the NCCL twin runs when the box
 has two GPUs.  bench.py --gpus 2 must spawn and run its two ranks."""
 import os
@@ -31,7 +34,7 @@ def _port():
     return p
 
 
-def _run(rank, world, port, out, backend="gloo"):
+def _run(rank, world, port, out, backend="gloo", transport="nccl"):
     import torch.distributed as dist
     sys.path.insert(0, ROOT)
     import bench
@@ -46,26 +49,35 @@ def _run(rank, world, port, out, backend="gloo"):
             dist.init_process_group("gloo", rank=rank, world_size=world)
     dev = torch.device("cuda", rank if backend == "nccl" else 0)
     torch.cuda.set_device(dev)
-    args = Namespace(layers=2, sources=4, seq=512, batch=3, hit=0.6, ratio=0.2)
+    args = Namespace(layers=2, sources=4, seq=512, batch=3, hit=0.6, ratio=0.2,
+                     transport=transport)
     cfg, model, pool, eng, sources = bench.build_engine(args, dev, rank, world)
     batch = request_batches(sources, 1, args.batch, args.seq, args.hit, cfg.vocab_size, seed=7)[0]
     st = eng.prefill_batch(batch, ratio=args.ratio)
     torch.cuda.synchronize()
     assert st.session_first == 1                          # fast path, also with a fetcher
-    if world > 1:
+    if world > 1 and transport == "nccl":
         assert st._remote_fetch.n_rows > 0                # rows came from the other shard
+    if world > 1 and transport == "peer":
+        assert eng.peers is not None and eng.fetcher is None
+        idx = pool._build_index()
+        owner = idx["slot_owner"][np.maximum(st.src_slot.cpu().numpy(), 0)]
+        hits = st.src_slot.cpu().numpy() >= 0
+        assert (hits & (owner >= 0) & (owner != rank)).any()   # rows read from the peer arena
     out.put((rank, st.src_slot.cpu().numpy(), st.src_cand.cpu().numpy(),
              st.hidden_last.cpu().numpy(), st.selected.cpu().numpy()))
     if world > 1:
+        bench.close_peers(eng, world)
         dist.barrier()
         dist.destroy_process_group()
 
 
-def _spawn(world, backend="gloo"):
+def _spawn(world, backend="gloo", transport="nccl"):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _port()
-    procs = [ctx.Process(target=_run, args=(r, world, port, q, backend)) for r in range(world)]
+    procs = [ctx.Process(target=_run, args=(r, world, port, q, backend, transport))
+             for r in range(world)]
     for p in procs:
         p.start()
     import queue
@@ -84,9 +96,10 @@ def _spawn(world, backend="gloo"):
     return sorted(res, key=lambda r: r[0])
 
 
-def test_sharded_pool_matches_single_rank():
+@pytest.mark.parametrize("transport", ["nccl", "peer"])
+def test_sharded_pool_matches_single_rank(transport):
     single = _spawn(1)[0]
-    sharded = _spawn(2)
+    sharded = _spawn(2, transport=transport)
     for rank, slot, cand, hidden, sel in sharded:
         np.testing.assert_array_equal(slot, single[1])
         np.testing.assert_array_equal(cand, single[2])
