@@ -17,6 +17,7 @@
 // sum_j exp(s_ji - lse_j) is a per-thread row reduction with no cross-thread
 // traffic and no P store.
 #include <algorithm>
+#include <atomic>
 #include <cstdlib>
 
 #include "common.cuh"
@@ -67,6 +68,7 @@ struct Params {
     // the softmax warps rotate the tile in shared memory before the first
     // Q.K^T (fp32 [max_pos][64] cos/sin tables, the scatter's rotation)
     const float *q_cos, *q_sin;
+    int32_t sched;        // persistent kernels: which ticket counter pair this launch uses
 };
 
 // In-place rotation of row i of a TMA-loaded [128 x 128] SW128 Q tile: chunk
@@ -766,10 +768,12 @@ struct SmemP {
     ItemSlot item[3];
 };
 
-// [0] next ticket, [1] CTAs done; the last CTA of a launch zeroes both, so
-// launches on one stream start from 0 (concurrent fwdp launches on several
-// streams of one device would share the counter and are not supported)
-__device__ int g_fwdp_sched[2];
+// Ticket counters of the persistent kernels: pair [0] next ticket, [1] CTAs
+// done; the last CTA of a launch zeroes its pair.  Each launch takes the next
+// of kSchedSlots pairs round-robin (host side), so launches that overlap on
+// different streams use different counters (up to kSchedSlots in flight).
+constexpr int kSchedSlots = 64;
+__device__ int g_fwdp_sched[kSchedSlots][2];
 
 __global__ void __launch_bounds__(kThreads2, 1)
     fwdp_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
@@ -817,7 +821,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
             // ------------------------------------------------ tickets, item slots, TMA
             auto ticket = [&]() {
                 int w = 0;
-                if (lane == 0) w = atomicAdd(&g_fwdp_sched[0], 1);
+                if (lane == 0) w = atomicAdd(&g_fwdp_sched[p.sched][0], 1);
                 return __shfl_sync(0xffffffffu, w, 0);
             };
             auto publish = [&](int k, int w) {       // item k = work item w -> slot k % 3
@@ -901,10 +905,10 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 w = wn;
                 ++k;
             }
-            if (lane == 0 && atomicAdd(&g_fwdp_sched[1], 1) == (int)gridDim.x - 1) {
+            if (lane == 0 && atomicAdd(&g_fwdp_sched[p.sched][1], 1) == (int)gridDim.x - 1) {
                 // every CTA has taken its last ticket: reset for the next launch
-                atomicExch(&g_fwdp_sched[0], 0);
-                atomicExch(&g_fwdp_sched[1], 0);
+                atomicExch(&g_fwdp_sched[p.sched][0], 0);
+                atomicExch(&g_fwdp_sched[p.sched][1], 0);
             }
         } else if (warp == 9 && lane == 0) {
             // ------------------------------------------------ MMA issuer
@@ -1465,7 +1469,7 @@ struct Smem6P {
     ItemSlot item[3];
 };
 
-__device__ int g_fwd6p_sched[2];
+__device__ int g_fwd6p_sched[kSchedSlots][2];
 
 __global__ void __launch_bounds__(kThreads6, 1)
     fwd6p_kernel(const __grid_constant__ CUtensorMap map_q, const __grid_constant__ CUtensorMap map_kv,
@@ -1508,7 +1512,7 @@ __global__ void __launch_bounds__(kThreads6, 1)
         // ------------------------------------------------ tickets, item slots, TMA
         auto ticket = [&]() {
             int w = 0;
-            if (lane == 0) w = atomicAdd(&g_fwd6p_sched[0], 1);
+            if (lane == 0) w = atomicAdd(&g_fwd6p_sched[p.sched][0], 1);
             return __shfl_sync(0xffffffffu, w, 0);
         };
         auto publish = [&](int k, int w) {           // item k = work item w -> slot k % 3
@@ -1590,9 +1594,9 @@ __global__ void __launch_bounds__(kThreads6, 1)
             w = wn;
             ++k;
         }
-        if (lane == 0 && atomicAdd(&g_fwd6p_sched[1], 1) == (int)gridDim.x - 1) {
-            atomicExch(&g_fwd6p_sched[0], 0);
-            atomicExch(&g_fwd6p_sched[1], 0);
+        if (lane == 0 && atomicAdd(&g_fwd6p_sched[p.sched][1], 1) == (int)gridDim.x - 1) {
+            atomicExch(&g_fwd6p_sched[p.sched][0], 0);
+            atomicExch(&g_fwd6p_sched[p.sched][1], 0);
         }
     } else if (warp == 5) {
         if (lane == 0) {
@@ -2092,6 +2096,8 @@ static kvs_status attention_fwd_impl(const void *q, int64_t q_row_stride, const 
     p.n_rows = n_rows;
     p.q_cos = rope != nullptr ? rope->cos : nullptr;
     p.q_sin = rope != nullptr ? rope->sin : nullptr;
+    static std::atomic<int> sched_next{0};
+    p.sched = sched_next.fetch_add(1, std::memory_order_relaxed) & (attn::kSchedSlots - 1);
     cudaStream_t s = (cudaStream_t)stream;
     const int group = num_heads / arena->kv_heads;
     const char *variant = getenv("KVS_ATTN");
