@@ -364,8 +364,19 @@ def build_engine(args, device, rank=0, world=1):
         import torch.distributed as dist
         from paper_2503_16525_b200.shard import PeerArenas
         dist.barrier()                       # every owner's pages are written
-        eng.peers = PeerArenas(eng)
-    elif world > 1:
+        err = None
+        try:
+            eng.peers = PeerArenas(eng)
+        except Exception as e:               # e.g. CUDA IPC not permitted here
+            err = f"{type(e).__name__}: {e}"[:200]
+        errs = [None] * world
+        dist.all_gather_object(errs, err)
+        if any(errs):
+            # every rank falls back together to the pack / exchange / unpack path
+            eng.peers = None
+            args.transport = "nccl (peer setup failed: " + next(x for x in errs if x) + ")"
+            peer = False
+    if world > 1 and not peer:
         from paper_2503_16525_b200.shard import RemoteFetcher
         eng.fetcher = RemoteFetcher(eng)
     return cfg, model, pool, eng, sources
