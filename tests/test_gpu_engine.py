@@ -191,3 +191,40 @@ def test_run_generation_api():
     ref2 = K.ReuseSession(model, target)
     gen2 = K.run_generation(plain, ref2, [1, 2, 3], 3)
     assert max(gen2.step_deviation) < 1e-3 and gen2.recompute_counts == [0, 0, 0]
+
+
+@pytest.mark.parametrize("rope", [None, 10000.0])
+def test_peer_gather_equals_local_gather(rope):
+    """kvs_gather_kv_peer with every slot marked as owned by "rank 0" whose
+    peer base is this process's own arena reads the same pages as the local
+    G1: the destination K/V must be bit-identical (the peer-memory transport's
+    kernel path, exercised without a second process)."""
+    import torch
+
+    from paper_2503_16525_b200 import _native as N
+    kw = dict(L=3, H=4, d_model=512, kvh=2) if rope is None else \
+        dict(L=3, H=4, d_model=512, kvh=2, rope=rope)
+    model, W, ocfg, table = _models(**kw)
+    rng = np.random.default_rng(5)
+    pool, target, reuse, oreuse = _scenario(model, W, ocfg, table, rng)
+    from paper_2503_16525_b200.engine import Engine
+    eng = Engine(model, pool)
+    st = eng.new_batch([np.asarray(target)])
+    eng.lookup(st)
+    assert int((st.src_slot >= 0).sum()) > 0
+    idx = pool._build_index()
+    eng.gather(st)
+    want = eng.arena.data.clone()
+    for p in st.pages[0]:
+        eng.arena.data[p].zero_()
+    owner = torch.zeros(idx["slot_pages"].shape[0], dtype=torch.int32, device=eng.device)
+    base = torch.tensor([eng.arena.data.data_ptr()], dtype=torch.int64, device=eng.device)
+    N.call("kvs_gather_kv_peer", eng.arena.c, st.batch_c, st.src_slot.data_ptr(),
+           st.src_cand.data_ptr(), idx["slot_pages"].data_ptr(), idx["slot_max_pages"],
+           owner.data_ptr(), base.data_ptr(), 0, ocfg.num_layers, eng._rope(), N.stream_ptr())
+    torch.cuda.synchronize()
+    hit_pos = (st.src_slot >= 0).nonzero().flatten()
+    for t in hit_pos.tolist():
+        p, r = st.pages[0][t // 64], t % 64
+        assert torch.equal(eng.arena.data[p, :, :, r], want[p, :, :, r])
+    eng.release(st)
