@@ -69,6 +69,9 @@ struct Params {
     // Q.K^T (fp32 [max_pos][64] cos/sin tables, the scatter's rotation)
     const float *q_cos, *q_sin;
     int32_t sched;        // persistent kernels: which ticket counter pair this launch uses
+    // head selection of the persistent kernels: fwdp walks ppg head pairs per GQA
+    // group (heads g*group + 2j, +1); fwd6p walks h_count heads k*h_stride + h_offset
+    int32_t ppg, h_stride, h_offset, h_count;
 };
 
 // In-place rotation of row i of a TMA-loaded [128 x 128] SW128 Q tile: chunk
@@ -781,7 +784,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
     extern __shared__ uint8_t dsmem[];
     __shared__ SmemP sh;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int pairs = p.num_heads / 2, group = p.num_heads / p.kv_heads;
+    const int group = p.num_heads / p.kv_heads, pairs = p.kv_heads * p.ppg;
     const bool qrope = p.q_cos != nullptr;
 
     const uint32_t base = align1024(smem_u32(dsmem));
@@ -829,7 +832,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
                 if (k >= 3) mbar_wait(&sh.item_empty[s], (uint32_t)((k / 3) - 1) & 1u);
                 ItemSlot &it = sh.item[s];
                 if (w < n_items) {
-                    const int tile = w / pairs;
+                    const int tile = w / pairs, pi = w - tile * pairs;
                     const int req = __ldg(p.tile_req + tile), row0 = __ldg(p.tile_row0 + tile);
                     const int nrows = __ldg(p.tile_rows + tile);
 #pragma unroll
@@ -843,7 +846,7 @@ __global__ void __launch_bounds__(kThreads2, 1)
                         it.nrows = nrows;
                         it.kmax = kmax;
                         it.n_kb = (kmax + BN - 1) / BN;
-                        it.h0 = 2 * (w - tile * pairs);
+                        it.h0 = (pi / p.ppg) * group + 2 * (pi % p.ppg);   // both heads in one group
                     }
                 }
                 if (lane == 0) it.w = w;
@@ -1477,7 +1480,7 @@ __global__ void __launch_bounds__(kThreads6, 1)
     extern __shared__ uint8_t dsmem[];
     __shared__ Smem6P sh;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int H = p.num_heads, group = p.num_heads / p.kv_heads;
+    const int group = p.num_heads / p.kv_heads;
 
     const uint32_t base = align1024(smem_u32(dsmem));
     const uint32_t sQ = base;                          // 2 tiles: item k uses Q buffer k & 1
@@ -1520,7 +1523,7 @@ __global__ void __launch_bounds__(kThreads6, 1)
             if (k >= 3) mbar_wait(&sh.item_empty[s], (uint32_t)((k / 3) - 1) & 1u);
             ItemSlot &it = sh.item[s];
             if (w < n_items) {
-                const int tile = w / H;
+                const int tile = w / p.h_count;
                 const int req = __ldg(p.tile_req + tile), row0 = __ldg(p.tile_row0 + tile);
                 const int nrows = __ldg(p.tile_rows + tile);
 #pragma unroll
@@ -1534,7 +1537,7 @@ __global__ void __launch_bounds__(kThreads6, 1)
                     it.nrows = nrows;
                     it.kmax = kmax;
                     it.n_kb = (kmax + BN - 1) / BN;
-                    it.h0 = w - tile * H;
+                    it.h0 = (w - tile * p.h_count) * p.h_stride + p.h_offset;
                 }
             }
             if (lane == 0) it.w = w;
@@ -2105,8 +2108,33 @@ static kvs_status attention_fwd_impl(const void *q, int64_t q_row_stride, const 
     // single heads with double-buffered S (fwd6p; fwd6 when Q is rotated in
     // the kernel) otherwise; KVS_ATTN=1|3|6|p|q pins a variant (1: the
     // single-head kernel with P through shared memory, 3 / 6: one-shot CTAs)
-    const char v = variant != nullptr ? variant[0] : (group % 2 == 0 ? 'p' : 'q');
-    if (out != nullptr && rope == nullptr && (v == 'q' || (v == 'p' && group % 2 != 0))) {
+    p.ppg = group / 2;
+    p.h_stride = 1;
+    p.h_offset = 0;
+    p.h_count = num_heads;
+    // odd groups > 1 (Qwen: 7): head pairs for all but the last head of each group
+    // (fwdp), then that head alone (fwd6p) - 'm'
+    const char v = variant != nullptr ? variant[0]
+                   : (group % 2 == 0 ? 'p' : (group > 1 && rope == nullptr ? 'm' : 'q'));
+    if (out != nullptr && rope == nullptr && v == 'm' && group % 2 != 0 && group > 1) {
+        p.ppg = (group - 1) / 2;
+        const size_t smem_p = 1024 + attn::TILE_BYTES * (2 + attn::RING3);
+        cudaFuncSetAttribute(attn::fwdp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem_p);
+        const int n_pairs = n_tiles * arena->kv_heads * p.ppg;
+        attn::fwdp_kernel<<<std::min(n_pairs, kNumSMs), attn::kThreads2, smem_p, s>>>(mq, mkv, p,
+                                                                                    n_pairs);
+        p.h_stride = group;
+        p.h_offset = group - 1;
+        p.h_count = arena->kv_heads;
+        p.sched = (p.sched + 1) & (attn::kSchedSlots - 1);
+        const size_t smem_q = 1024 + attn::TILE_BYTES * (2 + attn::RING6P);
+        cudaFuncSetAttribute(attn::fwd6p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem_q);
+        const int n_single = n_tiles * arena->kv_heads;
+        attn::fwd6p_kernel<<<std::min(n_single, kNumSMs), attn::kThreads6, smem_q, s>>>(
+            mq, mkv, p, n_single);
+    } else if (out != nullptr && rope == nullptr && (v == 'q' || ((v == 'p' || v == 'm') && group % 2 != 0))) {
         const size_t smem = 1024 + attn::TILE_BYTES * (2 + attn::RING6P);
         cudaFuncSetAttribute(attn::fwd6p_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem);
