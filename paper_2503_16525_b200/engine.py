@@ -310,6 +310,9 @@ class Engine:
                self.cfg.num_heads, rows.tiles[0].data_ptr(), rows.tiles[1].data_ptr(),
                rows.tiles[2].data_ptr(), rows.n_tiles, None, 1, layer, arena_c, batch_c,
                self.scale, N.ptr(out), N.ptr(lse), N.stream_ptr())
+        g = self.cfg.num_heads // self.cfg.kv_heads
+        if g % 2 == 1 and g > 1 and out is not None and rows.n_tiles > 0:
+            N.launch_count["kernels"] += 1      # odd groups: head-pair + single-head launches
 
     def _attention_qkv(self, qkv, rows: RowSet, layer: int, arena_c, batch_c, out):
         """A1 reading the un-rotated query heads straight from the QKV
