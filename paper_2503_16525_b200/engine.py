@@ -63,7 +63,8 @@ class _Scratch:
         numel = int(np.prod(shape))
         b = self.bufs.get((name, dtype))
         if b is None or b.numel() < numel:
-            b = torch.empty(max(numel, 1), dtype=dtype, device=self.device)
+            # 25% headroom: a batch slightly larger than the last does not reallocate
+            b = torch.empty(max(numel + numel // 4, 1), dtype=dtype, device=self.device)
             self.bufs[(name, dtype)] = b
         return b[:numel].view(*shape)
 

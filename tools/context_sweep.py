@@ -3,7 +3,8 @@ prefill throughput and batch latency of the Llama-3.1-8B-shape step for
 requests of 2k..64k tokens, next to full recompute on the same GPU.  The
 batch shrinks as the context grows (about 32k prompt tokens per step).
 
-    python tools/context_sweep.py [--hit 0.5] [--steps 2] [--out profiles/x.json]
+    python tools/context_sweep.py [--hit 0.5] [--steps 3] [--warmup 2] [--seqs 2048,4096]
+                                  [--out profiles/x.json]
 """
 import argparse
 import gc
@@ -26,7 +27,9 @@ CONFIGS = [(2048, 16, 16), (4096, 8, 16), (8192, 4, 8), (16384, 2, 4), (32768, 1
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--hit", type=float, default=0.5)
-    ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=2)
+    ap.add_argument("--seqs", default=None, help="comma-separated request lengths to run")
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--max-seq", type=int, default=65536)
     ap.add_argument("--out", default=None)
@@ -34,27 +37,31 @@ def main():
     dev = torch.device("cuda", 0)
     rows = []
     for seq, batch, sources in CONFIGS:
-        if seq > a.max_seq:
+        if seq > a.max_seq or (a.seqs and str(seq) not in a.seqs.split(",")):
             continue
         args = argparse.Namespace(layers=a.layers, sources=sources, seq=seq, batch=batch)
         cfg, model, pool, eng, srcs = bench.build_engine(args, dev)
-        batches = request_batches(srcs, a.steps + 1, batch, seq, a.hit, cfg.vocab_size, seed=11)
+        batches = request_batches(srcs, a.steps + a.warmup, batch, seq, a.hit, cfg.vocab_size,
+                                  seed=11)
         toks = [torch.from_numpy(np.concatenate(b)).to(dev) for b in batches]
         res = {"seq": seq, "batch": batch}
         for mode in ("selective", "full"):
-            eng.release(eng.prefill_batch(batches[0], ratio=0.2, mode=mode, tokens_dev=toks[0]))
+            for i in range(a.warmup):
+                eng.release(eng.prefill_batch(batches[i], ratio=0.2, mode=mode, tokens_dev=toks[i]))
             torch.cuda.synchronize()
-            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            e0.record()
+            ev = [torch.cuda.Event(enable_timing=True) for _ in range(a.steps + 1)]
+            ev[0].record()
             hits = []
-            for i in range(1, a.steps + 1):
+            for k, i in enumerate(range(a.warmup, a.warmup + a.steps)):
                 st = eng.prefill_batch(batches[i], ratio=0.2, mode=mode, tokens_dev=toks[i])
                 hits.append(st.n_hit_dev.sum())
                 eng.release(st)
-            e1.record()
+                ev[k + 1].record()
             torch.cuda.synchronize()
-            ms = e0.elapsed_time(e1) / a.steps
-            res[mode] = {"ms_per_batch": ms, "tok_s": batch * seq / (ms / 1000.0)}
+            ms = ev[0].elapsed_time(ev[-1]) / a.steps
+            res[mode] = {"ms_per_batch": ms, "tok_s": batch * seq / (ms / 1000.0),
+                         "ms_each": [round(ev[k].elapsed_time(ev[k + 1]), 2)
+                                     for k in range(a.steps)]}
             if mode == "selective":
                 res["measured_hit"] = float(torch.stack(hits).double().mean().item()) / (batch * seq)
         res["dhd_speedup"] = res["full"]["ms_per_batch"] / res["selective"]["ms_per_batch"]

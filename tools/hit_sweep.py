@@ -2,7 +2,7 @@
 premise): DHD prefill throughput and batch latency of the Llama-3.1-8B-shape
 step for chunk hit rates 0..0.9, next to full recompute on the same GPU.
 
-    python tools/hit_sweep.py [--seq 4096] [--batch 8] [--steps 3] [--out profiles/x.json]
+    python tools/hit_sweep.py [--seq 4096] [--batch 8] [--steps 3] [--warmup 2] [--out profiles/x.json]
 """
 import argparse
 import json
@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--seq", type=int, default=4096)
     ap.add_argument("--batch", type=int, default=8)
     ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=2)
     ap.add_argument("--layers", type=int, default=32)
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
@@ -32,15 +33,16 @@ def main():
     cfg, model, pool, eng, sources = bench.build_engine(args, dev)
     rows = []
     for mode, hit in [("full", 0.0)] + [("selective", h) for h in np.arange(0.0, 0.95, 0.1)]:
-        batches = request_batches(sources, a.steps + 1, a.batch, a.seq, float(hit),
+        batches = request_batches(sources, a.steps + a.warmup, a.batch, a.seq, float(hit),
                                   cfg.vocab_size, seed=11)
         toks = [torch.from_numpy(np.concatenate(b)).to(dev) for b in batches]
-        eng.release(eng.prefill_batch(batches[0], ratio=0.2, mode=mode, tokens_dev=toks[0]))
+        for i in range(a.warmup):
+            eng.release(eng.prefill_batch(batches[i], ratio=0.2, mode=mode, tokens_dev=toks[i]))
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         hits = []
-        for i in range(1, a.steps + 1):
+        for i in range(a.warmup, a.warmup + a.steps):
             st = eng.prefill_batch(batches[i], ratio=0.2, mode=mode, tokens_dev=toks[i])
             hits.append(st.n_hit_dev.sum())
             eng.release(st)
