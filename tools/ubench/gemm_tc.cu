@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+#include <algorithm>
 
 namespace kvs {
 bool encode_tmap(CUtensorMap *map, CUtensorMapDataType dtype, int rank, void *gaddr,
@@ -51,7 +52,10 @@ struct Cfg {
     static constexpr int A_BYTES = 128 * 128;
     static constexpr int B_BYTES = N_CTA * 128;
     static constexpr int STAGE = A_BYTES + B_BYTES;
-    static constexpr int STAGES = CG == 2 ? 6 : 4;
+#ifndef STAGES1
+#define STAGES1 4
+#endif
+    static constexpr int STAGES = CG == 2 ? 6 : STAGES1;
     static constexpr size_t SMEM = 1024 + (size_t)STAGE * STAGES;
 };
 
@@ -121,7 +125,9 @@ __device__ __forceinline__ void commit(uint64_t *bar) {
 template <int CG>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
-                __nv_bfloat16 *__restrict__ C, int M, int N, int K) {
+                __nv_bfloat16 *__restrict__ C, int M, int N, int K, int mode) {
+    // mode 0: GEMM; 1: MMAs on whatever the stages hold, no loads (tensor-pipe rate);
+    // 2: loads only (the MMA thread releases each stage as soon as it lands; CG = 1)
     using F = Cfg<CG>;
     extern __shared__ uint8_t dsm[];
     __shared__ uint64_t full[F::STAGES], empty[F::STAGES], acc_full[2], acc_empty[2];
@@ -172,6 +178,25 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(&empty[s], ((it / F::STAGES) & 1) ^ 1);
                     const uint32_t fb = full0 + s * 8;
                     const uint32_t sa = base + s * F::STAGE;
+                    if (mode == 1) {
+                        arrive_cluster(fb);
+                        continue;
+                    }
+                    if (mode == 3) {    // the same bytes as two contiguous 1-D bulk copies
+                        const char *src = reinterpret_cast<const char *>(C) +
+                                          ((size_t)(t * kblocks + kb) % 1024) * F::STAGE;
+                        arrive_expect_cluster(fb, F::STAGE);
+                        asm volatile(
+                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
+                            " [%0], [%1], %2, [%3];" ::"r"(sa), "l"(src), "r"(F::A_BYTES), "r"(fb)
+                            : "memory");
+                        asm volatile(
+                            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes"
+                            " [%0], [%1], %2, [%3];" ::"r"(sa + F::A_BYTES),
+                            "l"(src + F::A_BYTES), "r"(F::B_BYTES), "r"(fb)
+                            : "memory");
+                        continue;
+                    }
                     arrive_expect_cluster(fb, F::STAGE);
                     tma_2d<CG>(sa, &ta, fb, kb * BK, arow);
                     tma_2d<CG>(sa + F::A_BYTES, &tb, fb, kb * BK, brow);
@@ -191,6 +216,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const int s = it % F::STAGES;
                     mbar_wait(&full[s], (it / F::STAGES) & 1);
                     tc_fence_after();
+                    if (mode >= 2) {
+                        mbar_arrive(&empty[s]);
+                        continue;
+                    }
                     const uint32_t sa = base + s * F::STAGE, sb = sa + F::A_BYTES;
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)
@@ -199,7 +228,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 (kb | k) != 0 ? 1u : 0u);
                     commit<CG>(&empty[s]);
                 }
-                commit<CG>(&acc_full[buf]);
+                if (mode >= 2)
+                    mbar_arrive(&acc_full[buf]);
+                else
+                    commit<CG>(&acc_full[buf]);
             }
         }
     } else {
@@ -245,7 +277,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 template <int CG>
 cudaError_t launch(const CUtensorMap &ta, const CUtensorMap &tb, __nv_bfloat16 *C, int M, int N,
-                   int K, int grid) {
+                   int K, int grid, int mode = 0) {
     using F = Cfg<CG>;
     cudaFuncSetAttribute(gemm_kernel<CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)F::SMEM);
@@ -260,7 +292,7 @@ cudaError_t launch(const CUtensorMap &ta, const CUtensorMap &tb, __nv_bfloat16 *
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gemm_kernel<CG>, ta, tb, C, M, N, K);
+    return cudaLaunchKernelEx(&cfg, gemm_kernel<CG>, ta, tb, C, M, N, K, mode);
 }
 
 }  // namespace gemm
@@ -342,6 +374,16 @@ static void run(const char *name, int M, int N, int K, int reps) {
         cudaEventElapsedTime(&ms_ref, e0, e1);
     }
     const double flop = 2.0 * M * N * K;
+    float ms_mode[3] = {0, 0, 0};
+    for (int mode = 1; mode <= (CG == 1 ? 2 : 1); ++mode) {
+        cudaEventRecord(e0);
+        for (int r = 0; r < reps; ++r) gemm::launch<CG>(ta, tb, C, M, N, K, grid, mode);
+        cudaEventRecord(e1);
+        cudaEventSynchronize(e1);
+        cudaEventElapsedTime(&ms_mode[mode], e0, e1);
+    }
+    printf("%-8s   MMA-only %.1f us (%.0f TFLOP/s)   loads-only %.1f us\n", name,
+           1e3 * ms_mode[1] / reps, flop * reps / ms_mode[1] / 1e9, 1e3 * ms_mode[2] / reps);
     printf("%-8s M=%d N=%d K=%d  tcgen05 %.1f us (%.0f TFLOP/s)  cuBLAS %.1f us (%.0f TFLOP/s)  "
            "ratio %.3f  max|err| %.3g (max|ref| %.3g, %zu off)\n",
            name, M, N, K, 1e3 * ms_mine / reps, flop * reps / ms_mine / 1e9, 1e3 * ms_ref / reps,
@@ -353,8 +395,51 @@ static void run(const char *name, int M, int N, int K, int reps) {
     cudaFree(R);
 }
 
+// Loads-only rate (mode 2, CG = 1) against the number of SMs streaming.
+static void probe_loads(int M, int N, int K) {
+    __nv_bfloat16 *A, *B, *C;
+    cudaMalloc(&A, (size_t)M * K * 2);
+    cudaMalloc(&B, (size_t)N * K * 2);
+    cudaMalloc(&C, (size_t)M * N * 2);
+    CUtensorMap ta, tb;
+    make_map(&ta, A, M, K, 128);
+    make_map(&tb, B, N, K, 256);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    for (int grid : {1, 8, 37, 74, 148}) {
+        // each CTA streams ~the same number of tiles whatever the grid
+        const int m = std::min(M, (int)(128 * ((grid * 8 + 23) / 24)));
+        float ms = 0;
+        for (int pass = 0; pass < 2; ++pass) {
+            cudaEventRecord(e0);
+            gemm::launch<1>(ta, tb, C, m, N, K, grid, 2);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            cudaEventElapsedTime(&ms, e0, e1);
+        }
+        float ms_bulk = 0;
+        for (int pass = 0; pass < 2; ++pass) {
+            cudaEventRecord(e0);
+            gemm::launch<1>(ta, tb, C, m, N, K, grid, 3);
+            cudaEventRecord(e1);
+            cudaEventSynchronize(e1);
+            cudaEventElapsedTime(&ms_bulk, e0, e1);
+        }
+        const double bytes = (double)(m / 128) * (N / 256) * (K / 64) * 49152.0;
+        printf("loads-only grid %3d: %.2f GB in %.1f us = %.0f GB/s (%.1f B/clk/SM at 1.965 GHz)\n",
+               grid, bytes / 1e9, ms * 1e3, bytes / ms / 1e6, bytes / (ms * 1e-3) / grid / 1.965e9);
+        printf("   1-D bulk copies  grid %3d: %.1f us = %.0f GB/s (%.1f B/clk/SM)\n", grid,
+               ms_bulk * 1e3, bytes / ms_bulk / 1e6, bytes / (ms_bulk * 1e-3) / grid / 1.965e9);
+    }
+}
+
 int main(int argc, char **argv) {
     const int M = argc > 1 ? atoi(argv[1]) : 16384;
+    if (argc > 2) {
+        probe_loads(M, 6144, 4096);
+        return 0;
+    }
     const int reps = 20;
     run<1>("1-SM", M, 6144, 4096, reps);
     run<2>("2-SM", M, 6144, 4096, reps);
