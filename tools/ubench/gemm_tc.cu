@@ -46,16 +46,20 @@ namespace gemm {
 constexpr int BK = 64;           // K elements per stage (128 bytes: one SW128 row)
 constexpr int kThreads = 192;    // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue
 
-template <int CG>
+template <int CG, int NM>
 struct Cfg {
-    static constexpr int N_CTA = 256 / CG;       // B rows held by each CTA
+    // NM N=256 MMAs per K step: a CTA pair's tile is 256 x (256 NM); NM = 2 fills all 512
+    // TMEM columns (no second accumulator) but halves the operand bytes per FLOP for A
+    static constexpr int TN = 256 * NM;
+    static constexpr int NBUF = NM == 1 ? 2 : 1;
+    static constexpr int N_CTA = TN / CG;        // B rows held by each CTA
     static constexpr int A_BYTES = 128 * 128;
     static constexpr int B_BYTES = N_CTA * 128;
     static constexpr int STAGE = A_BYTES + B_BYTES;
 #ifndef STAGES1
 #define STAGES1 4
 #endif
-    static constexpr int STAGES = CG == 2 ? 6 : STAGES1;
+    static constexpr int STAGES = CG == 2 ? (NM == 2 ? 4 : 6) : STAGES1;
     static constexpr size_t SMEM = 1024 + (size_t)STAGE * STAGES;
 };
 
@@ -122,13 +126,13 @@ __device__ __forceinline__ void commit(uint64_t *bar) {
         umma_commit(bar);
 }
 
-template <int CG>
+template <int CG, int NM>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb,
                 __nv_bfloat16 *__restrict__ C, int M, int N, int K, int mode) {
     // mode 0: GEMM; 1: MMAs on whatever the stages hold, no loads (tensor-pipe rate);
     // 2: loads only (the MMA thread releases each stage as soon as it lands; CG = 1)
-    using F = Cfg<CG>;
+    using F = Cfg<CG, NM>;
     extern __shared__ uint8_t dsm[];
     __shared__ uint64_t full[F::STAGES], empty[F::STAGES], acc_full[2], acc_empty[2];
     __shared__ uint32_t tbase;
@@ -148,7 +152,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (threadIdx.x == 32) {
         for (int s = 0; s < F::STAGES; ++s) {
             mbar_init(&full[s], CG);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], mode == 4 ? 2 : 1);
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&acc_full[b], 1);
@@ -158,10 +162,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if constexpr (CG == 2) cluster_sync_all();
+    if (CG == 2 || mode == 4) cluster_sync_all();
     tc_fence_after();
     const uint32_t tmem = tbase;
-    const int tiles_n = N / 256, n_tiles = (M / (128 * CG)) * tiles_n;
+    const int tiles_n = N / F::TN, n_tiles = (M / (128 * CG)) * tiles_n;
     const int cid = blockIdx.x / CG, ncl = gridDim.x / CG, kblocks = K / BK;
 
     if (warp == 0) {
@@ -172,7 +176,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             int it = 0;
             for (int t = cid; t < n_tiles; t += ncl) {
                 const int mb = t / tiles_n, nb = t % tiles_n;
-                const int arow = mb * 128 * CG + rank * 128, brow = nb * 256 + rank * F::N_CTA;
+                const int arow = mb * 128 * CG + rank * 128;
+                const int brow = nb * F::TN + rank * (256 / CG);
                 for (int kb = 0; kb < kblocks; ++kb, ++it) {
                     const int s = it % F::STAGES;
                     mbar_wait(&empty[s], ((it / F::STAGES) & 1) ^ 1);
@@ -180,6 +185,19 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint32_t sa = base + s * F::STAGE;
                     if (mode == 1) {
                         arrive_cluster(fb);
+                        continue;
+                    }
+                    if (mode == 4) {    // cluster of 2: B split in halves, each multicast to both
+                        const uint32_t cr = cluster_rank();
+                        arrive_expect_cluster(fb, F::STAGE);
+                        tma_2d<1>(sa, &ta, fb, kb * BK, arow);
+                        asm volatile(
+                            "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+                            ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(
+                                sa + F::A_BYTES + cr * (F::B_BYTES / 2)),
+                            "l"(reinterpret_cast<uint64_t>(&tb)), "r"(fb), "r"(kb * BK),
+                            "r"(nb * 256 + (int)cr * 128), "h"((uint16_t)3)
+                            : "memory");
                         continue;
                     }
                     if (mode == 3) {    // the same bytes as two contiguous 1-D bulk copies
@@ -199,7 +217,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     arrive_expect_cluster(fb, F::STAGE);
                     tma_2d<CG>(sa, &ta, fb, kb * BK, arow);
-                    tma_2d<CG>(sa + F::A_BYTES, &tb, fb, kb * BK, brow);
+#pragma unroll
+                    for (int jj = 0; jj < NM; ++jj)
+                        tma_2d<CG>(sa + F::A_BYTES + jj * (256 / CG) * 128, &tb, fb, kb * BK,
+                                   brow + jj * 256);
                 }
             }
         }
@@ -208,8 +229,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint32_t idesc = umma_idesc_bf16(128 * CG, 256, false);
             int it = 0, j = 0;
             for (int t = cid; t < n_tiles; t += ncl, ++j) {
-                const int buf = j & 1;
-                mbar_wait(&acc_empty[buf], ((j >> 1) & 1) ^ 1);
+                const int buf = j % F::NBUF;
+                mbar_wait(&acc_empty[buf], ((j / F::NBUF) & 1) ^ 1);
                 tc_fence_after();
                 const uint32_t d = tmem + buf * 256;
                 for (int kb = 0; kb < kblocks; ++kb, ++it) {
@@ -218,14 +239,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc_fence_after();
                     if (mode >= 2) {
                         mbar_arrive(&empty[s]);
+                        if (mode == 4) arrive_cluster(mapa(smem_u32(&empty[s]), cluster_rank() ^ 1));
                         continue;
                     }
                     const uint32_t sa = base + s * F::STAGE, sb = sa + F::A_BYTES;
 #pragma unroll
                     for (int k = 0; k < BK / 16; ++k)
-                        mma<CG>(d, umma_desc_sw128(sa + k * 32, 16, 1024),
-                                umma_desc_sw128(sb + k * 32, 16, 1024), idesc,
-                                (kb | k) != 0 ? 1u : 0u);
+#pragma unroll
+                        for (int jj = 0; jj < NM; ++jj)
+                            mma<CG>(d + jj * 256, umma_desc_sw128(sa + k * 32, 16, 1024),
+                                    umma_desc_sw128(sb + jj * (256 / CG) * 128 + k * 32, 16, 1024),
+                                    idesc, (kb | k) != 0 ? 1u : 0u);
                     commit<CG>(&empty[s]);
                 }
                 if (mode >= 2)
@@ -240,14 +264,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             CG == 2 ? mapa(smem_u32(&acc_empty[0]), 0) : smem_u32(&acc_empty[0]);
         int j = 0;
         for (int t = cid; t < n_tiles; t += ncl, ++j) {
-            const int buf = j & 1;
+            const int buf = j % F::NBUF;
             const int mb = t / tiles_n, nb = t % tiles_n;
-            mbar_wait(&acc_full[buf], (j >> 1) & 1);
+            mbar_wait(&acc_full[buf], (j / F::NBUF) & 1);
             tc_fence_after();
             const int row = mb * 128 * CG + rank * 128 + q * 32 + lane;
-            __nv_bfloat16 *dst = C + (size_t)row * N + nb * 256;
+            __nv_bfloat16 *dst = C + (size_t)row * N + nb * F::TN;
 #pragma unroll 1
-            for (int c = 0; c < 8; ++c) {
+            for (int c = 0; c < 8 * NM; ++c) {
                 float v[32];
                 tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + buf * 256 + c * 32, v);
                 tmem_ld_wait();
@@ -264,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
-    if constexpr (CG == 2) cluster_sync_all();
+    if (CG == 2 || mode == 4) cluster_sync_all();
     if (warp == 0) {
         tc_fence_after();
         if constexpr (CG == 2)
@@ -275,11 +299,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
 }
 
-template <int CG>
+template <int CG, int NM = 1>
 cudaError_t launch(const CUtensorMap &ta, const CUtensorMap &tb, __nv_bfloat16 *C, int M, int N,
                    int K, int grid, int mode = 0) {
-    using F = Cfg<CG>;
-    cudaFuncSetAttribute(gemm_kernel<CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    using F = Cfg<CG, NM>;
+    cudaFuncSetAttribute(gemm_kernel<CG, NM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)F::SMEM);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
@@ -287,12 +311,12 @@ cudaError_t launch(const CUtensorMap &ta, const CUtensorMap &tb, __nv_bfloat16 *
     cfg.dynamicSmemBytes = F::SMEM;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.x = mode == 4 ? 2 : CG;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    return cudaLaunchKernelEx(&cfg, gemm_kernel<CG>, ta, tb, C, M, N, K, mode);
+    return cudaLaunchKernelEx(&cfg, gemm_kernel<CG, NM>, ta, tb, C, M, N, K, mode);
 }
 
 }  // namespace gemm
@@ -316,7 +340,7 @@ static bool make_map(CUtensorMap *m, void *p, int rows, int K, int box_rows) {
                             CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-template <int CG>
+template <int CG, int NM = 1>
 static void run(const char *name, int M, int N, int K, int reps) {
     __nv_bfloat16 *A, *B, *C, *R;
     cudaMalloc(&A, (size_t)M * K * 2);
@@ -339,7 +363,7 @@ static void run(const char *name, int M, int N, int K, int reps) {
                      K, &zero, R, CUDA_R_16BF, N, CUBLAS_COMPUTE_32F, CUBLAS_GEMM_DEFAULT);
     };
     const int grid = (148 / CG) * CG;
-    cudaError_t e = gemm::launch<CG>(ta, tb, C, M, N, K, grid);
+    cudaError_t e = gemm::launch<CG, NM>(ta, tb, C, M, N, K, grid);
     ref();
     cudaError_t e2 = cudaDeviceSynchronize();
     if (e != cudaSuccess || e2 != cudaSuccess) {
@@ -363,7 +387,7 @@ static void run(const char *name, int M, int N, int K, int reps) {
     float ms_mine = 0, ms_ref = 0;
     for (int pass = 0; pass < 2; ++pass) {
         cudaEventRecord(e0);
-        for (int r = 0; r < reps; ++r) gemm::launch<CG>(ta, tb, C, M, N, K, grid);
+        for (int r = 0; r < reps; ++r) gemm::launch<CG, NM>(ta, tb, C, M, N, K, grid);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         cudaEventElapsedTime(&ms_mine, e0, e1);
@@ -377,7 +401,7 @@ static void run(const char *name, int M, int N, int K, int reps) {
     float ms_mode[3] = {0, 0, 0};
     for (int mode = 1; mode <= (CG == 1 ? 2 : 1); ++mode) {
         cudaEventRecord(e0);
-        for (int r = 0; r < reps; ++r) gemm::launch<CG>(ta, tb, C, M, N, K, grid, mode);
+        for (int r = 0; r < reps; ++r) gemm::launch<CG, NM>(ta, tb, C, M, N, K, grid, mode);
         cudaEventRecord(e1);
         cudaEventSynchronize(e1);
         cudaEventElapsedTime(&ms_mode[mode], e0, e1);
@@ -407,7 +431,7 @@ static void probe_loads(int M, int N, int K) {
     cudaEvent_t e0, e1;
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
-    for (int grid : {1, 8, 37, 74, 148}) {
+    for (int grid : {2, 8, 38, 74, 148}) {
         // each CTA streams ~the same number of tiles whatever the grid
         const int m = std::min(M, (int)(128 * ((grid * 8 + 23) / 24)));
         float ms = 0;
@@ -417,6 +441,18 @@ static void probe_loads(int M, int N, int K) {
             cudaEventRecord(e1);
             cudaEventSynchronize(e1);
             cudaEventElapsedTime(&ms, e0, e1);
+        }
+        float ms_mc = 0;
+        if (grid % 2 == 0) {
+            CUtensorMap tb2;
+            make_map(&tb2, B, N, K, 128);
+            for (int pass = 0; pass < 2; ++pass) {
+                cudaEventRecord(e0);
+                gemm::launch<1>(ta, tb2, C, m, N, K, grid, 4);
+                cudaEventRecord(e1);
+                cudaEventSynchronize(e1);
+                cudaEventElapsedTime(&ms_mc, e0, e1);
+            }
         }
         float ms_bulk = 0;
         for (int pass = 0; pass < 2; ++pass) {
@@ -429,6 +465,8 @@ static void probe_loads(int M, int N, int K) {
         const double bytes = (double)(m / 128) * (N / 256) * (K / 64) * 49152.0;
         printf("loads-only grid %3d: %.2f GB in %.1f us = %.0f GB/s (%.1f B/clk/SM at 1.965 GHz)\n",
                grid, bytes / 1e9, ms * 1e3, bytes / ms / 1e6, bytes / (ms * 1e-3) / grid / 1.965e9);
+        printf("   B multicast in CTA pairs grid %3d: %.1f us = %.0f GB/s received (%.1f B/clk/SM)\n",
+               grid, ms_mc * 1e3, bytes / ms_mc / 1e6, bytes / (ms_mc * 1e-3) / grid / 1.965e9);
         printf("   1-D bulk copies  grid %3d: %.1f us = %.0f GB/s (%.1f B/clk/SM)\n", grid,
                ms_bulk * 1e3, bytes / ms_bulk / 1e6, bytes / (ms_bulk * 1e-3) / grid / 1.965e9);
     }
@@ -443,7 +481,9 @@ int main(int argc, char **argv) {
     const int reps = 20;
     run<1>("1-SM", M, 6144, 4096, reps);
     run<2>("2-SM", M, 6144, 4096, reps);
+    run<2, 2>("2-SM x2", M, 6144, 4096, reps);
     run<1>("1-SM", M, 4096, 4096, reps);
     run<2>("2-SM", M, 4096, 4096, reps);
+    run<2, 2>("2-SM x2", M, 4096, 4096, reps);
     return 0;
 }
