@@ -241,6 +241,17 @@ kvs_status kvs_embed_rows(const void *table, int64_t width, const int64_t *ids,
                           const int32_t *rows, int64_t n_rows, void *out, float *out_f32,
                           kvs_stream_t stream);
 
+/* Decode-size projection (1 <= m <= 64 rows; model.py:193-195 / :202):
+ * out = x @ W for W [k][n] bf16 given packed as 16 x 64 tiles of its
+ * transpose, w_p [n/16][k/64][16][64] (W[i][j] at [j/16][i/64][j%16][i%64]),
+ * x [m][k] bf16; n % 128 == 0, k % 512 == 0.  accumulate == 0: out is bf16
+ * [m][n] and out_bf16 must be NULL.  accumulate != 0: out is fp32 [m][n] and
+ * receives out += x @ W (the residual add); out_bf16 (nullable) then gets
+ * bf16(out), the next layer's projection operand.  Deterministic (fixed
+ * summation order).  Replaces the library GEMM of engine.py's decode steps. */
+kvs_status kvs_proj_skinny(const void *x, int64_t m, const void *w_p, int64_t n, int64_t k,
+                           int32_t accumulate, void *out, void *out_bf16, kvs_stream_t stream);
+
 /* Recompute row set S = non-reused U selected U {n-1} per request (the rows a
  * partial prefill must compute).  Call once with
  * row_tok == NULL to get counts[r]; then with row_off[r] (exclusive prefix of

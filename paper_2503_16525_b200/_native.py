@@ -58,6 +58,7 @@ _SIGS = {
     "kvs_fixed_chunk_lookup": [P(TokenIndex), c_vp, c_vp, c_i32, c_i64, c_i32, c_vp, c_vp, c_vp,
                                c_vp, c_i64, c_vp],
     "kvs_topk_select": [c_vp, c_vp, c_vp, c_i32, c_i64, c_vp, c_vp, c_vp],
+    "kvs_proj_skinny": [c_vp, c_i64, c_vp, c_i64, c_i64, c_i32, c_vp, c_vp, c_vp],
     "kvs_ideal_scores": [c_vp, c_vp, c_vp, c_vp, c_vp, c_i32, c_i32, c_i32, c_i32, c_i32, c_f32,
                          c_vp, c_vp, c_size, c_vp],
     "kvs_entry_import": [P(KVArena), c_vp, c_i64, c_i32, c_vp, c_vp, c_vp],
@@ -97,6 +98,7 @@ _lib = None
 KERNELS_PER_CALL = {
     "kvs_window_hashes": 1, "kvs_match_pairs": 9, "kvs_index_sort": 5, "kvs_pool_lookup": 4,
     "kvs_gather_kv": 1, "kvs_gather_kv_peer": 1, "kvs_qkv_rope_scatter": 1, "kvs_qkv_rope_scatter_rows": 1, "kvs_embed_rows": 1, "kvs_build_rows": 1,
+    "kvs_proj_skinny": 1,
     "kvs_attention_fwd": 1, "kvs_attention_fwd_qkv": 1, "kvs_decode_attention": 2, "kvs_dhd_alpha": 3,
     "kvs_dhd_select": 1, "kvs_ideal_scores": 3, "kvs_dhd_decode_select": 1, "kvs_pack_rows": 1, "kvs_unpack_rows": 1,
 }

@@ -23,7 +23,7 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", 
          "-I" + os.path.join(ROOT, "include")]
 SOURCES = ["capi.cu", "retriever.cu", "gather.cu", "dhd.cu", "attention_sm100.cu", "baselines.cu",
            "decode_attn.cu",
-           "decode_dhd.cu"]
+           "decode_dhd.cu", "projection.cu"]
 
 
 def _headers_mtime() -> float:

@@ -212,6 +212,10 @@ class Engine:
         self.scale = 1.0 / math.sqrt(self.cfg.d_k)
         self._ws = {k: N.Workspace() for k in ("alpha", "select", "decode", "dsel")}
         self._probe_arena = _ProbeArena()
+        # P1 decode-size projections, off by default: measured no faster than the library
+        # GEMM at the decode step's 32 rows (profiles/r2_p1_skinny.txt)
+        self.skinny = os.environ.get("KVS_SKINNY_PROJ", "0") != "0"
+        self._wt = None
         self.rope_c = None
         if model.rope is not None:
             self.rope_c = N.Rope(model.rope[0].data_ptr(), model.rope[1].data_ptr(),
@@ -396,6 +400,30 @@ class Engine:
                 capture.append((layer, "hidden", x.clone()))
         return x
 
+    SKINNY_MAX_ROWS = 64
+
+    def _skinny_ok(self, n: int) -> bool:
+        """Decode-size row counts take P1 (kvs_proj_skinny) when the widths allow."""
+        cfg = self.cfg
+        return (self.skinny and 1 <= n <= self.SKINNY_MAX_ROWS and cfg.d_model % 512 == 0
+                and (cfg.num_heads * HEAD_DIM) % 512 == 0 and cfg.d_model % 128 == 0
+                and self.model.w_qkv[0].shape[1] % 128 == 0)
+
+    @staticmethod
+    def pack_skinny(w: torch.Tensor) -> torch.Tensor:
+        """W [k][n] -> P1's layout: 16 x 64 tiles of W^T, [n/16][k/64][16][64]
+        (include/kvshare.h, kvs_proj_skinny)."""
+        k, n = w.shape
+        return w.t().reshape(n // 16, 16, k // 64, 64).permute(0, 2, 1, 3).contiguous()
+
+    def ensure_skinny_weights(self) -> None:
+        """P1-packed copies of every layer's projection weights.  Built once,
+        outside any graph capture."""
+        if self._wt is not None or not self._skinny_ok(1):
+            return
+        m = self.model
+        self._wt = ([self.pack_skinny(w) for w in m.w_qkv], [self.pack_skinny(w) for w in m.w_o])
+
     def _qkv(self, x: torch.Tensor, layer: int) -> torch.Tensor:
         """bf16(x) @ W_qkv into scratch (model.py:193-195)."""
         n = x.shape[0]
@@ -405,12 +433,26 @@ class Engine:
             xb.copy_(x)
             self._xb_of = (x.data_ptr(), n)
         qkv = self.scratch.get("qkv", (n, w.shape[1]), torch.bfloat16)
+        if self._skinny_ok(n):
+            self.ensure_skinny_weights()
+            N.call("kvs_proj_skinny", xb.data_ptr(), n, self._wt[0][layer].data_ptr(),
+                   w.shape[1], w.shape[0], 0, qkv.data_ptr(), None, N.stream_ptr())
+            return qkv
         return torch.matmul(xb, w, out=qkv)
 
     def _out_proj(self, x: torch.Tensor, o: torch.Tensor, layer: int) -> None:
         """x += merge(o) @ W_o in place (model.py:202): the residual add runs in
-        the cuBLAS epilogue with C = D = x (fp32), A/B bf16 - no copy of x."""
+        the cuBLAS epilogue with C = D = x (fp32), A/B bf16 - no copy of x.
+        Decode-size row counts run P1, whose epilogue also leaves bf16(x) in
+        the next projection's operand buffer."""
         n = x.shape[0]
+        if self._skinny_ok(n):
+            self.ensure_skinny_weights()
+            xb = self.scratch.get("xb", (n, x.shape[1]), torch.bfloat16)
+            N.call("kvs_proj_skinny", o.data_ptr(), n, self._wt[1][layer].data_ptr(),
+                   x.shape[1], o[0].numel(), 1, x.data_ptr(), xb.data_ptr(), N.stream_ptr())
+            self._xb_of = (x.data_ptr(), n)
+            return
         torch.addmm(x, o.view(n, -1), self.model.w_o[layer], out_dtype=torch.float32, out=x)
         self._xb_of = None
 
@@ -873,6 +915,7 @@ class DecodeGraph:
         if self.n_extra > 0 and st.eligible is not None:
             eng.ensure_dv(st)                       # host-dependent set-up stays outside
         eng._ctx_dev(st)
+        eng.ensure_skinny_weights()
         self.tok = torch.zeros(R, dtype=torch.int64, device=dev)
         saved = (eng.scratch, eng._ws, eng.timers)
         # the graph's own buffers, allocated while capturing (from the graph's
