@@ -37,6 +37,7 @@ import torch
 import torch.distributed as dist
 
 from . import _native as N
+from .errors import DeviceError
 
 
 def plan_remote(src_slot: torch.Tensor, slot_owner: torch.Tensor, rank: int, world: int):
@@ -191,11 +192,10 @@ class PeerArenas:
 
     def gather(self, st, idx, slot, layers):
         """G1 for layers [begin, end) over local and remote slots in one launch."""
+        if self.peer_base is None:
+            raise DeviceError("PeerArenas.gather after close()")
         eng = self.engine
-        owner = idx.get("slot_owner_i32")
-        if owner is None:
-            owner = idx["slot_owner_dev"].to(torch.int32)
-            idx["slot_owner_i32"] = owner
+        owner = idx["slot_owner_dev"]              # int32 per slot (-1: local), rebuilt with idx
         N.call("kvs_gather_kv_peer", eng.arena.c, st.batch_c, slot.data_ptr(),
                st.src_cand.data_ptr(), idx["slot_pages"].data_ptr(), idx["slot_max_pages"],
                owner.data_ptr(), self.peer_base.data_ptr(), layers[0], layers[1], eng._rope(),
