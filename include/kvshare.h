@@ -347,9 +347,10 @@ kvs_status kvs_dhd_select(const void *v_true, const float *alpha, const int32_t 
  * n_chosen: [n_req]; scores (nullable): [n_req][max_ctx] f32.
  * One fused persistent cooperative launch (page_size 64, head_dim 128, n_extra <= 16,
  * num_heads <= 64 and even, n_req <= 1024; else a two-kernel fallback).  Workspace:
- * kvs_dhd_decode_select_workspace() bytes whose first 4 * (n_req + 3) bytes
- * (work ticket, grid barrier and per-request counters) must be zero before
- * the first call on a buffer and are left zero by every call.              */
+ * kvs_dhd_decode_select_workspace() bytes whose first 4352 bytes (a counter
+ * header of one fixed size: work ticket, grid barrier and per-request
+ * counters for up to 1024 requests) must be zero before the first call on a
+ * buffer and are left zero by every call, of any shape and on either path. */
 size_t kvs_dhd_decode_select_workspace(int32_t n_req, int32_t num_heads, int32_t max_ctx);
 kvs_status kvs_dhd_decode_select(const void *q_t, int32_t num_heads, const int32_t *ctx_len,
                                  int32_t max_ctx, const float *dv_l1, uint8_t *eligible,

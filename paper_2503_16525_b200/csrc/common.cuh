@@ -324,6 +324,7 @@ bool encode_tmap(CUtensorMap *map, CUtensorMapDataType dtype, int rank, void *ga
 bool make_kv_map(CUtensorMap *m, const kvs_kv_arena *a);
 
 // D3 fused decode-stage DHD (decode_dhd.cu), dispatched by kvs_dhd_decode_select.
+size_t d3_counter_bytes();
 size_t d3_fused_workspace(int32_t n_req, int32_t num_heads, int32_t max_ctx);
 bool d3_fused_supported(const kvs_kv_arena *arena, int32_t n_req, int32_t num_heads,
                         int32_t n_extra);

@@ -721,11 +721,17 @@ extern "C" void kvs_d3_trace(unsigned long long *out) {
 
 static inline size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
 
+// The counter header (work ticket, grid barrier, exits, per-request slice
+// counters) has one fixed size for every n_req, and the two-kernel fallback
+// lays its buffers out after it too: a workspace reused across calls of any
+// shape or path keeps the header zero between calls.
+size_t d3_counter_bytes() { return al256(sizeof(int32_t) * ((size_t)d3::kMaxReq + 3)); }
+
 size_t d3_fused_workspace(int32_t n_req, int32_t num_heads, int32_t max_ctx) {
     const size_t ld = ((size_t)max_ctx + 3) & ~(size_t)3;
     const size_t tiles = ((size_t)max_ctx + d3::kTileKeys - 1) / d3::kTileKeys;
     const size_t hp = ((size_t)num_heads + 3) & ~(size_t)3;
-    return al256(sizeof(int32_t) * ((size_t)n_req + 3)) +
+    return d3_counter_bytes() +
            al256(sizeof(float) * (size_t)n_req * hp * ld) +
            al256(sizeof(float2) * (size_t)n_req * tiles * num_heads + 16) +
            al256(sizeof(uint64_t) * (size_t)n_req * 2 * kNumSMs * d3::kMaxK);
@@ -780,7 +786,7 @@ kvs_status d3_fused_launch(const void *q_t, int32_t num_heads, const int32_t *ct
     p.Hp = (num_heads + 3) & ~3;
     char *w = (char *)ws;
     p.ctr = (int32_t *)w;
-    w += al256(sizeof(int32_t) * ((size_t)batch->n_req + 3));
+    w += d3_counter_bytes();
     p.logits = (float *)w;
     w += al256(sizeof(float) * (size_t)batch->n_req * p.Hp * p.ld);
     p.part = (float2 *)w;

@@ -1133,7 +1133,7 @@ kvs_status kvs_dhd_select(const void *v_true, const float *alpha, const int32_t 
 
 size_t kvs_dhd_decode_select_workspace(int32_t n_req, int32_t num_heads, int32_t max_ctx) {
     const size_t tiles = ((size_t)max_ctx + 31) / 32;
-    const size_t two_pass =
+    const size_t two_pass = kvs::d3_counter_bytes() +
         align256(sizeof(float) * (size_t)n_req * num_heads * (((size_t)max_ctx + 3) & ~(size_t)3)) +
         align256(sizeof(float2) * (size_t)n_req * tiles * num_heads);
     const size_t fused = kvs::d3_fused_workspace(n_req, num_heads, max_ctx);
@@ -1163,8 +1163,9 @@ kvs_status kvs_dhd_decode_select(const void *q_t, int32_t num_heads, const int32
         return kvs::d3_fused_launch(q_t, num_heads, ctx_len, max_ctx, dv_l1, eligible, layer, arena,
                                     batch, n_extra, softmax_scale, chosen, n_chosen, scores, ws, s);
     const int chunks = (max_ctx + kDecChunk - 1) / kDecChunk;
-    float *logits = (float *)ws;
-    float2 *part = (float2 *)((char *)ws + align256(sizeof(float) * (size_t)batch->n_req *
+    // after the fused kernel's counter header, which stays zero
+    float *logits = (float *)((char *)ws + kvs::d3_counter_bytes());
+    float2 *part = (float2 *)((char *)logits + align256(sizeof(float) * (size_t)batch->n_req *
                                                      num_heads * (((size_t)max_ctx + 3) & ~(size_t)3)));
     const float scale_log2 = softmax_scale * 1.4426950408889634f;
     const int hq = num_heads / arena->kv_heads;

@@ -95,3 +95,22 @@ def test_decode_select_scores_output():
         want, scores = O.select_decode_step(q_t, k, dv, elig, 7, group=H // G)
         assert_scores_close(res.scores, scores)
         assert_selection_tie_band(res.indices, want, scores, 7)
+
+
+def test_shared_workspace_across_paths():
+    """The fused kernel and the two-kernel fallback (odd head counts) share one
+    workspace: the fallback's buffers sit after the fused kernel's counter
+    header, so a fused call after a fallback call still starts from zeroed
+    counters (regression: the fallback wrote logits over the work ticket)."""
+    import paper_2503_16525_b200 as K
+    rng = np.random.default_rng(11)
+    for H, G, n, n_extra in ((32, 8, 3000, 7), (1, 1, 300, 3), (2, 2, 50, 3),
+                             (3, 1, 900, 5), (4, 4, 64, 2), (28, 4, 777, 3)):
+        q_t = rng.normal(size=(H, 128)) * 0.3
+        k = rng.normal(size=(G, n, 128))
+        dv = rng.normal(size=(G, n, 128)) * 0.1
+        elig = set(rng.choice(n, size=n // 3, replace=False).tolist())
+        res = K.select_decode_step(q_t, k, dv, elig, n_extra)
+        want, scores = O.select_decode_step(q_t, k, dv, elig, n_extra, group=H // G)
+        assert_scores_close(res.scores, scores)
+        assert_selection_tie_band(res.indices, want, scores, n_extra)
