@@ -114,3 +114,48 @@ def test_shared_workspace_across_paths():
         want, scores = O.select_decode_step(q_t, k, dv, elig, n_extra, group=H // G)
         assert_scores_close(res.scores, scores)
         assert_selection_tie_band(res.indices, want, scores, n_extra)
+
+
+def test_engine_workspace_across_batch_sizes():
+    """One engine, one D3 workspace, batches of 100 / 2 / 100 requests: the
+    small batch's logits must not land on the large batch's per-request
+    counters (the counter header has one fixed size)."""
+    import torch
+
+    import paper_2503_16525_b200 as K
+    from paper_2503_16525_b200.engine import Engine
+    from paper_2503_16525_b200.pool import CachePool, KVArena
+    H, G, n_extra = 32, 8, 3
+    cfg = K.ModelConfig(num_layers=2, num_heads=H, num_kv_heads=G, d_model=H * 128,
+                        vocab_size=64, max_positions=512)
+    arena = KVArena(cfg, 2 * 102 * 3 + 8)
+    eng = Engine(K.ToyModel(cfg, init="device"), CachePool(cfg, arena=arena))
+    g = torch.Generator(device="cuda").manual_seed(5)
+    arena.data.copy_((torch.randn(arena.data.shape, generator=g, device="cuda") * 0.5)
+                     .to(torch.bfloat16))
+    rng = np.random.default_rng(5)
+
+    def run(R, ctx):
+        st = eng.new_batch([np.zeros(ctx, dtype=np.int64)] * R, decode_capacity=0)
+        st.ctx_len = np.full(R, ctx, dtype=np.int64)
+        n_tot = R * ctx
+        st.dv_l1 = torch.from_numpy(rng.uniform(0.0, 2.0, n_tot).astype(np.float32)).cuda()
+        elig = (rng.random(n_tot) < 0.3).astype(np.uint8)
+        st.eligible = torch.from_numpy(elig).cuda()
+        q = (torch.randn(R, H, 128, device="cuda") * 0.3).to(torch.bfloat16)
+        chosen = eng.decode_select(st, q, n_extra)
+        qh, dvl = q.double().cpu().numpy(), st.dv_l1.cpu().numpy().astype(np.float64)
+        for r in range(R):
+            a = int(st.req_off_host[r])
+            k = eng.arena.rows(st.pages[r], ctx, 1, 0).double().permute(1, 0, 2).cpu().numpy()
+            dv = np.zeros((G, ctx, 128))
+            dv[0, :, 0] = dvl[a:a + ctx]
+            want, scores = O.select_decode_step(qh[r], k, dv,
+                                                set(np.nonzero(elig[a:a + ctx])[0].tolist()),
+                                                n_extra, group=H // G)
+            assert_selection_tie_band(chosen[r], want, scores, len(want))
+        eng.release(st)
+
+    run(100, 130)
+    run(2, 300)
+    run(100, 130)
